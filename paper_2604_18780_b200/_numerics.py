@@ -1,0 +1,46 @@
+"""Log-domain constants and the instrumentation bundle of the streamcrf API.
+
+Mirrors the public constants of the reference (`pkg/src/streamcrf/_numerics.py:16-23`)
+so callers comparing against the sentinel keep working. The CUDA kernels do
+not use the sentinel internally: they carry IEEE -inf for "no path" and map
+it back to the reference's guard semantics (`max <= NEG_INF + 1` => dead) at
+the boundary (`_numerics.py:59-75`, `streaming.py:194-225`).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+NEG_INF = -1.0e9
+"""Reference sentinel for log(0) (`_numerics.py:18`)."""
+
+CLAMP_LIMIT = 1.0e6
+"""Reference clamp for finite intermediates (`_numerics.py:23`)."""
+
+LOG2E = 1.4426950408889634
+LN2 = 0.6931471805599453
+
+
+@dataclass
+class ClampStats:
+    """Counter kept for API compatibility (`_numerics.py:26-38`).
+
+    The device kernels never clamp finite intermediates (they carry a per-position
+    fp64 normaliser instead), so this counter stays at zero.
+    """
+
+    events: int = 0
+
+    def add(self, n: int) -> None:
+        self.events += int(n)
+
+
+@dataclass
+class RunStats:
+    """Per-call instrumentation bundle (`_numerics.py:104-112`)."""
+
+    clamp: ClampStats = field(default_factory=ClampStats)
+
+    @property
+    def clamp_events(self) -> int:
+        return self.clamp.events
