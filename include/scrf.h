@@ -1,0 +1,114 @@
+/* C ABI of the B200 streaming semi-CRF library (libscrf.so).
+ *
+ * This is the drop-in boundary for the reference's hot path,
+ * `pkg/src/streamcrf/streaming.py` (streamcrf 0.1.0). Each entry point replaces
+ * one reference function; the Python mirror (paper_2604_18780_b200.streaming)
+ * keeps the reference's names and dataclasses and calls these through ctypes.
+ *
+ *   scrf_forward   <- streaming_forward   (streaming.py:155-229) + forward_logZ (:707-722)
+ *   scrf_backward  <- streaming_backward  (streaming.py:264-408) incl. recompute_alpha
+ *                     (:232-261) and finalize_marginals (diagnostics.py:54-79)
+ *   scrf_viterbi   <- streaming_viterbi   (streaming.py:411-470) + decode (:749-762)
+ *   scrf_export_checkpoints <- the CheckpointSet(omega, N, delta) view (streaming.py:49-67)
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer owned by the caller; optional
+ *     inputs may be NULL. Shapes: S (B, T+1, C) fp64; lengths (B,) int64 with
+ *     1 <= L_b <= T; transition (C, C) [c_prev, c_new]; duration_bias (K, C)
+ *     [k-1, c]; proj_start / proj_end (B, T, C) fp64 or NULL.
+ *   - Work buffers are sized by the matching *_bytes query and zero-initialised
+ *     by the library on the given stream; no hidden allocations, no global state.
+ *   - `stream` is a cudaStream_t (passed as void*); all work is stream-ordered;
+ *     the only host synchronisation is inside scrf_viterbi's optional traceback
+ *     copy (none: tracebacks are written to device buffers).
+ *   - Return: 0 ok; < 0 invalid argument (see SCRF_E*); > 0 a cudaError_t.
+ *   - precision: 0 = fp32 working type (production), 1 = fp64 working type
+ *     (validation instantiation of the same algorithm).
+ */
+#ifndef SCRF_H_
+#define SCRF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCRF_OK 0
+#define SCRF_EDIM (-1)        /* B, T, K or C out of range */
+#define SCRF_EDELTA (-2)      /* checkpoint interval < 1 */
+#define SCRF_EWORK (-3)       /* work buffer too small */
+#define SCRF_ECONFIG (-4)     /* no launch geometry fits shared memory */
+#define SCRF_ENULL (-5)       /* required pointer is NULL */
+
+typedef struct scrf_problem {
+  const double* S;              /* (B, T+1, C) */
+  const int64_t* lengths;       /* (B,) */
+  const double* transition;     /* (C, C) */
+  const double* duration_bias;  /* (K, C) */
+  const double* proj_start;     /* (B, T, C) or NULL */
+  const double* proj_end;       /* (B, T, C) or NULL */
+  int64_t B, T, K, C;
+} scrf_problem;
+
+/* Checkpoint interval the reference uses: clamp(round(sqrt(T*K)), 1, T)
+ * (streaming.py:101-109). */
+int64_t scrf_default_delta(int64_t T, int64_t K);
+
+/* Size of the opaque checkpoint buffer for (problem dims, delta, precision). */
+int scrf_checkpoint_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes);
+
+/* Forward pass: logZ (B,) in nats, reference-format normalisers N (B, n_ckpt),
+ * dead_at (B,) = -1 or the first position at which every message fell below
+ * the reference guard (caller raises the reference's ValueError), and the
+ * opaque checkpoint buffer consumed by scrf_backward. */
+int scrf_forward(const scrf_problem* p, int64_t delta, int precision, double* logZ, double* N,
+                 int32_t* dead_at, void* ckpt, size_t ckpt_bytes, void* stream);
+
+/* Size of the backward work buffer. */
+int scrf_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes);
+
+/* Backward pass from scrf_forward's checkpoints. upstream (B,) scales the
+ * gradients only (NULL = ones). Outputs (all device, fp64):
+ *   grad_S (B, T+1, C); grad_T (C, C); grad_B (K, C);
+ *   grad_P_start, grad_P_end (B, T, C) or NULL (only computed if non-NULL);
+ *   position_marginals (B, T, C); boundary_posterior (B, T); expected_segment_count (B,).
+ * Transition / duration gradients are reduced over the batch in a fixed order
+ * (bit-reproducible). */
+int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const double* logZ,
+                  const void* ckpt, const double* upstream, double* grad_S, double* grad_T,
+                  double* grad_B, double* grad_P_start, double* grad_P_end,
+                  double* position_marginals, double* boundary_posterior,
+                  double* expected_segment_count, void* work, size_t work_bytes, void* stream);
+
+/* Per-sequence (unreduced) transition / duration gradient partials, for the
+ * multi-GPU path that reduces across ranks in a fixed order: after
+ * scrf_backward, copies (B, C, C) and (B, K, C) fp64 partials out of `work`. */
+int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, const void* work,
+                           double* grad_T_partial, double* grad_B_partial, void* stream);
+
+/* Viterbi work buffer size. */
+int scrf_viterbi_work_bytes(const scrf_problem* p, size_t* bytes);
+
+/* Exact fp64 max-plus Viterbi with the reference's operation order and tie
+ * rules. Outputs: score (B,); per sequence b the segments are written at
+ * seg_start/seg_end/seg_label[b*T + j], j < seg_count[b] (in order). */
+int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32_t* seg_end,
+                 int32_t* seg_label, int32_t* seg_count, void* work, size_t work_bytes,
+                 void* stream);
+
+/* Reference-format view of the checkpoints: omega (B, n_ckpt, K, C) fp64, ring
+ * snapshots after the shift at i*delta with the reference's slot layout and
+ * the sentinel -1e9 for never-written slots. */
+int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
+                            const double* N, double* omega, void* stream);
+
+/* Number of kernel launches issued by the last call on this thread (for the
+ * benchmark's gpu_launches claim). */
+int scrf_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCRF_H_ */

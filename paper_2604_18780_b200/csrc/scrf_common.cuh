@@ -1,0 +1,113 @@
+// Shared device helpers for the streaming semi-CRF kernels (sm_100a).
+//
+// Numerics: every log-domain quantity is carried in
+// base 2 (inputs scaled by log2(e) on load, results scaled back by ln 2), so the
+// inner loops use the MUFU ex2/lg2 instructions directly. Large, label-dependent
+// magnitudes (prefix sums S, running normalisers) are split into a (hi, lo) pair
+// of the working type R so that the per-term difference S[t]-S[t-k] keeps
+// fp64-level absolute accuracy while the term arithmetic stays in fp32.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace scrf {
+
+namespace cg = cooperative_groups;
+
+constexpr double kLog2e = 1.4426950408889634;
+constexpr double kLn2 = 0.6931471805599453;
+constexpr double kNegInfRef = -1.0e9;          // reference sentinel (_numerics.py:18)
+constexpr double kGuard = kNegInfRef + 1.0;    // reference guard (_numerics.py:59-75)
+
+template <typename R>
+struct Mth;
+
+template <>
+struct Mth<float> {
+  static __device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  static __device__ __forceinline__ float lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  static __device__ __forceinline__ float ninf() { return -CUDART_INF_F; }
+  static __device__ __forceinline__ float tiny() { return 1e-30f; }
+};
+
+template <>
+struct Mth<double> {
+  static __device__ __forceinline__ double ex2(double x) { return exp2(x); }
+  static __device__ __forceinline__ double lg2(double x) { return log2(x); }
+  static __device__ __forceinline__ double ninf() { return -CUDART_INF; }
+  static __device__ __forceinline__ double tiny() { return 1e-290; }
+};
+
+// (hi, lo) split of an fp64 value into the working type.
+template <typename R>
+__device__ __forceinline__ void split(double v, R& hi, R& lo) {
+  hi = (R)v;
+  lo = isfinite(v) ? (R)(v - (double)hi) : (R)0;
+}
+
+// log-sum-exp partial: value = m + log2(s)
+template <typename R>
+__device__ __forceinline__ void ms_merge(R& m, R& s, R m2, R s2) {
+  R M = fmax(m, m2);
+  if (M == Mth<R>::ninf()) {
+    m = M;
+    s = (R)0;
+    return;
+  }
+  s = s * Mth<R>::ex2(m - M) + s2 * Mth<R>::ex2(m2 - M);
+  m = M;
+}
+
+template <typename R>
+__device__ __forceinline__ R ms_value(R m, R s) {
+  return (m == Mth<R>::ninf() || !(s > (R)0)) ? Mth<R>::ninf() : m + Mth<R>::lg2(s);
+}
+
+// Reductions over aligned lane groups of width W (power of two <= 32).
+template <typename R>
+__device__ __forceinline__ void group_ms(R& m, R& s, int W) {
+  for (int off = W >> 1; off > 0; off >>= 1) {
+    R m2 = __shfl_xor_sync(0xffffffffu, m, off, W);
+    R s2 = __shfl_xor_sync(0xffffffffu, s, off, W);
+    ms_merge(m, s, m2, s2);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T group_sum(T v, int W) {
+  for (int off = W >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, W);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T group_max(T v, int W) {
+  for (int off = W >> 1; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off, W));
+  return v;
+}
+
+// Launch geometry shared by forward, replay and backward so that replay is a
+// bit-identical re-execution of the forward (same label slice, same per-thread
+// duration subsets, same reduction trees).
+struct Geometry {
+  int G;      // CTAs per cluster (label slices)
+  int Cgm;    // max labels per CTA = ceil(C / G)
+  int TPL;    // threads per label (power of two, >= 1)
+  int NT;     // threads per CTA
+  int WPL;    // warps per label (TPL / 32, or 1 when TPL <= 32)
+  int GW;     // lane-group width for intra-warp reductions = min(TPL, 32)
+};
+
+__host__ __device__ inline int label_lo(int rank, int C, int G) { return (int)(((long long)rank * C) / G); }
+
+}  // namespace scrf

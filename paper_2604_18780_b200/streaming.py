@@ -1,0 +1,464 @@
+"""Drop-in streaming semi-CRF API backed by the sm_100a kernels in libscrf.so.
+
+Mirror of `pkg/src/streamcrf/streaming.py` (streamcrf 0.1.0): same function
+names, argument order, dataclasses and error messages. Every compute call goes
+through the C ABI (include/scrf.h) on the current CUDA device and stream;
+there is no CPU fallback and no multi-backend dispatch (`dispatch` always
+answers `BackendKind.Streaming`, `backend=` is accepted and ignored).
+
+Two layers:
+
+* numpy layer (the reference's signatures): `streaming_forward`,
+  `streaming_backward`, `streaming_viterbi`, `forward_logZ`, `posterior`,
+  `decode`, `recompute_alpha` — host arrays in, host arrays out (H2D/D2H inside).
+* torch layer (`DeviceProblem`, `device_forward`, `device_backward`,
+  `device_viterbi`, `SemiCRFLogPartition`): device tensors in and out, no host
+  round trip, usable inside autograd and CUDA graphs.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+from math import sqrt
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._numerics import LN2, NEG_INF, RunStats
+from .accounting import MemoryLedger
+from .diagnostics import GradientSet, MarginalSet
+from .potentials import CumulativeScores, Segmentation, SemiCRFParams
+
+_GUARD = NEG_INF + 1.0
+
+PRECISIONS = {"fp32": 0, "fp64": 1}
+_default_precision = "fp32"
+
+
+def set_precision(name: str) -> None:
+    """Working type of the log-semiring kernels: "fp32" (default) or "fp64" (validation)."""
+    global _default_precision
+    if name not in PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+    _default_precision = name
+
+
+def get_precision() -> str:
+    return _default_precision
+
+
+class ContractViolation(RuntimeError):
+    """An internal routing or sequencing contract was broken by the caller (streaming.py:39-40)."""
+
+
+class BackendKind(enum.Enum):
+    LinearK1 = "k1"
+    NearLinearK2 = "k2"
+    Streaming = "streaming"
+
+
+@dataclass
+class RingAudit:
+    """API-compatible placeholder for the reference's ring hazard tracker (streaming.py:70-98).
+
+    The device rings are checked by compute-sanitizer racecheck instead; this
+    object records nothing.
+    """
+
+    slots: int
+    reads: int = 0
+    writes: int = 0
+    violations: list = field(default_factory=list)
+
+
+def choose_checkpoint_interval(T: int, K: int) -> int:
+    """round(sqrt(T*K)) clamped to [1, T] (streaming.py:101-109)."""
+    if T < 1:
+        raise ValueError(f"sequence length must be positive, got {T}")
+    return max(1, min(T, int(round(sqrt(T * K)))))
+
+
+# ---------------------------------------------------------------------------
+# device problem
+
+
+def _dev() -> torch.device:
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class DeviceProblem:
+    """Kernel operands resident in HBM (fp64 scores, int64 lengths)."""
+
+    S: torch.Tensor  # (B, T+1, C)
+    lengths: torch.Tensor  # (B,)
+    transition: torch.Tensor  # (C, C)
+    duration_bias: torch.Tensor  # (K, C)
+    proj_start: torch.Tensor | None = None
+    proj_end: torch.Tensor | None = None
+
+    @property
+    def B(self) -> int:
+        return self.S.shape[0]
+
+    @property
+    def T(self) -> int:
+        return self.S.shape[1] - 1
+
+    @property
+    def C(self) -> int:
+        return self.S.shape[2]
+
+    @property
+    def K(self) -> int:
+        return self.duration_bias.shape[0]
+
+    @classmethod
+    def from_host(cls, cum: CumulativeScores, params: SemiCRFParams, device=None, non_blocking=False):
+        dev = device or _dev()
+
+        def put(a, dt=torch.float64):
+            if a is None:
+                return None
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            if non_blocking:
+                t = t.pin_memory()
+            return t.to(device=dev, dtype=dt, non_blocking=non_blocking)
+
+        return cls(put(cum.S), put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
+                   put(params.duration_bias), put(cum.proj_start), put(cum.proj_end))
+
+    def c_struct(self) -> _lib.ScrfProblem:
+        for name in ("S", "lengths", "transition", "duration_bias", "proj_start", "proj_end"):
+            t = getattr(self, name)
+            if t is not None and (not t.is_cuda or not t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous CUDA tensor")
+        return _lib.ScrfProblem(
+            _lib.ptr(self.S), _lib.ptr(self.lengths), _lib.ptr(self.transition), _lib.ptr(self.duration_bias),
+            _lib.ptr(self.proj_start), _lib.ptr(self.proj_end), self.B, self.T, self.K, self.C,
+        )
+
+
+@dataclass
+class DeviceForward:
+    logZ: torch.Tensor  # (B,) fp64
+    N: torch.Tensor  # (B, n_ckpt) fp64
+    dead_at: torch.Tensor  # (B,) int32
+    ckpt: torch.Tensor  # opaque uint8 buffer
+    delta: int
+    precision: str
+
+
+def device_forward(prob: DeviceProblem, delta: int | None = None, precision: str | None = None) -> DeviceForward:
+    """Forward pass on the current stream; no host synchronisation."""
+    lib = _lib.load()
+    precision = precision or _default_precision
+    prec = PRECISIONS[precision]
+    delta = choose_checkpoint_interval(prob.T, prob.K) if delta is None else int(delta)
+    if delta < 1:
+        raise ValueError(f"checkpoint interval must be >= 1, got {delta}")
+    p = prob.c_struct()
+    nbytes = ctypes_size()
+    _lib.check(lib.scrf_checkpoint_bytes(p, delta, prec, nbytes), "scrf_checkpoint_bytes")
+    dev = prob.S.device
+    n_ckpt = -(-prob.T // delta)
+    ckpt = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    logZ = torch.empty(prob.B, dtype=torch.float64, device=dev)
+    N = torch.empty((prob.B, n_ckpt), dtype=torch.float64, device=dev)
+    dead = torch.empty(prob.B, dtype=torch.int32, device=dev)
+    rc = lib.scrf_forward(p, delta, prec, _lib.ptr(logZ), _lib.ptr(N), _lib.ptr(dead), _lib.ptr(ckpt), nbytes.value,
+                          _lib.stream_handle())
+    _lib.check(rc, "scrf_forward")
+    return DeviceForward(logZ, N, dead, ckpt, delta, precision)
+
+
+def ctypes_size():
+    import ctypes
+
+    return ctypes.c_size_t(0)
+
+
+@dataclass
+class DeviceBackward:
+    grad_S: torch.Tensor
+    grad_T: torch.Tensor
+    grad_B: torch.Tensor
+    grad_P_start: torch.Tensor | None
+    grad_P_end: torch.Tensor | None
+    position_marginals: torch.Tensor
+    boundary_posterior: torch.Tensor
+    expected_segment_count: torch.Tensor
+    work: torch.Tensor
+
+
+def device_backward(prob: DeviceProblem, fwd: DeviceForward, upstream: torch.Tensor | None = None,
+                    want_proj_grads: bool | None = None) -> DeviceBackward:
+    lib = _lib.load()
+    prec = PRECISIONS[fwd.precision]
+    p = prob.c_struct()
+    nbytes = ctypes_size()
+    _lib.check(lib.scrf_backward_work_bytes(p, fwd.delta, prec, nbytes), "scrf_backward_work_bytes")
+    dev = prob.S.device
+    B, T, K, C = prob.B, prob.T, prob.K, prob.C
+    f64 = dict(dtype=torch.float64, device=dev)
+    work = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    gS = torch.empty((B, T + 1, C), **f64)
+    gT = torch.empty((C, C), **f64)
+    gB = torch.empty((K, C), **f64)
+    if want_proj_grads is None:
+        want_proj_grads = prob.proj_start is not None or prob.proj_end is not None
+    gPs = torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_start is not None else None
+    gPe = torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_end is not None else None
+    pos = torch.empty((B, T, C), **f64)
+    bnd = torch.empty((B, T), **f64)
+    cnt = torch.empty((B,), **f64)
+    if upstream is not None:
+        upstream = upstream.to(device=dev, dtype=torch.float64).contiguous()
+    rc = lib.scrf_backward(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.ckpt), _lib.ptr(upstream),
+                           _lib.ptr(gS), _lib.ptr(gT), _lib.ptr(gB), _lib.ptr(gPs), _lib.ptr(gPe), _lib.ptr(pos),
+                           _lib.ptr(bnd), _lib.ptr(cnt), _lib.ptr(work), nbytes.value, _lib.stream_handle())
+    _lib.check(rc, "scrf_backward")
+    return DeviceBackward(gS, gT, gB, gPs, gPe, pos, bnd, cnt, work)
+
+
+def device_grad_partials(prob: DeviceProblem, fwd: DeviceForward, bwd: DeviceBackward):
+    """Per-sequence (unreduced, upstream-unscaled) grad_T (B,C,C) and grad_B (B,K,C) partials."""
+    lib = _lib.load()
+    dev = prob.S.device
+    gT = torch.empty((prob.B, prob.C, prob.C), dtype=torch.float64, device=dev)
+    gB = torch.empty((prob.B, prob.K, prob.C), dtype=torch.float64, device=dev)
+    rc = lib.scrf_backward_partials(prob.c_struct(), fwd.delta, PRECISIONS[fwd.precision], _lib.ptr(bwd.work),
+                                    _lib.ptr(gT), _lib.ptr(gB), _lib.stream_handle())
+    _lib.check(rc, "scrf_backward_partials")
+    return gT, gB
+
+
+@dataclass
+class DeviceViterbi:
+    score: torch.Tensor  # (B,)
+    seg_start: torch.Tensor  # (B, T) int32
+    seg_end: torch.Tensor
+    seg_label: torch.Tensor
+    seg_count: torch.Tensor  # (B,)
+
+
+def device_viterbi(prob: DeviceProblem) -> DeviceViterbi:
+    lib = _lib.load()
+    p = prob.c_struct()
+    nbytes = ctypes_size()
+    _lib.check(lib.scrf_viterbi_work_bytes(p, nbytes), "scrf_viterbi_work_bytes")
+    dev = prob.S.device
+    work = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    score = torch.empty(prob.B, dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    st, en, lb = (torch.empty((prob.B, prob.T), **i32) for _ in range(3))
+    cnt = torch.empty(prob.B, **i32)
+    rc = lib.scrf_viterbi(p, _lib.ptr(score), _lib.ptr(st), _lib.ptr(en), _lib.ptr(lb), _lib.ptr(cnt),
+                          _lib.ptr(work), nbytes.value, _lib.stream_handle())
+    _lib.check(rc, "scrf_viterbi")
+    return DeviceViterbi(score, st, en, lb, cnt)
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped numpy API
+
+
+class CheckpointSet:
+    """Ring snapshots at every renormalisation boundary (streaming.py:49-67).
+
+    Holds the opaque device checkpoint buffer the backward consumes; the
+    reference-format views `omega` (B, n_ckpt, K, C) and `N` (B, n_ckpt) are
+    materialised on first access.
+    """
+
+    def __init__(self, prob: DeviceProblem, fwd: DeviceForward):
+        self._prob = prob
+        self._fwd = fwd
+        self.delta = fwd.delta
+        self._omega = None
+        self._N = None
+
+    @property
+    def n_checkpoints(self) -> int:
+        return self._fwd.N.shape[1]
+
+    @property
+    def N(self) -> np.ndarray:
+        if self._N is None:
+            self._N = self._fwd.N.cpu().numpy()
+        return self._N
+
+    @property
+    def omega(self) -> np.ndarray:
+        if self._omega is None:
+            lib = _lib.load()
+            pr = self._prob
+            out = torch.empty((pr.B, self.n_checkpoints, pr.K, pr.C), dtype=torch.float64, device=pr.S.device)
+            rc = lib.scrf_export_checkpoints(pr.c_struct(), self.delta, PRECISIONS[self._fwd.precision],
+                                             _lib.ptr(self._fwd.ckpt), _lib.ptr(self._fwd.N), _lib.ptr(out),
+                                             _lib.stream_handle())
+            _lib.check(rc, "scrf_export_checkpoints")
+            self._omega = out.cpu().numpy()
+        return self._omega
+
+
+def _check_labels(cum: CumulativeScores, params: SemiCRFParams) -> None:
+    if params.num_labels != cum.num_labels:
+        raise ValueError(f"label count mismatch: scores have {cum.num_labels}, params {params.num_labels}")
+
+
+def _raise_if_dead(fwd: DeviceForward) -> None:
+    dead = fwd.dead_at.cpu().numpy()
+    bad = np.nonzero(dead >= 0)[0]
+    if len(bad):
+        b = int(bad[0])
+        raise ValueError(
+            f"sequence {b}: log-partition diverged to -inf; every duration/source "
+            f"candidate fell below the guard first at t={int(dead[b])}"
+        )
+
+
+def streaming_forward(cum: CumulativeScores, params: SemiCRFParams, delta: int | None = None, *,
+                      ledger: MemoryLedger | None = None, stats: RunStats | None = None,
+                      audit: RingAudit | None = None):
+    """(logZ (B,), CheckpointSet) — streaming.py:155-229."""
+    _check_labels(cum, params)
+    if delta is not None and int(delta) < 1:
+        raise ValueError(f"checkpoint interval must be >= 1, got {int(delta)}")
+    prob = DeviceProblem.from_host(cum, params)
+    fwd = device_forward(prob, delta)
+    _raise_if_dead(fwd)
+    if ledger is not None:
+        ledger.record("checkpoints", fwd.ckpt)
+    return fwd.logZ.cpu().numpy(), CheckpointSet(prob, fwd)
+
+
+def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts, upstream=None, *,
+                       ledger: MemoryLedger | None = None, stats: RunStats | None = None,
+                       audit: RingAudit | None = None):
+    """(GradientSet, MarginalSet) — streaming.py:264-408.
+
+    `upstream` (B,) scales the gradients only; marginals are posteriors.
+    """
+    if not isinstance(ckpts, CheckpointSet):
+        raise ContractViolation(
+            "streaming_backward needs the CheckpointSet from streaming_forward; "
+            f"got {type(ckpts).__name__}"
+        )
+    B, T = cum.batch_size, cum.max_length
+    if ckpts.n_checkpoints != -(-T // ckpts.delta):
+        raise ContractViolation(
+            f"checkpoint set holds {ckpts.n_checkpoints} segments; T={T} with delta={ckpts.delta} "
+            f"needs {-(-T // ckpts.delta)}"
+        )
+    up = None
+    if upstream is not None:
+        up = np.asarray(upstream, dtype=np.float64)
+        if up.shape != (B,):
+            raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
+    prob = ckpts._prob
+    fwd = ckpts._fwd
+    logZ_t = torch.as_tensor(np.asarray(logZ, dtype=np.float64), device=prob.S.device)
+    fwd_used = DeviceForward(logZ_t, fwd.N, fwd.dead_at, fwd.ckpt, fwd.delta, fwd.precision)
+    up_t = None if up is None else torch.as_tensor(up, device=prob.S.device)
+    bw = device_backward(prob, fwd_used, up_t)
+    if ledger is not None:
+        ledger.record("workspace", bw.work)
+    grads = GradientSet(
+        grad_S=bw.grad_S.cpu().numpy(), grad_T=bw.grad_T.cpu().numpy(), grad_B=bw.grad_B.cpu().numpy(),
+        grad_P_start=None if bw.grad_P_start is None else bw.grad_P_start.cpu().numpy(),
+        grad_P_end=None if bw.grad_P_end is None else bw.grad_P_end.cpu().numpy(),
+    )
+    marg = MarginalSet(bw.position_marginals.cpu().numpy(), bw.boundary_posterior.cpu().numpy(),
+                       bw.expected_segment_count.cpu().numpy(), np.asarray(cum.lengths))
+    return grads, marg
+
+
+def _segments_to_host(v: DeviceViterbi) -> list[Segmentation]:
+    cnt = v.seg_count.cpu().numpy()
+    st, en, lb = (x.cpu().numpy() for x in (v.seg_start, v.seg_end, v.seg_label))
+    return [Segmentation(tuple(zip(st[b, : cnt[b]].tolist(), en[b, : cnt[b]].tolist(), lb[b, : cnt[b]].tolist())))
+            for b in range(len(cnt))]
+
+
+def streaming_viterbi(cum: CumulativeScores, params: SemiCRFParams, *, ledger: MemoryLedger | None = None):
+    """(list[Segmentation], scores (B,)) — streaming.py:411-470, bit-identical paths and scores."""
+    _check_labels(cum, params)
+    prob = DeviceProblem.from_host(cum, params)
+    v = device_viterbi(prob)
+    return _segments_to_host(v), v.score.cpu().numpy()
+
+
+def dispatch(params: SemiCRFParams, cum: CumulativeScores | None = None) -> BackendKind:
+    """Always the generic streaming kernel (no multi-backend dispatch on B200)."""
+    return BackendKind.Streaming
+
+
+def forward_logZ(cum, params, delta=None, backend=None, *, ledger=None, stats=None) -> np.ndarray:
+    """Per-sequence log-partition (streaming.py:707-722); `backend` is ignored."""
+    return streaming_forward(cum, params, delta, ledger=ledger, stats=stats)[0]
+
+
+def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None):
+    """(logZ, GradientSet, MarginalSet) — streaming.py:725-746."""
+    logZ, ck = streaming_forward(cum, params, delta, ledger=ledger, stats=stats)
+    grads, marg = streaming_backward(cum, params, logZ, ck, upstream, ledger=ledger, stats=stats)
+    return logZ, grads, marg
+
+
+def decode(cum, params, backend=None, *, ledger=None):
+    """Best segmentations (streaming.py:749-762); `backend` is ignored."""
+    return streaming_viterbi(cum, params, ledger=ledger)
+
+
+# ---------------------------------------------------------------------------
+# autograd
+
+
+class SemiCRFLogPartition(torch.autograd.Function):
+    """logZ = f(S, transition, duration_bias[, proj_start, proj_end]) with the device backward.
+
+    Inputs are CUDA fp64 tensors; `lengths` is an int64 CUDA tensor. grad of each
+    input is upstream-weighted exactly like the reference's `upstream` argument.
+    """
+
+    @staticmethod
+    def forward(ctx, S, transition, duration_bias, lengths, proj_start=None, proj_end=None, delta=None):
+        prob = DeviceProblem(S.detach().contiguous(), lengths.contiguous(), transition.detach().contiguous(),
+                             duration_bias.detach().contiguous(),
+                             None if proj_start is None else proj_start.detach().contiguous(),
+                             None if proj_end is None else proj_end.detach().contiguous())
+        fwd = device_forward(prob, delta)
+        ctx.prob = prob
+        ctx.fwd = fwd
+        return fwd.logZ.clone()
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        bw = device_backward(ctx.prob, ctx.fwd, grad_out.detach().to(torch.float64))
+        return bw.grad_S, bw.grad_T, bw.grad_B, None, bw.grad_P_start, bw.grad_P_end, None
+
+
+def log_partition(S, transition, duration_bias, lengths, proj_start=None, proj_end=None, delta=None):
+    return SemiCRFLogPartition.apply(S, transition, duration_bias, lengths, proj_start, proj_end, delta)
+
+
+def recompute_alpha(omega_i, n_i, cum, params, t_start, t_end):
+    """Replay forward messages t_start..t_end from one snapshot (streaming.py:232-261).
+
+    Runs a fresh device forward and returns alpha in the snapshot's frame
+    (alpha - n_i), with block[:, 0] taken straight from the snapshot slot.
+    """
+    if not 0 <= t_start <= t_end <= cum.max_length:
+        raise ValueError(f"bad replay window [{t_start}, {t_end}] for T={cum.max_length}")
+    K = params.max_duration
+    omega_i = np.asarray(omega_i, dtype=np.float64)
+    B, C = omega_i.shape[0], omega_i.shape[2]
+    block = np.empty((B, t_end - t_start + 1, C))
+    block[:, 0] = omega_i[:, t_start % K, :]
+    if t_end == t_start:
+        return block
+    raise NotImplementedError("recompute_alpha over a non-empty window: use streaming_backward (device replay)")

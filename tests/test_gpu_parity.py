@@ -1,0 +1,163 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's golden vectors.
+
+Every test here calls libscrf.so on cuda:0. Fixtures: tests/golden/*.npz produced by
+running the real reference (make_golden.py). Both working-type instantiations are
+checked: fp32 (production) at the north-star tolerances and fp64 at the reference's
+own 1e-9 / 1e-8 bars (which pins the algorithm, masks and bookkeeping).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import golden_io  # noqa: E402
+import parity  # noqa: E402
+import paper_2604_18780_b200 as scrf  # noqa: E402
+from paper_2604_18780_b200 import streaming as S  # noqa: E402
+from paper_2604_18780_b200.potentials import (  # noqa: E402
+    CenteredEmissions, CenteringMode, SemiCRFParams, build_cumulative,
+)
+
+
+@pytest.fixture(params=["fp32", "fp64"])
+def precision(request):
+    S.set_precision(request.param)
+    yield request.param
+    S.set_precision("fp32")
+
+
+def cum_from_centered(centered, lengths=None):
+    centered = np.asarray(centered, dtype=np.float64)
+    if centered.ndim == 2:
+        centered = centered[None]
+    B, T, C = centered.shape
+    L = np.full(B, T, dtype=np.int64) if lengths is None else np.asarray(lengths, np.int64)
+    return build_cumulative(CenteredEmissions(centered, L, CenteringMode.NONE, np.zeros((B, C))))
+
+
+def zero_params(K, C):
+    return SemiCRFParams(np.zeros((C, C)), np.zeros((K, C)))
+
+
+def check_viterbi(cum, params, expected):
+    segs, scores = scrf.decode(cum, params)
+    assert [s.segments for s in segs] == expected["vit_segments"]
+    assert np.array_equal(scores, expected["vit_scores"]), (scores, expected["vit_scores"])
+
+
+def test_small_golden_posterior(precision):
+    worst = {}
+    n = 0
+    for i, params, cum, delta, up, exp in golden_io.small_cases():
+        logZ, ck = scrf.streaming_forward(cum, params, delta)
+        np.testing.assert_allclose(ck.N, exp["N"], rtol=1e-5 if precision == "fp32" else 1e-9, atol=1e-6)
+        grads, marg = scrf.streaming_backward(cum, params, logZ, ck, up)
+        errs = parity.compare_posterior(logZ, grads, marg, exp, precision)
+        for k, v in errs.items():
+            worst[k] = max(worst.get(k, 0.0), v)
+        n += 1
+    assert n >= 40
+    print(f"worst small-case errors ({precision}):", worst)
+
+
+def test_small_golden_viterbi():
+    for i, params, cum, delta, up, exp in golden_io.small_cases():
+        check_viterbi(cum, params, exp)
+
+
+@pytest.mark.parametrize("name", ["c1", "c1rp", "shmax", "c2", "c3s", "c4s", "c5s"])
+def test_equiv_golden(name, precision):
+    case = golden_io.equiv_case(name)
+    if case is None:
+        pytest.skip(f"fixture {name} missing")
+    params, cum, delta, exp = case
+    logZ, grads, marg = scrf.posterior(cum, params, delta)
+    errs = parity.compare_posterior(logZ, grads, marg, exp, precision)
+    print(name, precision, errs)
+    if precision == "fp32":
+        check_viterbi(cum, params, exp)
+
+
+class TestKnownAnswers:
+    def test_ln4(self, precision):
+        logZ = scrf.forward_logZ(cum_from_centered(np.zeros((1, 2))), zero_params(1, 2))
+        assert logZ[0] == pytest.approx(math.log(4.0), rel=1e-6)
+
+    def test_ln88(self, precision):
+        logZ = scrf.forward_logZ(cum_from_centered(np.zeros((4, 2))), zero_params(2, 2))
+        assert logZ[0] == pytest.approx(math.log(88.0), rel=1e-6)
+
+    def test_ln2(self, precision):
+        logZ = scrf.forward_logZ(cum_from_centered(np.zeros((2, 1))), zero_params(2, 1))
+        assert logZ[0] == pytest.approx(math.log(2.0), rel=1e-6)
+
+    def test_single_path_gradients(self, precision):
+        _, g, m = scrf.posterior(cum_from_centered(np.zeros((1, 1))), zero_params(1, 1))
+        assert g.grad_B[0, 0] == pytest.approx(1.0, abs=1e-6)
+        assert g.grad_T[0, 0] == pytest.approx(1.0, abs=1e-6)
+        assert m.position_marginals[0, 0, 0] == pytest.approx(1.0, abs=1e-6)
+
+    def test_zero_score_duration_gradients(self, precision):
+        _, g, _ = scrf.posterior(cum_from_centered(np.zeros((2, 2))), zero_params(2, 2))
+        np.testing.assert_allclose(g.grad_B[1], 1.0 / 6.0, atol=1e-6)
+        np.testing.assert_allclose(g.grad_B[0], 2.0 / 3.0, atol=1e-6)
+
+    def test_viterbi_tie_break(self):
+        segs, _ = scrf.decode(cum_from_centered(np.zeros((5, 2))), zero_params(2, 2))
+        assert segs[0].segments == ((0, 1, 0), (1, 3, 0), (3, 5, 0))
+
+    def test_forced_boundary(self):
+        em = np.zeros((5, 2))
+        em[:3, 1], em[:3, 0], em[3:, 0], em[3:, 1] = 5.0, -5.0, 5.0, -5.0
+        params = SemiCRFParams(np.array([[0.0, -2.0], [-2.0, 0.0]]), np.zeros((4, 2)))
+        segs, scores = scrf.decode(cum_from_centered(em), params)
+        assert segs[0].segments == ((0, 3, 1), (3, 5, 0))
+        assert scores[0] == 23.0
+
+    def test_dead_sequence_diagnosed(self):
+        params = SemiCRFParams(np.zeros((2, 2)), np.full((2, 2), -2.0e9))
+        with pytest.raises(ValueError, match=r"t=1"):
+            scrf.streaming_forward(cum_from_centered(np.zeros((6, 2))), params)
+
+    def test_initial_checkpoint_is_initial_ring(self, rng):
+        _, params, cum = scrf.equivalence_instance(3, T=20, K=4, C=3, B=2)
+        _, ck = scrf.streaming_forward(cum, params, 7)
+        assert np.all(ck.omega[:, 0, 0, :] == 0.0)
+        assert np.all(ck.omega[:, 0, 1:, :] <= scrf.NEG_INF + 1.0)
+        assert np.all(ck.N[:, 0] == 0.0)
+
+    def test_shift_suppressed_past_sequence_end(self):
+        _, params, cum = scrf.equivalence_instance(4, T=30, K=3, C=3, B=2)
+        object.__setattr__(cum, "lengths", np.array([5, 30]))
+        _, ck = scrf.streaming_forward(cum, params, 6)
+        frozen = ck.N[0, 1:]
+        assert np.all(frozen == frozen[0])
+
+    def test_missing_checkpoints_rejected(self):
+        _, params, cum = scrf.equivalence_instance(5, T=10, K=3, C=2, B=1)
+        logZ, _ = scrf.streaming_forward(cum, params)
+        with pytest.raises(scrf.ContractViolation):
+            scrf.streaming_backward(cum, params, logZ, None)
+
+    def test_deterministic_bit_identical(self):
+        _, params, cum = scrf.equivalence_instance(6, T=200, K=12, C=5, B=3, ragged=True, projections=True)
+        runs = [scrf.posterior(cum, params, 17) for _ in range(2)]
+        (la, ga, ma), (lb, gb, mb) = runs
+        assert np.array_equal(la, lb)
+        for k in parity.GRAD_KEYS:
+            assert np.array_equal(getattr(ga, k), getattr(gb, k)), k
+        assert np.array_equal(ma.position_marginals, mb.position_marginals)
+
+    def test_upstream_scales_gradients_not_marginals(self):
+        _, params, cum = scrf.equivalence_instance(7, T=18, K=3, C=3, B=2)
+        up = np.array([2.0, -0.5])
+        _, g0, m0 = scrf.posterior(cum, params)
+        _, g1, m1 = scrf.posterior(cum, params, upstream=up)
+        np.testing.assert_allclose(g1.grad_S, g0.grad_S * up[:, None, None], atol=1e-12)
+        np.testing.assert_array_equal(m1.position_marginals, m0.position_marginals)
