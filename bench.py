@@ -1,0 +1,405 @@
+"""Benchmark: streaming semi-CRF forward+backward positions/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+
+One step = one full forward + backward (logZ, all gradients, all marginals) of the
+batch of BASELINE.json config 4 (B=8, T=100000, K=1000, C=24; synthetic instance
+`equivalence_instance(seed=rank, ..., mode=MEAN)`), followed — for N > 1 — by the
+only cross-GPU exchange of the path: the fixed-rank-order reduction of the shared
+transition / duration gradients over NCCL. Weak scaling: every rank owns its own
+B=8 batch. `value` = all ranks' positions / max-over-ranks device time.
+
+`e2e` = the same metric through the public numpy API (`posterior`) with host inputs
+and host outputs (H2D of S and parameters, D2H of logZ, gradients, marginals) inside
+the timed region. `--impl reference` times the CPU oracle port of the reference
+algorithm (oracle/streaming_oracle.py) on the host cores.
+
+The inputs (S: 8 x 100001 x 24 fp64 = 154 MB) are larger than the 126 MB L2, so no
+explicit flush is done between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "positions/sec (B*T) for fwd+bwd at T=100k,K=1000,C=24"
+UNIT = "positions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time forward-only and Viterbi")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm, steady-state sample
+
+
+def _cpu_worker(args):
+    cfg, seed, n_steps = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import streaming_oracle as oracle
+
+    from paper_2604_18780_b200.instances import equivalence_instance
+    from paper_2604_18780_b200.potentials import CenteringMode
+
+    K = cfg["K"]
+    _, params, cum = equivalence_instance(seed, T=K + n_steps + 2, K=K, C=cfg["C"], B=1, mode=CenteringMode.MEAN)
+    return oracle.steady_position_seconds(cum, params, n_steps)
+
+
+def cpu_baseline(cfg: dict, budget_s: float) -> dict:
+    """positions/s of the reference algorithm (oracle port) on all host cores.
+
+    Each core runs one sequence's steady-state forward + replay + backward
+    positions (t >= K, every duration live); per-position cost is constant there,
+    so rate = cores / seconds-per-position (SURVEY §6.2 method).
+    """
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    workers = max(1, min(cores, cfg["B"] if cfg["B"] > 1 else cores))
+    # calibrate the number of sampled positions to the time budget
+    probe = _cpu_worker((cfg, 0, 2))
+    n_steps = int(max(2, min(200, budget_s / max(probe, 1e-6) / 1.5)))
+    with mp.get_context("spawn").Pool(workers) as pool:
+        t0 = time.perf_counter()
+        secs = pool.map(_cpu_worker, [(cfg, s, n_steps) for s in range(workers)])
+        wall = time.perf_counter() - t0
+    per_pos = float(np.mean(secs))
+    value = workers / per_pos
+    return {
+        "value": value,
+        "unit": UNIT,
+        "cores": workers,
+        "kind": "port",
+        "sample": (f"oracle/streaming_oracle.py (reference algorithm, fp64 numpy) steady-state fwd+replay+bwd "
+                   f"positions t>=K at K={cfg['K']}, C={cfg['C']}: {n_steps} positions per core on {workers} "
+                   f"processes x 1 sequence, {wall:.1f}s wall; value = cores / mean s-per-position"),
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 7:
+                for n, v in zip(names, s[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def mufu_peak_per_s(sm_mhz: float | None) -> tuple[float, str]:
+    """MUFU ex2 peak = 148 SMs x 16 / clk x f_SM (16/clk/SM measured: profiles/r01_microbench.jsonl)."""
+    peaks = measured_peaks()
+    mhz = sm_mhz or peaks.get("sm_max_mhz", 1965.0)
+    return 148 * 16 * mhz * 1e6, f"148 SM x 16 ex2/clk (microbenchmarked) x {mhz:.0f} MHz (median SM clock in the timed region)"
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_2604_18780_b200 as scrf
+    from paper_2604_18780_b200 import _lib
+    from paper_2604_18780_b200 import streaming as S
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    S.set_precision(args.precision)
+    cfg = dict(CONFIGS[args.config])
+    B, T, K, C = cfg["B"], cfg["T"], cfg["K"], cfg["C"]
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    # synthetic instance of the config's shape (per-rank seed: weak scaling)
+    _, params, cum = scrf.equivalence_instance(rank, T=T, K=K, C=C, B=B, mode=scrf.CenteringMode.MEAN)
+    prob = scrf.DeviceProblem.from_host(cum, params, device=dev)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+
+    ev_main = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    bwd_ms, fwd_ms = [], []
+    launches = [0]
+
+    def exchange(fwd, bw):
+        # the path's only collective: fixed-order sum of per-rank grad_T / grad_B partials
+        if dist is None:
+            return bw.grad_T, bw.grad_B
+        flat = torch.cat([bw.grad_T.reshape(-1), bw.grad_B.reshape(-1)])
+        gathered = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(gathered, flat)
+        tot = gathered[0].clone()
+        for g in gathered[1:]:
+            tot += g
+        return tot[: C * C].view(C, C), tot[C * C:].view(K, C)
+
+    def step(record: bool):
+        st = torch.cuda.current_stream()
+        if record:
+            lib.scrf_profile_events(ev_main[0].cuda_event, ev_main[1].cuda_event)
+        fwd = S.device_forward(prob)
+        n = lib.scrf_last_launch_count()
+        if record:
+            torch.cuda.synchronize()
+            fwd_ms.append(ev_main[0].elapsed_time(ev_main[1]))
+        bw = S.device_backward(prob, fwd)
+        n += lib.scrf_last_launch_count()
+        if record:
+            lib.scrf_profile_events(None, None)
+        exchange(fwd, bw)
+        launches[0] += n
+        return bw
+
+    # warmup
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+
+    # live kernel timing pass (events around the forward and the backward main kernels)
+    for _ in range(min(2, args.steps)):
+        lib.scrf_profile_events(ev_main[0].cuda_event, ev_main[1].cuda_event)
+        fwd = S.device_forward(prob)
+        lib.scrf_profile_events(None, None)
+        torch.cuda.synchronize()
+        fwd_ms.append(ev_main[0].elapsed_time(ev_main[1]))
+        lib.scrf_profile_events(ev_main[0].cuda_event, ev_main[1].cuda_event)
+        S.device_backward(prob, fwd)
+        lib.scrf_profile_events(None, None)
+        torch.cuda.synchronize()
+        bwd_ms.append(ev_main[0].elapsed_time(ev_main[1]))
+
+    launches[0] = 0
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_stop = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        t_start.record()
+        for _ in range(args.steps):
+            step(False)
+        t_stop.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_stop) / args.steps
+    if dist is not None:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    positions = world * B * T
+    value = positions / (ms / 1e3)
+    clocks = sampler.summary()
+    peak_mem = torch.cuda.max_memory_allocated(dev)
+
+    out = None
+    if rank == 0:
+        # roofline of the dominant kernel (the backward cluster kernel: replay + beta + marginals)
+        E_bwd = 3 * (K * C + C * C)  # exps per position executed by bwd_kernel (replay KC+C^2, delta KC, M KC, beta C^2, grad_T C^2)
+        E_fwd = K * C + C * C
+        bwd_avg = float(np.mean(bwd_ms))
+        fwd_avg = float(np.mean(fwd_ms))
+        peak, peak_note = mufu_peak_per_s(clocks["sm_mhz"])
+        achieved = B * T * E_bwd / (bwd_avg / 1e3)
+        step_ach = value / world * (E_bwd + E_fwd)
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32 log-semiring (fp64 prefix sums / normalisers; fp64 outputs)" if args.precision == "fp32" else "f64",
+            "data": "synthetic: equivalence_instance(seed=rank, mode=MEAN) of config 4, per-rank batch",
+            "config": {
+                "workload": f"BASELINE config 4 fwd+bwd (logZ, grad_S/T/B, marginals), B={B} T={T} K={K} C={C} per GPU",
+                "B_per_gpu": B, "T": T, "K": K, "C": C, "delta": S.choose_checkpoint_interval(T, K),
+                "parallelism": f"batch-sharded dp{world}; grad_T/grad_B fixed-order all_gather-sum over NCCL",
+                "l2": "inputs larger than L2 (S = 154 MB fp64 per GPU); no flush",
+            },
+            "roofline": {
+                "bound": "sfu",
+                "kernel": "bwd_kernel (alpha replay + beta sweep + marginals/gradients)",
+                "achieved": achieved / 1e9,
+                "peak": peak / 1e9,
+                "unit": "Gexp2/s",
+                "frac": achieved / peak,
+                "traffic": None,
+                "algorithm": "factored: per position fwd K*C+C^2, bwd 3*(K*C+C^2) ex2 (SURVEY §8d counts 4*(K*C+C^2) fwd+bwd)",
+                "per_launch_exps": B * T * E_bwd,
+                "kernel_ms": bwd_avg,
+                "fwd_kernel_ms": fwd_avg,
+                "step_sfu_frac": step_ach / peak,
+                "peak_note": peak_note,
+            },
+            "clocks": clocks,
+            "peak_hbm_bytes": int(peak_mem),
+            "gpu_launches": int(launches[0]),
+        }
+    return out, (prob, cum, params, cfg, dev, lib, S, scrf, torch, dist)
+
+
+def e2e_measure(ctx, args):
+    """The public numpy API end to end: host arrays in, host arrays out."""
+    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist = ctx
+    B, T, K, C = cfg["B"], cfg["T"], cfg["K"], cfg["C"]
+    scrf.posterior(cum, params)  # warm
+    torch.cuda.synchronize()
+    n = max(1, min(3, args.steps))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        logZ, grads, marg = scrf.posterior(cum, params)
+    wall = (time.perf_counter() - t0) / n
+    h2d = cum.S.nbytes + np.asarray(cum.lengths).nbytes + params.transition.nbytes + params.duration_bias.nbytes
+    d2h = (logZ.nbytes + grads.grad_S.nbytes + grads.grad_T.nbytes + grads.grad_B.nbytes
+           + marg.position_marginals.nbytes + marg.boundary_posterior.nbytes + marg.expected_segment_count.nbytes
+           + B * 4 + B * 8 * (-(-T // S.choose_checkpoint_interval(T, K))))
+    return {"value": B * T / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "paper_2604_18780_b200.posterior (numpy in / numpy out, host wall clock)", "steps": n}
+
+
+def extras_measure(ctx, args):
+    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist = ctx
+    B, T = cfg["B"], cfg["T"]
+    res = {}
+    for name, fn in (("forward", lambda: S.device_forward(prob)), ("viterbi", lambda: S.device_viterbi(prob))):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        reps = 2
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        res[name + "_positions_per_s"] = B * T / (a.elapsed_time(b) / reps / 1e3)
+    return res
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        cb = cpu_baseline(cfg, args.cpu_seconds)
+        line = {
+            "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": cfg["B"] * cfg["T"] / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 4 fwd+bwd, B={cfg['B']} T={cfg['T']} K={cfg['K']} C={cfg['C']}",
+                       "note": "CPU time per position measured in steady state and scaled to the config"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    out, ctx = run_ours(args, rank, world, local)
+    if rank == 0:
+        if not args.no_e2e and world == 1:
+            out["e2e"] = e2e_measure(ctx, args)
+        elif not args.no_e2e:
+            out["e2e"] = None
+        if args.extras:
+            out["extras"] = extras_measure(ctx, args)
+        if not args.no_cpu and world == 1:
+            out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+        print(json.dumps(out), flush=True)
+    dist = ctx[-1]
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

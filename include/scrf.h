@@ -108,6 +108,12 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
  * benchmark's gpu_launches claim). */
 int scrf_last_launch_count(void);
 
+/* Record the given cudaEvent_t pair (or NULL, NULL to disable) immediately before and
+ * after the main cluster kernel of every subsequent scrf_forward / scrf_backward /
+ * scrf_viterbi call on this thread, on the call's stream. Used by bench.py to time the
+ * dominant kernel live (no profiler). */
+void scrf_profile_events(void* start, void* stop);
+
 #ifdef __cplusplus
 }
 #endif

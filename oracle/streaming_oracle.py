@@ -177,6 +177,93 @@ def finalize_marginals(coverage_diff, boundary, total_mass, lengths):
     return pos, bnd, np.asarray(total_mass, dtype=np.float64)
 
 
+@dataclass
+class _BwdState:
+    beta: np.ndarray
+    work: np.ndarray
+    gS: np.ndarray
+    gPs: np.ndarray | None
+    gPe: np.ndarray | None
+    cov: np.ndarray
+    bnd: np.ndarray
+    mass: np.ndarray
+    scale: np.ndarray
+    L: np.ndarray
+    R: int
+    proj: bool
+
+
+def _beta_step(st: _BwdState, cum, params, t: int, i: int, alpha_t: np.ndarray, shift: np.ndarray) -> None:
+    """One backward position: beta[t], joint marginals of segments starting at t (streaming.py:337-387)."""
+    B, T, C = cum.S.shape[0], cum.S.shape[1] - 1, cum.S.shape[2]
+    K = params.max_duration
+    trans = params.transition
+    ks = np.arange(1, min(K, T - t) + 1)
+    h = cum.S[:, t + ks, :] - cum.S[:, t, None, :] + params.duration_bias[None, : len(ks), :]
+    if st.proj:
+        h = h + cum.proj_start[:, None, t, :] + cum.proj_end[:, t + ks - 1, :]
+    h = clamp_log(h)
+    hb = h + st.beta[(t + ks) % st.R].transpose(1, 0, 2)  # (B, kmax, C)
+    ok = (t + ks)[None, :] <= st.L[:, None]
+    hb = np.where(ok[:, :, None], hb, NEG_INF)
+    q = hb[:, :, None, :] + trans[None, None]  # (B, kmax, C', C)
+    nb = lse(q.transpose(0, 2, 1, 3).reshape(B, C, len(ks) * C), axis=2)
+    lm = hb[:, :, :, None] + trans.T[None, None] + alpha_t[:, None, None, :]
+    lm = lm + shift[:, None, None, None]
+    np.clip(lm, -80.0, 80.0, out=lm)
+    mu = np.where(ok[:, :, None, None], np.exp(lm), 0.0)
+    mug = mu * st.scale[:, None, None, None]
+    st.work[:, i, : len(ks)] += mug
+    post = mu.sum(axis=3)
+    grad = mug.sum(axis=3)
+    st.gS[:, t, :] -= grad.sum(axis=1)
+    st.gS[:, t + ks, :] += grad
+    if st.proj:
+        st.gPs[:, t, :] += grad.sum(axis=1)
+        st.gPe[:, t + ks - 1, :] += grad
+    st.cov[:, t, :] += post.sum(axis=1)
+    st.cov[:, t + ks, :] -= post
+    s0 = post.sum(axis=(1, 2))
+    st.bnd[:, t] += s0
+    st.mass += s0
+    w = t < st.L
+    st.beta[t % st.R] = np.where(w[:, None], clamp_log(nb), st.beta[t % st.R])
+
+
+def steady_position_seconds(cum, params, n_steps: int = 8) -> float:
+    """CPU seconds per position of fwd + replay + bwd in steady state (t >= K, t + K <= T).
+
+    Times the oracle's own per-position bodies (`_alpha_step`, `_beta_step`) on a
+    primed state; per-position cost is value-independent once t >= K (numpy
+    does the same work), which is how BASELINE.md §4 extrapolates c4/c5.
+    """
+    import time
+
+    B, T, C = cum.S.shape[0], cum.S.shape[1] - 1, cum.S.shape[2]
+    K = params.max_duration
+    ring = np.zeros((K, B, C))
+    t_lo = K
+    if K + n_steps + 1 > T:
+        raise ValueError("instance too short for a steady-state sample")
+    t0 = time.perf_counter()
+    for t in range(t_lo + 1, t_lo + 1 + n_steps):
+        ring[t % K] = _alpha_step(ring, t, cum, params)
+    t_fwd = (time.perf_counter() - t0) / n_steps
+    R = 2 * K
+    st = _BwdState(np.zeros((R, B, C)), np.zeros((B, 1, K, C, C)), np.zeros((B, T + 1, C)), None, None,
+                   np.zeros((B, T + 1, C)), np.zeros((B, T)), np.zeros(B), np.ones(B),
+                   np.asarray(cum.lengths), R, cum.proj_start is not None)
+    if st.proj:
+        st.gPs, st.gPe = np.zeros((B, T, C)), np.zeros((B, T, C))
+    alpha_t = np.zeros((B, C))
+    shift = np.zeros(B)
+    t0 = time.perf_counter()
+    for t in range(n_steps, 0, -1):  # t + K <= T: every duration is live
+        _beta_step(st, cum, params, t, 0, alpha_t, shift)
+    t_bwd = (time.perf_counter() - t0) / n_steps
+    return 2.0 * t_fwd + t_bwd  # forward + replay + backward per position (B sequences)
+
+
 def backward(cum, params, logZ, ckpts: Checkpoints, upstream=None) -> dict:
     """Gradients + marginals by checkpointed replay (streaming.py:264-408).
 
@@ -208,41 +295,13 @@ def backward(cum, params, logZ, ckpts: Checkpoints, upstream=None) -> dict:
     bnd = np.zeros((B, T))
     mass = np.zeros(B)
 
+    st = _BwdState(beta, work, gS, gPs, gPe, cov, bnd, mass, scale, L, R, proj)
     for i in range(n_ckpt - 1, -1, -1):
         t0, t1 = i * delta, min((i + 1) * delta, T)
         alpha = replay(ckpts.omega[:, i], cum, params, t0, t1)
         shift = ckpts.N[:, i] - logZ
         for t in range(t1 - 1, t0 - 1, -1):
-            ks = np.arange(1, min(K, T - t) + 1)
-            h = cum.S[:, t + ks, :] - cum.S[:, t, None, :] + params.duration_bias[None, : len(ks), :]
-            if proj:
-                h = h + cum.proj_start[:, None, t, :] + cum.proj_end[:, t + ks - 1, :]
-            h = clamp_log(h)
-            hb = h + beta[(t + ks) % R].transpose(1, 0, 2)  # (B, kmax, C)
-            ok = (t + ks)[None, :] <= L[:, None]
-            hb = np.where(ok[:, :, None], hb, NEG_INF)
-            q = hb[:, :, None, :] + trans[None, None]  # (B, kmax, C', C)
-            nb = lse(q.transpose(0, 2, 1, 3).reshape(B, C, len(ks) * C), axis=2)
-            lm = hb[:, :, :, None] + trans.T[None, None] + alpha[:, t - t0][:, None, None, :]
-            lm = lm + shift[:, None, None, None]
-            np.clip(lm, -80.0, 80.0, out=lm)
-            mu = np.where(ok[:, :, None, None], np.exp(lm), 0.0)
-            mug = mu * scale[:, None, None, None]
-            work[:, i, : len(ks)] += mug
-            post = mu.sum(axis=3)
-            grad = mug.sum(axis=3)
-            gS[:, t, :] -= grad.sum(axis=1)
-            gS[:, t + ks, :] += grad
-            if proj:
-                gPs[:, t, :] += grad.sum(axis=1)
-                gPe[:, t + ks - 1, :] += grad
-            cov[:, t, :] += post.sum(axis=1)
-            cov[:, t + ks, :] -= post
-            st = post.sum(axis=(1, 2))
-            bnd[:, t] += st
-            mass += st
-            w = t < L
-            beta[t % R] = np.where(w[:, None], clamp_log(nb), beta[t % R])
+            _beta_step(st, cum, params, t, i, alpha[:, t - t0], shift)
 
     gT = np.zeros((C, C))
     gB = np.zeros((K, C))

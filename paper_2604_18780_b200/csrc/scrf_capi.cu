@@ -16,6 +16,9 @@ using namespace scrf;
 namespace {
 
 thread_local int g_launches = 0;
+// optional events recorded around the next main kernel launch (forward / backward / Viterbi)
+thread_local cudaEvent_t g_ev_start = nullptr;
+thread_local cudaEvent_t g_ev_stop = nullptr;
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -155,13 +158,13 @@ CkLayout ck_layout(const scrf_problem* p, int64_t delta, int precision) {
   L.g_lo = o;
   o += al(ring * rs);
   L.alpha = o;
-  o += al(ring * 4);
+  o += al(ring * rs);
   L.n = o;
   o += al((size_t)p->B * nck * p->K * 8);
   L.hdr = o;
   o += al((size_t)p->B * nck * 2 * 8);
   L.tail_alpha = o;
-  o += al((size_t)p->B * p->K * p->C * 4);
+  o += al((size_t)p->B * p->K * p->C * rs);
   L.tail_n = o;
   o += al((size_t)p->B * p->K * 8);
   L.total = o;
@@ -172,20 +175,21 @@ struct WorkLayout {
   size_t ws_alpha, ws_gamma, ws_n, start, end, gT, gB, total;
 };
 
-WorkLayout work_layout(const scrf_problem* p, int64_t delta, const Geometry& g) {
+WorkLayout work_layout(const scrf_problem* p, int64_t delta, const Geometry& g, int precision) {
   WorkLayout W;
   size_t o = 0;
   const size_t win = (size_t)p->B * (delta + 1) * p->C;
+  const size_t rs = precision ? 8 : 4;
   W.ws_alpha = o;
-  o += al(win * 4);
+  o += al(win * rs);
   W.ws_gamma = o;
-  o += al(win * 4);
+  o += al(win * rs);
   W.ws_n = o;
   o += al((size_t)p->B * g.G * (delta + 1) * 8);
   W.start = o;
-  o += al((size_t)p->B * (p->T + 1) * p->C * 4);
+  o += al((size_t)p->B * (p->T + 1) * p->C * rs);
   W.end = o;
-  o += al((size_t)p->B * (p->T + 1) * p->C * 4);
+  o += al((size_t)p->B * (p->T + 1) * p->C * rs);
   W.gT = o;
   o += al((size_t)p->B * p->C * p->C * 8);
   W.gB = o;
@@ -216,7 +220,10 @@ cudaError_t launch_cluster(Kern kern, const Geometry& g, int B, size_t smem, cud
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ++g_launches;
-  return cudaLaunchKernelEx(&cfg, kern, arg);
+  if (g_ev_start) cudaEventRecord(g_ev_start, st);
+  e = cudaLaunchKernelEx(&cfg, kern, arg);
+  if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
+  return e;
 }
 
 template <typename R>
@@ -239,10 +246,10 @@ void fill_args(Args<R>& a, const scrf_problem* p, int64_t delta, const Geometry&
   unsigned char* base = (unsigned char*)ckpt;
   a.ck.g_hi = (R*)(base + L.g_hi);
   a.ck.g_lo = (R*)(base + L.g_lo);
-  a.ck.alpha = (float*)(base + L.alpha);
+  a.ck.alpha = (R*)(base + L.alpha);
   a.ck.n = (double*)(base + L.n);
   a.ck.hdr = (double*)(base + L.hdr);
-  a.tail_alpha = (float*)(base + L.tail_alpha);
+  a.tail_alpha = (R*)(base + L.tail_alpha);
   a.tail_n = (double*)(base + L.tail_n);
 }
 
@@ -268,18 +275,18 @@ int run_backward(const scrf_problem* p, int64_t delta, const double* logZ, const
   Geometry g;
   int rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, &g);
   if (rc) return rc;
-  WorkLayout W = work_layout(p, delta, g);
+  WorkLayout W = work_layout(p, delta, g, sizeof(R) == 8);
   if (work_bytes < W.total) return SCRF_EWORK;
   Args<R> a;
   fill_args(a, p, delta, g, (void*)ckpt);
   unsigned char* w = (unsigned char*)work;
   a.logZ_in = logZ;
   a.upstream = upstream;
-  a.ws_alpha = (float*)(w + W.ws_alpha);
-  a.ws_gamma = (float*)(w + W.ws_gamma);
+  a.ws_alpha = (R*)(w + W.ws_alpha);
+  a.ws_gamma = (R*)(w + W.ws_gamma);
   a.ws_n = (double*)(w + W.ws_n);
-  a.start_g = (float*)(w + W.start);
-  a.end_g = (float*)(w + W.end);
+  a.start_g = (R*)(w + W.start);
+  a.end_g = (R*)(w + W.end);
   a.gT_part = (double*)(w + W.gT);
   a.gB_part = (double*)(w + W.gB);
   cudaError_t e = cudaMemsetAsync(w + W.start, 0, W.total - W.start, st);
@@ -291,10 +298,10 @@ int run_backward(const scrf_problem* p, int64_t delta, const double* logZ, const
   {
     int n = B * C, blk = 128;
     ++g_launches;
-    finalize_kernel<<<(n + blk - 1) / blk, blk, 0, st>>>(a.start_g, a.end_g, p->lengths, upstream, B, T, C, grad_S, gPs,
+    finalize_kernel<R><<<(n + blk - 1) / blk, blk, 0, st>>>(a.start_g, a.end_g, p->lengths, upstream, B, T, C, grad_S, gPs,
                                                          gPe, pos);
     ++g_launches;
-    boundary_kernel<<<B, 256, 0, st>>>(a.start_g, p->lengths, B, T, C, bnd, cnt);
+    boundary_kernel<R><<<B, 256, 0, st>>>(a.start_g, p->lengths, B, T, C, bnd, cnt);
     size_t nT = (size_t)C * C, nB = (size_t)K * C;
     ++g_launches;
     reduce_partials_kernel<<<(unsigned)((nT + 255) / 256), 256, 0, st>>>(a.gT_part, upstream, B, nT, grad_T);
@@ -304,14 +311,15 @@ int run_backward(const scrf_problem* p, int64_t delta, const double* logZ, const
   return (int)cudaGetLastError();
 }
 
-__global__ void export_kernel(const float* alpha, const double* n, const double* N, int B, int nck, int K, int C,
+template <typename A>
+__global__ void export_kernel(const A* alpha, const double* n, const double* N, int B, int nck, int K, int C,
                               double* omega) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   size_t total = (size_t)B * nck * K * C;
   if (i >= total) return;
   size_t bi = i / ((size_t)K * C);  // (b, ckpt)
   size_t slot = (i / C) % K;
-  float av = alpha[i];
+  A av = alpha[i];
   double nv = n[bi * K + slot];
   if (!(av > -INFINITY) || !(nv > -INFINITY)) {
     omega[i] = kNegInfRef;
@@ -361,7 +369,7 @@ int scrf_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision
   Geometry g;
   rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, precision, &g);
   if (rc) return rc;
-  *bytes = work_layout(p, delta, g).total;
+  *bytes = work_layout(p, delta, g, precision).total;
   return SCRF_OK;
 }
 
@@ -392,7 +400,7 @@ int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, 
   Geometry g;
   rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, precision, &g);
   if (rc) return rc;
-  WorkLayout W = work_layout(p, delta, g);
+  WorkLayout W = work_layout(p, delta, g, precision);
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned char* w = (const unsigned char*)work;
   cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + W.gT, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
@@ -456,11 +464,21 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
   const int nck = (int)n_ckpt_of(p->T, delta);
   size_t total = (size_t)p->B * nck * p->K * p->C;
   ++g_launches;
-  export_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      (const float*)(base + L.alpha), (const double*)(base + L.n), N, (int)p->B, nck, (int)p->K, (int)p->C, omega);
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  if (precision)
+    export_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const double*)(base + L.alpha), (const double*)(base + L.n), N, (int)p->B, nck, (int)p->K, (int)p->C, omega);
+  else
+    export_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const float*)(base + L.alpha), (const double*)(base + L.n), N, (int)p->B, nck, (int)p->K, (int)p->C, omega);
   return (int)cudaGetLastError();
 }
 
 int scrf_last_launch_count(void) { return g_launches; }
+
+void scrf_profile_events(void* start, void* stop) {
+  g_ev_start = (cudaEvent_t)start;
+  g_ev_stop = (cudaEvent_t)stop;
+}
 
 }  // extern "C"

@@ -38,7 +38,7 @@ struct Ckpt {
   // normaliser of the K ring positions [K], header {n_{t0-1}, n_{t0}}
   R* g_hi;
   R* g_lo;
-  float* alpha;
+  R* alpha;
   double* n;
   double* hdr;
 };
@@ -58,16 +58,16 @@ struct Args {
   double* logZ;
   double* N;
   int32_t* dead_at;
-  float* tail_alpha;  // [B][K][C]
+  R* tail_alpha;      // [B][K][C]
   double* tail_n;     // [B][K]
   // backward inputs / outputs
   const double* logZ_in;
   const double* upstream;
-  float* ws_alpha;   // [B][delta+1][C]
-  float* ws_gamma;   // [B][delta+1][C]
+  R* ws_alpha;       // [B][delta+1][C]
+  R* ws_gamma;       // [B][delta+1][C]
   double* ws_n;      // [B][G][delta+1]
-  float* start_g;    // [B][T+1][C]
-  float* end_g;      // [B][T+1][C]
+  R* start_g;        // [B][T+1][C]  mass of segments starting at t (working type)
+  R* end_g;          // [B][T+1][C]  mass of segments ending at t
   double* gT_part;   // [B][C][C]
   double* gB_part;   // [B][K][C]
 };
@@ -113,10 +113,10 @@ struct BwdSmem {
   R* T2o;      // [Cgm][C]  T2 own rows (grad_T exponent)
   R* d_all;    // [2][C]
   R* bpart;    // [2][Cgm][WPL][3]
-  float* end_acc;  // [K+1][Cgm]
-  float* end1;     // [K+1][Cgm]
-  float* gBs;      // [K][Cgm]
-  float* gTs;      // [Cgm][C]
+  R* end_acc;  // [K+1][Cgm]
+  R* end1;     // [K+1][Cgm]
+  R* gBs;      // [K][Cgm]
+  R* gTs;      // [Cgm][C]
 };
 
 __device__ __forceinline__ double ld_or0(const double* p, size_t i) { return p ? __ldg(p + i) : 0.0; }
@@ -146,8 +146,8 @@ __host__ __device__ inline size_t bwd_extra_smem_bytes(int K, int C, const Geome
   const size_t KC = (size_t)K * g.Cgm;
   return 2 * r16(KC * sizeof(R)) + 2 * r16((size_t)g.Cgm * C * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
          r16(2 * (size_t)C * sizeof(R)) + r16(6 * (size_t)g.Cgm * g.WPL * sizeof(R)) +
-         2 * r16((size_t)(K + 1) * g.Cgm * sizeof(float)) + r16(KC * sizeof(float)) +
-         r16((size_t)g.Cgm * C * sizeof(float));
+         2 * r16((size_t)(K + 1) * g.Cgm * sizeof(R)) + r16(KC * sizeof(R)) +
+         r16((size_t)g.Cgm * C * sizeof(R));
 }
 
 template <typename T>
@@ -178,10 +178,10 @@ __device__ void carve_bwd(unsigned char*& p, int K, int C, const Geometry& g, Bw
   s.Trmax = carve<R>(p, g.Cgm);
   s.d_all = carve<R>(p, 2 * (size_t)C);
   s.bpart = carve<R>(p, 2 * 3 * (size_t)g.Cgm * g.WPL);
-  s.end_acc = carve<float>(p, (size_t)(K + 1) * g.Cgm);
-  s.end1 = carve<float>(p, (size_t)(K + 1) * g.Cgm);
-  s.gBs = carve<float>(p, (size_t)K * g.Cgm);
-  s.gTs = carve<float>(p, (size_t)g.Cgm * C);
+  s.end_acc = carve<R>(p, (size_t)(K + 1) * g.Cgm);
+  s.end1 = carve<R>(p, (size_t)(K + 1) * g.Cgm);
+  s.gBs = carve<R>(p, (size_t)K * g.Cgm);
+  s.gTs = carve<R>(p, (size_t)g.Cgm * C);
 }
 
 template <typename R>
@@ -248,13 +248,13 @@ __device__ void load_bwd_tables(const Args<R>& a, const Ctx& x, BwdSmem<R>& s) {
     R t2 = (r < x.Cg) ? (R)(a.trans[(size_t)(x.c0 + r) * C + c] * kLog2e) : (R)0;
     s.T2o[i] = t2;
     s.T2r[i] = (r < x.Cg) ? t2 - s.Trmax[r] : (R)0;
-    s.gTs[i] = 0.f;
+    s.gTs[i] = (R)0;
   }
   for (int i = x.tid; i < (K + 1) * g.Cgm; i += g.NT) {
-    s.end_acc[i] = 0.f;
-    s.end1[i] = 0.f;
+    s.end_acc[i] = (R)0;
+    s.end1[i] = (R)0;
   }
-  for (int i = x.tid; i < K * g.Cgm; i += g.NT) s.gBs[i] = 0.f;
+  for (int i = x.tid; i < K * g.Cgm; i += g.NT) s.gBs[i] = (R)0;
 }
 
 // gamma-tilde of own label `cl` from exchanged alpha-hat values (relative, <= 0).
@@ -440,11 +440,11 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, cg::clu
         s.ring_hi[slot * Cgm + x.cl] = hi;
         s.ring_lo[slot * Cgm + x.cl] = lo;
         if (MODE == MODE_FWD) {
-          a.tail_alpha[((size_t)x.b * K + slot) * C + c] = (float)ahat_own;
+          a.tail_alpha[((size_t)x.b * K + slot) * C + c] = ahat_own;
         } else {
           const size_t r = (size_t)x.b * (a.delta + 1) + (t - win_t0);
-          a.ws_alpha[r * C + c] = (float)ahat_own;
-          a.ws_gamma[r * C + c] = (float)gam;
+          a.ws_alpha[r * C + c] = ahat_own;
+          a.ws_gamma[r * C + c] = gam;
         }
       }
     }
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   // tail: position 0 has alpha = 0, every other slot is "never written"
   for (int q = x.tid; q < K * x.Cg; q += g.NT) {
     int slot = q / x.Cg, cc = q % x.Cg;
-    a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc] = slot == 0 ? 0.f : -CUDART_INF_F;
+    a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc] = slot == 0 ? (R)0 : Mth<R>::ninf();
   }
   if (x.rank == 0)
     for (int q = x.tid; q < K; q += g.NT) a.tail_n[(size_t)x.b * K + q] = q == 0 ? 0.0 : -CUDART_INF;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
       size_t gi = (base * K + slot) * C + x.c0 + cc;
       a.ck.g_hi[gi] = s.ring_hi[slot * Cgm + cc];
       a.ck.g_lo[gi] = s.ring_lo[slot * Cgm + cc];
-      a.ck.alpha[gi] = slot == 0 ? 0.f : -CUDART_INF_F;
+      a.ck.alpha[gi] = slot == 0 ? (R)0 : Mth<R>::ninf();
     }
     if (x.rank == 0) {
       for (int q = x.tid; q < K; q += g.NT) a.ck.n[base * K + q] = q == 0 ? 0.0 : -CUDART_INF;
@@ -595,18 +595,18 @@ __device__ void flush_grads(const Args<R>& a, const Ctx& x, BwdSmem<R>& sb) {
   __syncthreads();
   for (int q = x.tid; q < K * x.Cg; q += g.NT) {
     int k = q / x.Cg, cc = q % x.Cg;
-    float v = sb.gBs[k * g.Cgm + cc];
-    if (v != 0.f) {
+    R v = sb.gBs[k * g.Cgm + cc];
+    if (v != (R)0) {
       a.gB_part[((size_t)x.b * K + k) * C + x.c0 + cc] += (double)v;
-      sb.gBs[k * g.Cgm + cc] = 0.f;
+      sb.gBs[k * g.Cgm + cc] = (R)0;
     }
   }
   for (int q = x.tid; q < x.Cg * C; q += g.NT) {
     int r = q / C, cc = q % C;
-    float v = sb.gTs[r * C + cc];
-    if (v != 0.f) {
+    R v = sb.gTs[r * C + cc];
+    if (v != (R)0) {
       a.gT_part[((size_t)x.b * C + x.c0 + r) * C + cc] += (double)v;
-      sb.gTs[r * C + cc] = 0.f;
+      sb.gTs[r * C + cc] = (R)0;
     }
   }
   __syncthreads();
@@ -626,10 +626,10 @@ __device__ __forceinline__ SrcVals<R> src_vals(const Args<R>& a, const Ctx& x, i
   const int c = x.c0 + (x.active ? x.cl : 0);
   const size_t r = (size_t)x.b * (a.delta + 1) + (t - win_t0);
   const double n_t = a.ws_n[((size_t)x.b * a.geo.G + x.rank) * (a.delta + 1) + (t - win_t0)];
-  const float gt = a.ws_gamma[r * C + c];
+  const R gt = a.ws_gamma[r * C + c];
   double w = -S2(x, C, t, c) + PS2(x, C, t, c) - Fp;
   split(w, v.w_hi, v.w_lo);
-  v.gam = (R)(Fp + n_t - logZ2) + (R)gt;
+  v.gam = (R)(Fp + n_t - logZ2) + gt;
   return v;
 }
 
@@ -662,8 +662,8 @@ __device__ __forceinline__ void bwd_bulk(const Args<R>& a, const Ctx& x, BwdSmem
       if (m != Mth<R>::ninf()) sum += Mth<R>::ex2(y - m);
       R M = Mth<R>::ex2(y + v.gam);
       msum += M;
-      sb.gBs[(k - 1) * Cgm + x.cl] += (float)M;
-      sb.end_acc[eslot * Cgm + x.cl] += (float)M;
+      sb.gBs[(k - 1) * Cgm + x.cl] += M;
+      sb.end_acc[eslot * Cgm + x.cl] += M;
       slot += step;
       if (slot >= K) slot -= K;
       eslot += stepE;
@@ -749,8 +749,8 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
       R gam = gamma_from_alpha(ah, s.T2c, s.Tcmax, C, Cgm, x.cls, x.jj, g.GW);
       if (x.active && x.jj == 0) {
         const size_t r = (size_t)x.b * (a.delta + 1);
-        a.ws_alpha[r * C + c] = (float)ah[c];
-        a.ws_gamma[r * C + c] = (float)gam;
+        a.ws_alpha[r * C + c] = ah[c];
+        a.ws_gamma[r * C + c] = gam;
       }
     }
     if (x.tid == 0) a.ws_n[((size_t)x.b * g.G + x.rank) * (a.delta + 1)] = n_t0;
@@ -785,9 +785,9 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
         ms += M1;
         R dv = ms_value(m, sm);
         if (x.jj == 0) {
-          sb.end1[((t + 1) % (K + 1)) * Cgm + x.cl] = (float)M1;
-          sb.gBs[x.cl] += (float)M1;
-          a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = (float)ms;
+          sb.end1[((t + 1) % (K + 1)) * Cgm + x.cl] = M1;
+          sb.gBs[x.cl] += M1;
+          a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = ms;
         }
         publish(cl, g, x, sb.d_all, par * C + c, dv);
       }
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
         for (int q = x.jj; q < C; q += g.GW) {
           const R dh = dd[q] - dmax;
           ssum += Mth<R>::ex2(sb.T2r[(size_t)x.cls * C + q] + dh);
-          if (x.active && ahat != Mth<R>::ninf()) sb.gTs[(size_t)x.cls * C + q] += (float)Mth<R>::ex2(ahat + sb.T2o[(size_t)x.cls * C + q] + dh + Zt);
+          if (x.active && ahat != Mth<R>::ninf()) sb.gTs[(size_t)x.cls * C + q] += Mth<R>::ex2(ahat + sb.T2o[(size_t)x.cls * C + q] + dh + Zt);
         }
         ssum = group_sum(ssum, g.GW);
         R bt;
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
         if (e <= L) {
           const int es = e % (K + 1);
           a.end_g[((size_t)x.b * (a.T + 1) + e) * C + c] = sb.end_acc[es * Cgm + x.cl] + sb.end1[es * Cgm + x.cl];
-          sb.end_acc[es * Cgm + x.cl] = 0.f;
+          sb.end_acc[es * Cgm + x.cl] = (R)0;
         }
       }
       Fp_cur = nd_prev;
@@ -878,7 +878,8 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
 //
 // One thread per (b, c): sequential fp64 scan over t (coverage cumsum).
 
-__global__ void finalize_kernel(const float* start_g, const float* end_g, const int64_t* lengths,
+template <typename R>
+__global__ void finalize_kernel(const R* start_g, const R* end_g, const int64_t* lengths,
                                 const double* upstream, int B, int T, int C, double* grad_S, double* grad_Ps,
                                 double* grad_Pe, double* pos) {
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -903,7 +904,8 @@ __global__ void finalize_kernel(const float* start_g, const float* end_g, const 
 }
 
 // boundary posterior + expected segment count, one block per b
-__global__ void boundary_kernel(const float* start_g, const int64_t* lengths, int B, int T, int C, double* boundary,
+template <typename R>
+__global__ void boundary_kernel(const R* start_g, const int64_t* lengths, int B, int T, int C, double* boundary,
                                 double* count) {
   const int b = blockIdx.x;
   const int L = (int)lengths[b];
