@@ -198,6 +198,9 @@ def run_ours(args, rank, world, local):
     lib = _lib.load()
 
     ev_main = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for e in ev_main:  # torch creates the CUDA event lazily on first record
+        e.record()
+    torch.cuda.synchronize()
     bwd_ms, fwd_ms = [], []
     launches = [0]
 
