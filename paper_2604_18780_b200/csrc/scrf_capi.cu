@@ -77,8 +77,8 @@ Geometry make_geo(int G, int K, int C) {
 }
 
 size_t fb_smem(const Geometry& g, int K, int C, int precision) {
-  return precision ? fwd_smem_bytes<double>(K, C, g) + bwd_extra_smem_bytes<double>(K, C, g)
-                   : fwd_smem_bytes<float>(K, C, g) + bwd_extra_smem_bytes<float>(K, C, g);
+  return precision ? fwd_smem_bytes<double>(K, C, g) + bwd_extra_smem_bytes<double>(K, C, g) + stage_smem_bytes<double>(g)
+                   : fwd_smem_bytes<float>(K, C, g) + bwd_extra_smem_bytes<float>(K, C, g) + stage_smem_bytes<float>(g);
 }
 
 // Geometry shared by forward and backward (the replay must re-execute the forward
@@ -264,7 +264,7 @@ int run_forward(const scrf_problem* p, int64_t delta, double* logZ, double* N, i
   a.logZ = logZ;
   a.N = N;
   a.dead_at = dead_at;
-  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g);
+  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g) + stage_smem_bytes<R>(g);
   return (int)launch_cluster(fwd_kernel<R>, g, a.B, smem, st, a);
 }
 
@@ -291,7 +291,7 @@ int run_backward(const scrf_problem* p, int64_t delta, const double* logZ, const
   a.gB_part = (double*)(w + W.gB);
   cudaError_t e = cudaMemsetAsync(w + W.start, 0, W.total - W.start, st);
   if (e != cudaSuccess) return (int)e;
-  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g) + bwd_extra_smem_bytes<R>(a.K, a.C, g);
+  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g) + bwd_extra_smem_bytes<R>(a.K, a.C, g) + stage_smem_bytes<R>(g);
   e = launch_cluster(bwd_kernel<R>, g, a.B, smem, st, a);
   if (e != cudaSuccess) return (int)e;
   const int B = a.B, T = a.T, C = a.C, K = a.K;

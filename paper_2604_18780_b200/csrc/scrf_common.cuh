@@ -74,12 +74,22 @@ __device__ __forceinline__ R ms_value(R m, R s) {
   return (m == Mth<R>::ninf() || !(s > (R)0)) ? Mth<R>::ninf() : m + Mth<R>::lg2(s);
 }
 
-// Reductions over aligned lane groups of width W (power of two <= 32).
+// Reductions over aligned lane groups of width W (power of two <= 32). Each
+// butterfly level merges (lower lane, upper lane) in that order in both partners,
+// so every lane of the group ends with the bit-identical result.
 template <typename R>
 __device__ __forceinline__ void group_ms(R& m, R& s, int W) {
+  const int lane = threadIdx.x & 31;
   for (int off = W >> 1; off > 0; off >>= 1) {
     R m2 = __shfl_xor_sync(0xffffffffu, m, off, W);
     R s2 = __shfl_xor_sync(0xffffffffu, s, off, W);
+    if (lane & off) {
+      R tm = m, ts = s;
+      m = m2;
+      s = s2;
+      m2 = tm;
+      s2 = ts;
+    }
     ms_merge(m, s, m2, s2);
   }
 }

@@ -340,6 +340,149 @@ __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
 // ----------------------------------------------------------------------------
+// per-position input staging
+//
+// Every position needs a handful of fp64 inputs per own label (prefix sums and
+// projections, and in the backward the replayed window values). Loading them on
+// the critical path costs a full HBM/L2 round trip per position, so they are
+// staged in chunks of P positions: chunk q+2 is loaded into registers while chunk
+// q is consumed, then parked in one of two shared-memory chunk buffers.
+//   E0[t,c] = S2[t,c] + Pe2[t-1,c]     (forward target term, backward v[t] base)
+//   G0[t,c] = -S2[t,c] + Ps2[t,c]      (forward g[t] base, backward w[t] base)
+// backward only: gam[t,c] = gamma~, ahat[t,c] = alpha-hat, n[t] (window store).
+
+constexpr int kStageMax = 2;
+
+template <typename R>
+struct StageSmem {
+  double* E0;  // [2][P][Cgm]
+  double* G0;
+  R* gam;      // [2][P][Cgm]
+  R* ahat;
+  double* n;   // [2][P]
+};
+
+__host__ __device__ inline int stage_chunk(const Geometry& g) {
+  int P = 64;
+  while (P > 2 && P * g.Cgm > g.NT * kStageMax) P >>= 1;
+  return P;
+}
+
+template <typename R>
+__host__ __device__ inline size_t stage_smem_bytes(const Geometry& g) {
+  const size_t P = stage_chunk(g);
+  return 2 * r16(2 * P * g.Cgm * 8) + 2 * r16(2 * P * g.Cgm * sizeof(R)) + r16(2 * P * 8);
+}
+
+template <typename R>
+__device__ void carve_stage(unsigned char*& p, const Geometry& g, StageSmem<R>& st) {
+  const size_t P = stage_chunk(g);
+  st.E0 = carve<double>(p, 2 * P * g.Cgm);
+  st.G0 = carve<double>(p, 2 * P * g.Cgm);
+  st.gam = carve<R>(p, 2 * P * g.Cgm);
+  st.ahat = carve<R>(p, 2 * P * g.Cgm);
+  st.n = carve<double>(p, 2 * P);
+}
+
+template <typename R, bool BWD>
+struct Stager {
+  int P, tb, dir, win_t0;
+  double rE[kStageMax], rG[kStageMax], rn;
+  R rg[kStageMax], ra[kStageMax];
+
+  __device__ __forceinline__ int pos(int q, int i) const { return tb + dir * (q * P + i); }
+
+  __device__ __forceinline__ void load(const Args<R>& a, const Ctx& x, int q) {
+    const int n = P * x.Cg;
+#pragma unroll
+    for (int r = 0; r < kStageMax; ++r) {
+      const int e = x.tid + r * a.geo.NT;
+      rE[r] = 0.0;
+      rG[r] = 0.0;
+      rg[r] = (R)0;
+      ra[r] = (R)0;
+      if (e < n) {
+        const int i = e / x.Cg, cc = e % x.Cg, c = x.c0 + cc;
+        const int t = pos(q, i);
+        if (t >= 0 && t <= a.T) {
+          const double s2 = __ldg(x.S + (size_t)t * a.C + c) * kLog2e;
+          rE[r] = s2 + PE2(x, a.C, t - 1, c);
+          rG[r] = -s2 + ((t < a.T) ? PS2(x, a.C, t, c) : 0.0);
+          if (BWD && t >= win_t0 && t <= win_t0 + a.delta) {
+            const size_t row = (size_t)x.b * (a.delta + 1) + (t - win_t0);
+            rg[r] = a.ws_gamma[row * a.C + c];
+            ra[r] = a.ws_alpha[row * a.C + c];
+          }
+        }
+      }
+    }
+    rn = 0.0;
+    if (BWD && x.tid < P) {
+      const int t = pos(q, x.tid);
+      if (t >= win_t0 && t <= win_t0 + a.delta && t >= 0 && t <= a.T)
+        rn = a.ws_n[((size_t)x.b * a.geo.G + x.rank) * (a.delta + 1) + (t - win_t0)];
+    }
+  }
+
+  __device__ __forceinline__ void store(const Args<R>& a, const Ctx& x, StageSmem<R>& st, int q) {
+    const int n = P * x.Cg;
+    const int buf = q & 1;
+    const int Cgm = a.geo.Cgm;
+#pragma unroll
+    for (int r = 0; r < kStageMax; ++r) {
+      const int e = x.tid + r * a.geo.NT;
+      if (e < n) {
+        const int i = e / x.Cg, cc = e % x.Cg;
+        const size_t k = ((size_t)buf * P + i) * Cgm + cc;
+        st.E0[k] = rE[r];
+        st.G0[k] = rG[r];
+        if (BWD) {
+          st.gam[k] = rg[r];
+          st.ahat[k] = ra[r];
+        }
+      }
+    }
+    if (BWD && x.tid < P) st.n[buf * P + x.tid] = rn;
+  }
+
+  // shared-memory index of (t, own label cl) / of position t
+  __device__ __forceinline__ size_t idx(int t, int cl, int Cgm) const {
+    const int d = dir * (t - tb);
+    const int q = d / P, i = d - q * P;
+    return ((size_t)(q & 1) * P + i) * Cgm + cl;
+  }
+  __device__ __forceinline__ int nidx(int t) const {
+    const int d = dir * (t - tb);
+    const int q = d / P, i = d - q * P;
+    return (q & 1) * P + i;
+  }
+
+  // prime chunks 0 and 1 in shared memory and chunk 2 in registers (ends with a barrier)
+  __device__ void begin(const Args<R>& a, const Ctx& x, StageSmem<R>& st, int tb_, int dir_, int win) {
+    P = stage_chunk(a.geo);
+    tb = tb_;
+    dir = dir_;
+    win_t0 = win;
+    load(a, x, 0);
+    store(a, x, st, 0);
+    load(a, x, 1);
+    store(a, x, st, 1);
+    load(a, x, 2);
+    __syncthreads();
+  }
+
+  // call at the top of the iteration that processes position t (before any use)
+  __device__ __forceinline__ void advance(const Args<R>& a, const Ctx& x, StageSmem<R>& st, int t) {
+    const int d = dir * (t - tb);
+    if (d > 0 && d % P == 0) {
+      const int q = d / P;
+      store(a, x, st, q + 1);
+      load(a, x, q + 2);
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------
 // forward sweep (shared by the forward kernel and the backward's replay)
 
 enum { MODE_FWD = 0, MODE_REPLAY = 1 };
@@ -353,18 +496,19 @@ struct FwdBook {
 // Runs targets t = t_begin+1 .. t_end. Preconditions: ring holds g[s] for
 // s in (t_begin-K, t_begin]; Fcur = frame of target t_begin+1; n_prev = n_{t_begin}.
 template <typename R, int MODE>
-__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, cg::cluster_group& cl, int t_begin, int t_end,
-                          double Fcur, double n_prev, FwdBook& bk, int win_t0) {
+__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSmem<R>& st, cg::cluster_group& cl,
+                          int t_begin, int t_end, double Fcur, double n_prev, FwdBook& bk, int win_t0) {
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm;
   const int c = x.c0 + (x.active ? x.cl : 0);
   if (t_end <= t_begin) return;
+  Stager<R, false> sg;
+  sg.begin(a, x, st, t_begin, +1, 0);
 
   // e for target t_begin+1
   R e_hi, e_lo;
   {
-    int t1 = t_begin + 1;
-    double e = x.active ? S2(x, C, t1, c) + PE2(x, C, t1 - 1, c) - Fcur : 0.0;
+    double e = st.E0[sg.idx(t_begin + 1, x.cls, Cgm)] - Fcur;
     split(e, e_hi, e_lo);
   }
   {
@@ -376,25 +520,28 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, cg::clu
 
   for (int t = t_begin + 1; t <= t_end; ++t) {
     const int par = t & 1;
-    // (A) critical: merge bulk partial with the k = 1 term, publish a[t]
-    if (x.glane) {
+    sg.advance(a, x, st, t);
+    // (A) critical: merge bulk partials (lane-parallel tree) with the k = 1 term, publish a[t]
+    if (x.gl) {
       R m = Mth<R>::ninf(), sm = 0;
-      for (int w = 0; w < g.WPL; ++w) {
-        size_t i = ((size_t)par * Cgm + x.cl) * g.WPL + w;
-        ms_merge(m, sm, s.part_m[i], s.part_s[i]);
+      if (x.active && x.jj < g.WPL) {
+        size_t i = ((size_t)par * Cgm + x.cl) * g.WPL + x.jj;
+        m = s.part_m[i];
+        sm = s.part_s[i];
       }
+      group_ms(m, sm, g.GW);
       const int slot = (t - 1) % K;
-      R v1 = (s.ring_hi[slot * Cgm + x.cl] + e_hi) + (s.ring_lo[slot * Cgm + x.cl] + e_lo) + s.B2[x.cl];
+      R v1 = (s.ring_hi[slot * Cgm + x.cls] + e_hi) + (s.ring_lo[slot * Cgm + x.cls] + e_lo) + s.B2[x.cls];
       ms_merge(m, sm, v1, (R)1);
       R av = ms_value(m, sm);
-      publish(cl, g, x, s.a_all, par * C + c, av);
+      if (x.active) publish(cl, g, x, s.a_all, par * C + c, av);
     }
     cluster_arrive();
     // (C) bulk for target t+1 (frame n_{t-1} = n_prev)
     const double Fnext = n_prev;
     R en_hi = 0, en_lo = 0;
     if (t < t_end) {
-      double e = x.active ? S2(x, C, t + 1, c) + PE2(x, C, t, c) - Fnext : 0.0;
+      double e = st.E0[sg.idx(t + 1, x.cls, Cgm)] - Fnext;
       split(e, en_hi, en_lo);
       R m, sm;
       fwd_bulk(a, x, s, t + 1, en_hi, en_lo, m, sm);
@@ -433,7 +580,7 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, cg::clu
         }
       }
       if (x.active && x.jj == 0) {
-        double gv = (gam == Mth<R>::ninf()) ? -CUDART_INF : n_t + (double)gam - S2(x, C, t, c) + PS2(x, C, t, c);
+        double gv = (gam == Mth<R>::ninf()) ? -CUDART_INF : n_t + (double)gam + st.G0[sg.idx(t, x.cl, Cgm)];
         R hi, lo;
         split(gv, hi, lo);
         const int slot = t % K;
@@ -508,7 +655,9 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* p = smem_raw;
   FwdSmem<R> s;
+  StageSmem<R> st;
   carve_fwd<R>(p, a.K, a.C, a.geo, s);
+  carve_stage<R>(p, a.geo, st);
   Ctx x = make_ctx(a, cl);
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm;
@@ -564,7 +713,7 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   bk.N_cur = 0.0;
   bk.dead_at = -1;
   cl.sync();
-  fwd_sweep<R, MODE_FWD>(a, x, s, cl, 0, x.L, 0.0, 0.0, bk, 0);
+  fwd_sweep<R, MODE_FWD>(a, x, s, st, cl, 0, x.L, 0.0, 0.0, bk, 0);
   // checkpoints past the sequence end hold the frozen ring at L
   const int i_first = x.L / a.delta + 1;
   for (int i = i_first; i < a.n_ckpt; ++i) {
@@ -617,21 +766,6 @@ template <typename R>
 struct SrcVals {
   R w_hi, w_lo, gam;
 };
-
-template <typename R>
-__device__ __forceinline__ SrcVals<R> src_vals(const Args<R>& a, const Ctx& x, int t, int win_t0, double Fp,
-                                               double logZ2) {
-  SrcVals<R> v;
-  const int C = a.C;
-  const int c = x.c0 + (x.active ? x.cl : 0);
-  const size_t r = (size_t)x.b * (a.delta + 1) + (t - win_t0);
-  const double n_t = a.ws_n[((size_t)x.b * a.geo.G + x.rank) * (a.delta + 1) + (t - win_t0)];
-  const R gt = a.ws_gamma[r * C + c];
-  double w = -S2(x, C, t, c) + PS2(x, C, t, c) - Fp;
-  split(w, v.w_hi, v.w_lo);
-  v.gam = (R)(Fp + n_t - logZ2) + gt;
-  return v;
-}
 
 // bulk for source ts (durations k >= 2, k <= min(K, L - ts))
 template <typename R>
@@ -697,8 +831,10 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
   unsigned char* p = smem_raw;
   FwdSmem<R> s;
   BwdSmem<R> sb;
+  StageSmem<R> st;
   carve_fwd<R>(p, a.K, a.C, a.geo, s);
   carve_bwd<R>(p, a.K, a.C, a.geo, sb);
+  carve_stage<R>(p, a.geo, st);
   Ctx x = make_ctx(a, cl);
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm, L = x.L;
@@ -755,13 +891,22 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     }
     if (x.tid == 0) a.ws_n[((size_t)x.b * g.G + x.rank) * (a.delta + 1)] = n_t0;
     __syncthreads();
-    fwd_sweep<R, MODE_REPLAY>(a, x, s, cl, t0, t1, (t0 == 0) ? 0.0 : n_t0m1, n_t0, bk, t0);
+    fwd_sweep<R, MODE_REPLAY>(a, x, s, st, cl, t0, t1, (t0 == 0) ? 0.0 : n_t0m1, n_t0, bk, t0);
     __syncthreads();
     // all CTAs must finish the replay (they exchange through a_all) before we reuse barriers
     cl.sync();
 
     // ---- beta sweep over sources t = t1-1 .. t0
-    SrcVals<R> cur = src_vals(a, x, t1 - 1, t0, Fp_cur, logZ2);
+    Stager<R, true> sg;
+    sg.begin(a, x, st, t1 - 1, -1, t0);
+    auto src = [&](int ts, double Fp) {
+      SrcVals<R> v;
+      const size_t k = sg.idx(ts, x.cls, Cgm);
+      split(st.G0[k] - Fp, v.w_hi, v.w_lo);
+      v.gam = (R)(Fp + st.n[sg.nidx(ts)] - logZ2) + st.gam[k];
+      return v;
+    };
+    SrcVals<R> cur = src(t1 - 1, Fp_cur);
     {
       R m, sm, ms;
       bwd_bulk(a, x, sb, s.B2, t1 - 1, cur, m, sm, ms);
@@ -770,32 +915,36 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     __syncthreads();
     for (int t = t1 - 1; t >= t0; --t) {
       const int par = t & 1;
+      sg.advance(a, x, st, t);
       // (A) critical k = 1 term for source t
-      if (x.glane) {
+      if (x.gl) {
         R m = Mth<R>::ninf(), sm = 0, ms = 0;
-        for (int w = 0; w < g.WPL; ++w) {
-          size_t q = (((size_t)par * Cgm + x.cl) * g.WPL + w) * 3;
-          ms_merge(m, sm, sb.bpart[q], sb.bpart[q + 1]);
-          ms += sb.bpart[q + 2];
+        if (x.active && x.jj < g.WPL) {
+          size_t q = (((size_t)par * Cgm + x.cl) * g.WPL + x.jj) * 3;
+          m = sb.bpart[q];
+          sm = sb.bpart[q + 1];
+          ms = sb.bpart[q + 2];
         }
+        group_ms(m, sm, g.GW);
+        ms = group_sum(ms, g.GW);
         const int slot = (t + 1) % K;
-        R y1 = (sb.vr_hi[slot * Cgm + x.cl] + cur.w_hi) + (sb.vr_lo[slot * Cgm + x.cl] + cur.w_lo) + s.B2[x.cl];
+        R y1 = (sb.vr_hi[slot * Cgm + x.cls] + cur.w_hi) + (sb.vr_lo[slot * Cgm + x.cls] + cur.w_lo) + s.B2[x.cls];
         R M1 = Mth<R>::ex2(y1 + cur.gam);
         ms_merge(m, sm, y1, (R)1);
         ms += M1;
         R dv = ms_value(m, sm);
-        if (x.jj == 0) {
+        if (x.active && x.jj == 0) {
           sb.end1[((t + 1) % (K + 1)) * Cgm + x.cl] = M1;
           sb.gBs[x.cl] += M1;
           a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = ms;
         }
-        publish(cl, g, x, sb.d_all, par * C + c, dv);
+        if (x.active) publish(cl, g, x, sb.d_all, par * C + c, dv);
       }
       cluster_arrive();
       // (C) bulk for source t-1 (frame nd_{t+1})
       SrcVals<R> nxt = cur;
       if (t - 1 >= t0) {
-        nxt = src_vals(a, x, t - 1, t0, nd_prev, logZ2);
+        nxt = src(t - 1, nd_prev);
         R m, sm, ms;
         bwd_bulk(a, x, sb, s.B2, t - 1, nxt, m, sm, ms);
         store_bpart(g, x, sb.bpart, (t - 1) & 1, m, sm, ms);
@@ -809,10 +958,10 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
       const bool dead = (dmax == Mth<R>::ninf());
       const double nd_t = dead ? Fp_cur : Fp_cur + (double)dmax;
       if (x.gl && !dead) {
-        const size_t r = (size_t)x.b * (a.delta + 1) + (t - t0);
-        const double n_t = a.ws_n[((size_t)x.b * g.G + x.rank) * (a.delta + 1) + (t - t0)];
+        const size_t k = sg.idx(t, x.cls, Cgm);
+        const double n_t = st.n[sg.nidx(t)];
         const R Zt = (R)(n_t + nd_t - logZ2);
-        const R ahat = (R)a.ws_alpha[r * C + c];
+        const R ahat = st.ahat[k];
         R ssum = 0;
         for (int q = x.jj; q < C; q += g.GW) {
           const R dh = dd[q] - dmax;
@@ -834,7 +983,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
           bt = sb.Trmax[x.cls] + Mth<R>::lg2(ssum);
         }
         if (x.active && x.jj == 0 && t >= 1) {
-          double vv = (bt == Mth<R>::ninf()) ? -CUDART_INF : S2(x, C, t, c) + PE2(x, C, t - 1, c) + nd_t + (double)bt;
+          double vv = (bt == Mth<R>::ninf()) ? -CUDART_INF : st.E0[k] + nd_t + (double)bt;
           R hi, lo;
           split(vv, hi, lo);
           sb.vr_hi[(t % K) * Cgm + x.cl] = hi;

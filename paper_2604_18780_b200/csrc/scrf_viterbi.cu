@@ -37,6 +37,13 @@ struct VitArgs {
   int32_t* seg_count;
 };
 
+// per-position inputs (raw fp64 S[t], Ps[t], Pe[t-1] of own labels) staged in chunks of P
+__host__ __device__ inline int vit_chunk(const Geometry& g) {
+  int P = 64;
+  while (P > 2 && P * g.Cgm > g.NT * 2) P >>= 1;
+  return P;
+}
+
 __host__ __device__ inline size_t vit_smem_bytes(int K, int C, const Geometry& g, bool has_ps) {
   auto r16 = [](size_t n) { return (n + 15) & ~(size_t)15; };
   const size_t KC = (size_t)K * g.Cgm;
@@ -47,6 +54,7 @@ __host__ __device__ inline size_t vit_smem_bytes(int K, int C, const Geometry& g
   n += r16(KC * sizeof(int32_t));     // argmax
   n += r16((size_t)C * g.Cgm * sizeof(double));  // T columns
   n += r16(2 * (size_t)C * sizeof(double));      // exchange
+  n += 3 * r16(2 * (size_t)vit_chunk(g) * g.Cgm * sizeof(double));  // staged S, Ps, Pe rows
   return n;
 }
 
@@ -78,6 +86,10 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
   int32_t* garg = (int32_t*)take(KC * 4);
   double* Tcol = (double*)take((size_t)C * Cgm * 8);
   double* xall = (double*)take(2 * (size_t)C * 8);
+  const int P = vit_chunk(g);
+  double* stS = (double*)take(2 * (size_t)P * Cgm * 8);
+  double* stPs = (double*)take(2 * (size_t)P * Cgm * 8);
+  double* stPe = (double*)take(2 * (size_t)P * Cgm * 8);
 
   const int rank = (int)cl.block_rank();
   const int b = blockIdx.x / g.G;
@@ -95,6 +107,43 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
   const double* pe = a.pe ? a.pe + (size_t)b * a.T * C : nullptr;
   double* dvr = a.dvring + (size_t)b * K * C;
   int32_t* bp = a.bp + (size_t)b * (a.T + 1) * C;
+
+  // chunk q holds positions [q*P, (q+1)*P); registers carry chunk q+2 while q is consumed
+  double rS[2], rPs[2], rPe[2];
+  auto vload = [&](int q) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + r * g.NT;
+      rS[r] = rPs[r] = rPe[r] = 0.0;
+      if (e < P * Cg) {
+        const int i = e / Cg, cc = e % Cg, t = q * P + i;
+        if (t <= a.T) {
+          rS[r] = __ldg(S + (size_t)t * C + c0 + cc);
+          rPs[r] = (ps && t < a.T) ? __ldg(ps + (size_t)t * C + c0 + cc) : 0.0;
+          rPe[r] = (pe && t >= 1) ? __ldg(pe + (size_t)(t - 1) * C + c0 + cc) : 0.0;
+        }
+      }
+    }
+  };
+  auto vstore = [&](int q) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + r * g.NT;
+      if (e < P * Cg) {
+        const int i = e / Cg, cc = e % Cg;
+        const size_t k = ((size_t)(q & 1) * P + i) * Cgm + cc;
+        stS[k] = rS[r];
+        stPs[k] = rPs[r];
+        stPe[k] = rPe[r];
+      }
+    }
+  };
+  auto vidx = [&](int t, int cc) { return ((size_t)((t / P) & 1) * P + (t % P)) * Cgm + cc; };
+  vload(0);
+  vstore(0);
+  vload(1);
+  vstore(1);
+  vload(2);
 
   for (int i = tid; i < (int)KC; i += g.NT) {
     int k = i / Cgm, cc = i % Cgm;
@@ -134,8 +183,8 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
       gmax[slot * Cgm + cls] = best;
       gsec[slot * Cgm + cls] = sec;
       garg[slot * Cgm + cls] = arg;
-      sring[slot * Cgm + cls] = __ldg(S + (size_t)s * C + c);
-      if (psring) psring[slot * Cgm + cls] = (s < a.T) ? __ldg(ps + (size_t)s * C + c) : 0.0;
+      sring[slot * Cgm + cls] = stS[vidx(s, cls)];
+      if (psring) psring[slot * Cgm + cls] = stPs[vidx(s, cls)];
     }
   };
 
@@ -152,8 +201,13 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
     const int kmax = min(K, t);
     double best = -CUDART_INF;
     int bk = 0;
-    const double St = active ? __ldg(S + (size_t)t * C + c) : 0.0;
-    const double Pet = (active && pe) ? __ldg(pe + (size_t)(t - 1) * C + c) : 0.0;
+    if (t % P == 0) {  // entering chunk q = t / P: park chunk q+1, prefetch chunk q+2
+      vstore(t / P + 1);
+      vload(t / P + 2);
+      __syncthreads();
+    }
+    const double St = stS[vidx(t, cls)];
+    const double Pet = stPe[vidx(t, cls)];
     if (active) {
       for (int k = 1 + j; k <= kmax; k += g.TPL) {
         const int slot = (t - k) % K;
