@@ -409,10 +409,15 @@ int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, 
   return (int)e;
 }
 
+static size_t vit_dvr_bytes(const scrf_problem* p, const Geometry& g) { return al((size_t)p->B * g.G * p->K * p->C * 8); }
+
 int scrf_viterbi_work_bytes(const scrf_problem* p, size_t* bytes) {
   int rc = check_problem(p);
   if (rc) return rc;
-  *bytes = al((size_t)p->B * p->K * p->C * 8) + al((size_t)p->B * (p->T + 1) * p->C * 4);
+  Geometry g;
+  rc = choose_vit_geo((int)p->B, (int)p->K, (int)p->C, p->proj_start != nullptr, &g);
+  if (rc) return rc;
+  *bytes = vit_dvr_bytes(p, g) + al((size_t)p->B * (p->T + 1) * p->C * 4);
   return SCRF_OK;
 }
 
@@ -443,7 +448,7 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
   a.geo = g;
   unsigned char* w = (unsigned char*)work;
   a.dvring = (double*)w;
-  a.bp = (int32_t*)(w + al((size_t)p->B * p->K * p->C * 8));
+  a.bp = (int32_t*)(w + vit_dvr_bytes(p, g));
   a.score = score;
   a.seg_start = seg_start;
   a.seg_end = seg_end;

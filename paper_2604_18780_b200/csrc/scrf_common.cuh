@@ -106,6 +106,89 @@ __device__ __forceinline__ T group_max(T v, int W) {
   return v;
 }
 
+// ----------------------------------------------------------------------------
+// Cluster exchange without cluster barriers.
+//
+// Each CTA owns two mbarriers per exchanged vector (one per position parity). A
+// producer lane sends its label's value to every CTA of the cluster with
+// st.async ... mbarrier::complete_tx (async proxy: no release fence, so the
+// sender's in-flight global loads / stores never stall it); the receiving CTA
+// arms its barrier with expect_tx(C * sizeof(R)) and all its threads wait on
+// the barrier's phase parity. Parity double-buffering is WAR-safe because a peer
+// can only send position t+2 after receiving our position t+1, which we publish
+// after finishing every read of position t.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "SCRF_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra SCRF_WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_async(uint32_t dst, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(dst),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+
+// One exchanged vector of C values of type T (double-buffered by parity).
+template <typename T>
+struct Xchg {
+  T* buf;          // [2][C] local buffer
+  uint64_t* bar;   // [2] local mbarriers
+  uint32_t phase;  // bit p = parity of the next wait on bar[p]
+  int C;
+
+  __device__ void init(int tid) {
+    if (tid == 0) {
+      mbar_init(smem_u32(&bar[0]), 1);
+      mbar_init(smem_u32(&bar[1]), 1);
+      mbar_fence_init();
+    }
+    phase = 0;
+  }
+  // one thread per CTA, once per use of parity p, before waiting on it
+  __device__ __forceinline__ void arm(int p) { mbar_expect(smem_u32(&bar[p]), (uint32_t)(C * sizeof(T))); }
+  // send value v for label c to ranks r = first, first+stride, ... < G
+  __device__ __forceinline__ void send(int p, int c, T v, int first, int stride, int G) {
+    const uint32_t la = smem_u32(&buf[p * C + c]);
+    const uint32_t lb = smem_u32(&bar[p]);
+    for (int r = first; r < G; r += stride) st_async(mapa_u32(la, r), v, mapa_u32(lb, r));
+  }
+  __device__ __forceinline__ const T* wait(int p) {
+    mbar_wait(smem_u32(&bar[p]), (phase >> p) & 1u);
+    phase ^= (1u << p);
+    return buf + p * C;
+  }
+};
+
 // Launch geometry shared by forward, replay and backward so that replay is a
 // bit-identical re-execution of the forward (same label slice, same per-thread
 // duration subsets, same reduction trees).

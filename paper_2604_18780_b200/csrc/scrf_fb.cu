@@ -100,6 +100,7 @@ struct FwdSmem {
   R* T2c;      // [C][Cgm]  T2[c'][c] - Tcmax[c]
   R* Tcmax;    // [Cgm]
   R* a_all;    // [2][C]    exchanged messages (relative to the target frame)
+  uint64_t* a_bar;  // [2]   mbarriers of the a_all exchange
   R* part_m;   // [2][Cgm][WPL]
   R* part_s;
 };
@@ -112,6 +113,7 @@ struct BwdSmem {
   R* Trmax;    // [Cgm]
   R* T2o;      // [Cgm][C]  T2 own rows (grad_T exponent)
   R* d_all;    // [2][C]
+  uint64_t* d_bar;  // [2]
   R* bpart;    // [2][Cgm][WPL][3]
   R* end_acc;  // [K+1][Cgm]
   R* end1;     // [K+1][Cgm]
@@ -138,14 +140,14 @@ template <typename R>
 __host__ __device__ inline size_t fwd_smem_bytes(int K, int C, const Geometry& g) {
   const size_t KC = (size_t)K * g.Cgm;
   return 3 * r16(KC * sizeof(R)) + r16((size_t)C * g.Cgm * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
-         r16(2 * (size_t)C * sizeof(R)) + 2 * r16(2 * (size_t)g.Cgm * g.WPL * sizeof(R));
+         r16(2 * (size_t)C * sizeof(R)) + r16(16) + 2 * r16(2 * (size_t)g.Cgm * g.WPL * sizeof(R));
 }
 
 template <typename R>
 __host__ __device__ inline size_t bwd_extra_smem_bytes(int K, int C, const Geometry& g) {
   const size_t KC = (size_t)K * g.Cgm;
   return 2 * r16(KC * sizeof(R)) + 2 * r16((size_t)g.Cgm * C * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
-         r16(2 * (size_t)C * sizeof(R)) + r16(6 * (size_t)g.Cgm * g.WPL * sizeof(R)) +
+         r16(2 * (size_t)C * sizeof(R)) + r16(16) + r16(6 * (size_t)g.Cgm * g.WPL * sizeof(R)) +
          2 * r16((size_t)(K + 1) * g.Cgm * sizeof(R)) + r16(KC * sizeof(R)) +
          r16((size_t)g.Cgm * C * sizeof(R));
 }
@@ -165,6 +167,7 @@ __device__ void carve_fwd(unsigned char*& p, int K, int C, const Geometry& g, Fw
   s.T2c = carve<R>(p, (size_t)C * g.Cgm);
   s.Tcmax = carve<R>(p, g.Cgm);
   s.a_all = carve<R>(p, 2 * (size_t)C);
+  s.a_bar = carve<uint64_t>(p, 2);
   s.part_m = carve<R>(p, 2 * (size_t)g.Cgm * g.WPL);
   s.part_s = carve<R>(p, 2 * (size_t)g.Cgm * g.WPL);
 }
@@ -177,6 +180,7 @@ __device__ void carve_bwd(unsigned char*& p, int K, int C, const Geometry& g, Bw
   s.T2o = carve<R>(p, (size_t)g.Cgm * C);
   s.Trmax = carve<R>(p, g.Cgm);
   s.d_all = carve<R>(p, 2 * (size_t)C);
+  s.d_bar = carve<uint64_t>(p, 2);
   s.bpart = carve<R>(p, 2 * 3 * (size_t)g.Cgm * g.WPL);
   s.end_acc = carve<R>(p, (size_t)(K + 1) * g.Cgm);
   s.end1 = carve<R>(p, (size_t)(K + 1) * g.Cgm);
@@ -326,19 +330,6 @@ __device__ __forceinline__ void store_part(const Geometry& g, const Ctx& x, R* p
   }
 }
 
-// publish one R value of own label to every CTA of the cluster at buf[idx]
-template <typename R>
-__device__ __forceinline__ void publish(cg::cluster_group& cl, const Geometry& g, const Ctx& x, R* buf, int idx, R v) {
-  if (!x.glane) return;
-  for (int r = x.jj; r < g.G; r += g.GW) {
-    R* dst = cl.map_shared_rank(buf, r);
-    dst[idx] = v;
-  }
-}
-
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
-
 // ----------------------------------------------------------------------------
 // per-position input staging
 //
@@ -387,7 +378,7 @@ __device__ void carve_stage(unsigned char*& p, const Geometry& g, StageSmem<R>& 
 template <typename R, bool BWD>
 struct Stager {
   int P, tb, dir, win_t0;
-  double rE[kStageMax], rG[kStageMax], rn;
+  double rE[kStageMax], rG[kStageMax], rn[2];
   R rg[kStageMax], ra[kStageMax];
 
   __device__ __forceinline__ int pos(int q, int i) const { return tb + dir * (q * P + i); }
@@ -416,11 +407,16 @@ struct Stager {
         }
       }
     }
-    rn = 0.0;
-    if (BWD && x.tid < P) {
-      const int t = pos(q, x.tid);
-      if (t >= win_t0 && t <= win_t0 + a.delta && t >= 0 && t <= a.T)
-        rn = a.ws_n[((size_t)x.b * a.geo.G + x.rank) * (a.delta + 1) + (t - win_t0)];
+    // per-position normaliser: P <= 64 <= 2 * NT positions, at most two per thread
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      rn[r] = 0.0;
+      const int i = x.tid + r * a.geo.NT;
+      if (BWD && i < P) {
+        const int t = pos(q, i);
+        if (t >= win_t0 && t <= win_t0 + a.delta && t >= 0 && t <= a.T)
+          rn[r] = a.ws_n[((size_t)x.b * a.geo.G + x.rank) * (a.delta + 1) + (t - win_t0)];
+      }
     }
   }
 
@@ -442,7 +438,11 @@ struct Stager {
         }
       }
     }
-    if (BWD && x.tid < P) st.n[buf * P + x.tid] = rn;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = x.tid + r * a.geo.NT;
+      if (BWD && i < P) st.n[buf * P + i] = rn[r];
+    }
   }
 
   // shared-memory index of (t, own label cl) / of position t
@@ -496,7 +496,7 @@ struct FwdBook {
 // Runs targets t = t_begin+1 .. t_end. Preconditions: ring holds g[s] for
 // s in (t_begin-K, t_begin]; Fcur = frame of target t_begin+1; n_prev = n_{t_begin}.
 template <typename R, int MODE>
-__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSmem<R>& st, cg::cluster_group& cl,
+__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSmem<R>& st, Xchg<R>& xa,
                           int t_begin, int t_end, double Fcur, double n_prev, FwdBook& bk, int win_t0) {
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm;
@@ -521,6 +521,7 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
   for (int t = t_begin + 1; t <= t_end; ++t) {
     const int par = t & 1;
     sg.advance(a, x, st, t);
+    if (x.tid == 0) xa.arm(par);
     // (A) critical: merge bulk partials (lane-parallel tree) with the k = 1 term, publish a[t]
     if (x.gl) {
       R m = Mth<R>::ninf(), sm = 0;
@@ -534,9 +535,8 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
       R v1 = (s.ring_hi[slot * Cgm + x.cls] + e_hi) + (s.ring_lo[slot * Cgm + x.cls] + e_lo) + s.B2[x.cls];
       ms_merge(m, sm, v1, (R)1);
       R av = ms_value(m, sm);
-      if (x.active) publish(cl, g, x, s.a_all, par * C + c, av);
+      if (x.active) xa.send(par, c, av, x.jj, g.GW, g.G);
     }
-    cluster_arrive();
     // (C) bulk for target t+1 (frame n_{t-1} = n_prev)
     const double Fnext = n_prev;
     R en_hi = 0, en_lo = 0;
@@ -547,9 +547,8 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
       fwd_bulk(a, x, s, t + 1, en_hi, en_lo, m, sm);
       store_part(g, x, s.part_m, s.part_s, (t + 1) & 1, m, sm);
     }
-    cluster_wait();
     // (E) normaliser, gamma, ring write
-    const R* aa = s.a_all + par * C;
+    const R* aa = xa.wait(par);
     R amax = Mth<R>::ninf();
     for (int i = x.lane; i < C; i += 32) amax = fmax(amax, aa[i]);
     amax = group_max(amax, 32);
@@ -712,8 +711,13 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   FwdBook bk;
   bk.N_cur = 0.0;
   bk.dead_at = -1;
+  Xchg<R> xa;
+  xa.buf = s.a_all;
+  xa.bar = s.a_bar;
+  xa.C = C;
+  xa.init(x.tid);
   cl.sync();
-  fwd_sweep<R, MODE_FWD>(a, x, s, st, cl, 0, x.L, 0.0, 0.0, bk, 0);
+  fwd_sweep<R, MODE_FWD>(a, x, s, st, xa, 0, x.L, 0.0, 0.0, bk, 0);
   // checkpoints past the sequence end hold the frozen ring at L
   const int i_first = x.L / a.delta + 1;
   for (int i = i_first; i < a.n_ckpt; ++i) {
@@ -841,7 +845,17 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
   const int c = x.c0 + (x.active ? x.cl : 0);
   load_fwd_tables(a, x, s);
   load_bwd_tables(a, x, sb);
+  Xchg<R> xa, xd;
+  xa.buf = s.a_all;
+  xa.bar = s.a_bar;
+  xa.C = C;
+  xa.init(x.tid);
+  xd.buf = sb.d_all;
+  xd.bar = sb.d_bar;
+  xd.C = C;
+  xd.init(x.tid);
   __syncthreads();
+  cl.sync();
   const double logZ2 = a.logZ_in[x.b] * kLog2e;
   const double up = a.upstream ? a.upstream[x.b] : 1.0;
 
@@ -891,7 +905,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     }
     if (x.tid == 0) a.ws_n[((size_t)x.b * g.G + x.rank) * (a.delta + 1)] = n_t0;
     __syncthreads();
-    fwd_sweep<R, MODE_REPLAY>(a, x, s, st, cl, t0, t1, (t0 == 0) ? 0.0 : n_t0m1, n_t0, bk, t0);
+    fwd_sweep<R, MODE_REPLAY>(a, x, s, st, xa, t0, t1, (t0 == 0) ? 0.0 : n_t0m1, n_t0, bk, t0);
     __syncthreads();
     // all CTAs must finish the replay (they exchange through a_all) before we reuse barriers
     cl.sync();
@@ -916,6 +930,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     for (int t = t1 - 1; t >= t0; --t) {
       const int par = t & 1;
       sg.advance(a, x, st, t);
+      if (x.tid == 0) xd.arm(par);
       // (A) critical k = 1 term for source t
       if (x.gl) {
         R m = Mth<R>::ninf(), sm = 0, ms = 0;
@@ -938,9 +953,8 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
           sb.gBs[x.cl] += M1;
           a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = ms;
         }
-        if (x.active) publish(cl, g, x, sb.d_all, par * C + c, dv);
+        if (x.active) xd.send(par, c, dv, x.jj, g.GW, g.G);
       }
-      cluster_arrive();
       // (C) bulk for source t-1 (frame nd_{t+1})
       SrcVals<R> nxt = cur;
       if (t - 1 >= t0) {
@@ -949,9 +963,8 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
         bwd_bulk(a, x, sb, s.B2, t - 1, nxt, m, sm, ms);
         store_bpart(g, x, sb.bpart, (t - 1) & 1, m, sm, ms);
       }
-      cluster_wait();
       // (E) beta at t, grad_T, v[t], end emission
-      const R* dd = sb.d_all + par * C;
+      const R* dd = xd.wait(par);
       R dmax = Mth<R>::ninf();
       for (int q = x.lane; q < C; q += 32) dmax = fmax(dmax, dd[q]);
       dmax = group_max(dmax, 32);

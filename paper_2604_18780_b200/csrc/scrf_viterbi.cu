@@ -53,7 +53,7 @@ __host__ __device__ inline size_t vit_smem_bytes(int K, int C, const Geometry& g
   n += r16(KC * sizeof(double));      // duration bias
   n += r16(KC * sizeof(int32_t));     // argmax
   n += r16((size_t)C * g.Cgm * sizeof(double));  // T columns
-  n += r16(2 * (size_t)C * sizeof(double));      // exchange
+  n += r16(2 * (size_t)C * sizeof(double)) + r16(16);  // exchange + mbarriers
   n += 3 * r16(2 * (size_t)vit_chunk(g) * g.Cgm * sizeof(double));  // staged S, Ps, Pe rows
   return n;
 }
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
   int32_t* garg = (int32_t*)take(KC * 4);
   double* Tcol = (double*)take((size_t)C * Cgm * 8);
   double* xall = (double*)take(2 * (size_t)C * 8);
+  uint64_t* xbar = (uint64_t*)take(16);
   const int P = vit_chunk(g);
   double* stS = (double*)take(2 * (size_t)P * Cgm * 8);
   double* stPs = (double*)take(2 * (size_t)P * Cgm * 8);
@@ -105,7 +106,8 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
   const double* S = a.S + (size_t)b * (a.T + 1) * C;
   const double* ps = a.ps ? a.ps + (size_t)b * a.T * C : nullptr;
   const double* pe = a.pe ? a.pe + (size_t)b * a.T * C : nullptr;
-  double* dvr = a.dvring + (size_t)b * K * C;
+  // this CTA's private copy of the full message history (for the tie re-scan)
+  double* dvr = a.dvring + ((size_t)b * g.G + rank) * K * C;
   int32_t* bp = a.bp + (size_t)b * (a.T + 1) * C;
 
   // chunk q holds positions [q*P, (q+1)*P); registers carry chunk q+2 while q is consumed
@@ -188,9 +190,16 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
     }
   };
 
+  Xchg<double> xv;
+  xv.buf = xall;
+  xv.bar = xbar;
+  xv.C = C;
+  xv.init(tid);
   // position 0: every label starts from the virtual source with message 0
-  for (int i = tid; i < C; i += g.NT) xall[i] = 0.0;
-  for (int i = tid; i < Cg; i += g.NT) dvr[c0 + i] = 0.0;
+  for (int i = tid; i < C; i += g.NT) {
+    xall[i] = 0.0;
+    dvr[i] = 0.0;
+  }
   __syncthreads();
   gamma_step(xall, 0);
   __syncthreads();
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
       vload(t / P + 2);
       __syncthreads();
     }
+    if (tid == 0) xv.arm(par);
     const double St = stS[vidx(t, cls)];
     const double Pet = stPe[vidx(t, cls)];
     if (active) {
@@ -259,11 +269,11 @@ __global__ void __launch_bounds__(1024) vit_kernel(VitArgs a) {
         }
       }
       bp[(size_t)t * C + c] = (bk << 16) | src;
-      dvr[(size_t)(t % K) * C + c] = best;
-      for (int r = 0; r < g.G; ++r) cl.map_shared_rank(xall, r)[par * C + c] = best;
+      xv.send(par, c, best, 0, 1, g.G);
     }
-    cl.sync();
-    gamma_step(xall + par * C, t);
+    const double* xin = xv.wait(par);
+    for (int i = tid; i < C; i += g.NT) dvr[(size_t)(t % K) * C + i] = xin[i];
+    gamma_step(xin, t);
     __syncthreads();
   }
   __threadfence();
