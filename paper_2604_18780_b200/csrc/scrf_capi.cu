@@ -63,8 +63,8 @@ Geometry make_geo(int G, int K, int C) {
   g.Cgm = (C + G - 1) / G;
   int tpl = env_int("SCRF_TPL", 0);
   if (tpl <= 0) {
-    // ~4 durations per thread, at most 1024 threads per CTA
-    tpl = pow2_ceil(K / 4 > 0 ? K / 4 : 1);
+    // ~8 durations per thread, at most 1024 threads per CTA
+    tpl = pow2_ceil(K / 8 > 0 ? K / 8 : 1);
     int cap = pow2_floor(1024 / g.Cgm > 0 ? 1024 / g.Cgm : 1);
     if (tpl > cap) tpl = cap;
   }

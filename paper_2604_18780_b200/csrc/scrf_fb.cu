@@ -2,32 +2,50 @@
 //
 // Replaces the reference's hot path `pkg/src/streamcrf/streaming.py`:
 //   streaming_forward  (:155-229)  -> fwd_kernel
-//   recompute_alpha    (:232-261)  -> fwd_sweep<REPLAY> inside bwd_kernel
-//   streaming_backward (:264-408)  -> bwd_kernel + finalize_kernel + reduce_kernel
-//   finalize_marginals (diagnostics.py:54-79) -> finalize_kernel
+//   recompute_alpha    (:232-261)  -> fwd_sweep<MODE_REPLAY> inside bwd_kernel
+//   streaming_backward (:264-408)  -> bwd_kernel + finalize_kernel + reduce_partials_kernel
+//   finalize_marginals (diagnostics.py:54-79) -> finalize_kernel / boundary_kernel
 //
 // Algorithm: the exact factorisation of the reference recursion
 //   gamma[s,c] = LSE_c' (alpha[s,c'] + T[c',c])              (C^2 per position)
 //   alpha[t,c] = LSE_k  (gamma[t-k,c] + h[t,k,c])             (K*C per position)
 // with h = S[t,c]-S[t-k,c] + B[k-1,c] (+Ps[t-k,c] + Pe[t-1,c]); the backward is the
 // mirror image (delta = LSE_k(h + beta[t+k]); beta[t,c'] = LSE_c(T[c',c] + delta[t,c]))
-// and every joint marginal the reference materialises as mu[b,k,c,c'] is consumed
-// in its two contracted forms:
+// and the joint marginals mu[b,k,c,c'] the reference materialises are consumed in
+// their two contracted forms:
 //   M[t,k,c]     = sum_c' mu = exp(gamma[t,c] + h + beta[t+k,c] - logZ)   (durations, S, coverage)
 //   grad_T[c',c] = sum_t exp(alpha[t,c'] + T[c',c] + delta[t,c] - logZ).
 //
-// Parallel layout: one thread-block cluster per sequence; CTA r of the cluster owns
-// a contiguous label slice. The K-term sum of a label only needs that label's
-// history, so the ring of per-source terms g[s,c] lives in the owning CTA's shared
-// memory; the only cross-CTA traffic per position is the C-vector of new messages
-// (DSMEM stores + one split cluster barrier). The bulk of the K*C work for position
-// t+1 (durations k >= 2, which do not depend on position t) is computed between the
-// barrier's arrive and wait, hiding the cluster round trip.
+// Parallel layout: one thread-block cluster per sequence; CTA r owns a label slice.
+// The K-term sum of a label only needs that label's history, so the ring of
+// per-source terms g[s,c] lives in the owning CTA's shared memory (label-major,
+// (hi, lo) pairs -> one conflict-free LDS.64 per term). The only cross-CTA traffic
+// per position is the C-vector of new messages, sent with st.async + mbarrier
+// (scrf_common.cuh). The K-1 durations k >= 2 of position t+1 do not depend on
+// position t, so they are summed while the exchange of position t is in flight.
+//
+// Inner-loop numerics: every thread of a label uses the same reference value
+// m_ref = term(k = 2) (computable by all of them), so the K-term log-sum-exp is a
+// single pass of ex2(x - m_ref) with plain-sum reductions; an exact own-max path
+// takes over only if some term exceeds m_ref by more than kRefSlack (log2 units).
 #include <stdint.h>
 
 #include "scrf_common.cuh"
 
 namespace scrf {
+
+constexpr float kRefSlack = 60.f;
+
+template <typename R>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using T = float2;
+};
+template <>
+struct Vec2<double> {
+  using T = double2;
+};
 
 // ----------------------------------------------------------------------------
 // kernel arguments
@@ -58,18 +76,18 @@ struct Args {
   double* logZ;
   double* N;
   int32_t* dead_at;
-  R* tail_alpha;      // [B][K][C]
-  double* tail_n;     // [B][K]
+  R* tail_alpha;  // [B][K][C]
+  double* tail_n; // [B][K]
   // backward inputs / outputs
   const double* logZ_in;
   const double* upstream;
-  R* ws_alpha;       // [B][delta+1][C]
-  R* ws_gamma;       // [B][delta+1][C]
-  double* ws_n;      // [B][G][delta+1]
-  R* start_g;        // [B][T+1][C]  mass of segments starting at t (working type)
-  R* end_g;          // [B][T+1][C]  mass of segments ending at t
-  double* gT_part;   // [B][C][C]
-  double* gB_part;   // [B][K][C]
+  R* ws_alpha;    // [B][delta+1][C]
+  R* ws_gamma;    // [B][delta+1][C]
+  double* ws_n;   // [B][G][delta+1]
+  R* start_g;     // [B][T+1][C]  mass of segments starting at t
+  R* end_g;       // [B][T+1][C]  mass of segments ending at t
+  double* gT_part;  // [B][C][C]
+  double* gB_part;  // [B][K][C]
 };
 
 template <typename R>
@@ -83,6 +101,7 @@ __device__ __forceinline__ size_t ck_off(const Args<R>& a, int b, int i) {
 struct Ctx {
   int b, rank, c0, Cg, L;
   int tid, cl, j, lane, warp, jj;  // jj = index within the label's first lane group
+  int wl;                           // warp index within the label
   int cls;                          // cl if active else 0 (safe shared-memory index)
   bool active;                      // cl < Cg
   bool gl;                          // j < GW: label's first lane group (warp-uniform predicate)
@@ -94,36 +113,30 @@ struct Ctx {
 
 template <typename R>
 struct FwdSmem {
-  R* ring_hi;  // [K][Cgm]
-  R* ring_lo;
-  R* B2;       // [K][Cgm]  duration bias * log2e
-  R* T2c;      // [C][Cgm]  T2[c'][c] - Tcmax[c]
-  R* Tcmax;    // [Cgm]
-  R* a_all;    // [2][C]    exchanged messages (relative to the target frame)
-  uint64_t* a_bar;  // [2]   mbarriers of the a_all exchange
-  R* part_m;   // [2][Cgm][WPL]
-  R* part_s;
+  typename Vec2<R>::T* ring;  // [Cgm][K]  g (hi, lo)
+  R* B2;                      // [Cgm][K]  duration bias * log2e
+  R* T2c;                     // [C][Cgm]  T2[c'][c] - Tcmax[c]
+  R* Tcmax;                   // [Cgm]
+  R* a_all;                   // [2][C]    exchanged messages (relative to the target frame)
+  uint64_t* a_bar;            // [2]
+  R* part;                    // [2][Cgm][WPL][2]  (m, s) bulk partials
 };
 
 template <typename R>
 struct BwdSmem {
-  R* vr_hi;    // [K][Cgm]  beta-side terms v[e,c]
-  R* vr_lo;
-  R* T2r;      // [Cgm][C]  T2[c'][c] - Trmax[c'] (own rows c')
-  R* Trmax;    // [Cgm]
-  R* T2o;      // [Cgm][C]  T2 own rows (grad_T exponent)
-  R* d_all;    // [2][C]
-  uint64_t* d_bar;  // [2]
-  R* bpart;    // [2][Cgm][WPL][3]
-  R* end_acc;  // [K+1][Cgm]
-  R* end1;     // [K+1][Cgm]
-  R* gBs;      // [K][Cgm]
-  R* gTs;      // [Cgm][C]
+  typename Vec2<R>::T* vr;  // [Cgm][K]  beta-side terms v[e,c] (hi, lo)
+  R* T2r;                   // [Cgm][C]  T2[c'][c] - Trmax[c'] (own rows c')
+  R* T2o;                   // [Cgm][C]  T2 own rows (grad_T exponent)
+  R* Trmax;                 // [Cgm]
+  R* d_all;                 // [2][C]
+  uint64_t* d_bar;          // [2]
+  R* bpart;                 // [2][Cgm][WPL][3]  (m, s, msum)
+  R* end_acc;               // [Cgm][K+1]
+  R* end1;                  // [Cgm][K+1]
+  R* gBs;                   // [Cgm][K]
+  R* gTs;                   // [Cgm][C]
 };
 
-__device__ __forceinline__ double ld_or0(const double* p, size_t i) { return p ? __ldg(p + i) : 0.0; }
-
-// S[b,t,c] * log2e etc.
 __device__ __forceinline__ double S2(const Ctx& x, int C, int t, int c) { return __ldg(x.S + (size_t)t * C + c) * kLog2e; }
 __device__ __forceinline__ double PS2(const Ctx& x, int C, int t, int c) { return x.ps ? __ldg(x.ps + (size_t)t * C + c) * kLog2e : 0.0; }
 __device__ __forceinline__ double PE2(const Ctx& x, int C, int t, int c) {
@@ -131,25 +144,24 @@ __device__ __forceinline__ double PE2(const Ctx& x, int C, int t, int c) {
 }
 
 // ----------------------------------------------------------------------------
-// shared-memory carving
+// shared-memory carving (byte counts mirror the carve functions exactly)
 
 __host__ __device__ inline size_t r16(size_t n) { return (n + 15) & ~(size_t)15; }
 
-// byte counts mirror carve_fwd / carve_bwd exactly (each chunk rounded to 16 B)
 template <typename R>
 __host__ __device__ inline size_t fwd_smem_bytes(int K, int C, const Geometry& g) {
   const size_t KC = (size_t)K * g.Cgm;
-  return 3 * r16(KC * sizeof(R)) + r16((size_t)C * g.Cgm * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
-         r16(2 * (size_t)C * sizeof(R)) + r16(16) + 2 * r16(2 * (size_t)g.Cgm * g.WPL * sizeof(R));
+  return r16(KC * 2 * sizeof(R)) + r16(KC * sizeof(R)) + r16((size_t)C * g.Cgm * sizeof(R)) +
+         r16(g.Cgm * sizeof(R)) + r16(2 * (size_t)C * sizeof(R)) + r16(16) +
+         r16(4 * (size_t)g.Cgm * g.WPL * sizeof(R));
 }
 
 template <typename R>
 __host__ __device__ inline size_t bwd_extra_smem_bytes(int K, int C, const Geometry& g) {
   const size_t KC = (size_t)K * g.Cgm;
-  return 2 * r16(KC * sizeof(R)) + 2 * r16((size_t)g.Cgm * C * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
+  return r16(KC * 2 * sizeof(R)) + 2 * r16((size_t)g.Cgm * C * sizeof(R)) + r16(g.Cgm * sizeof(R)) +
          r16(2 * (size_t)C * sizeof(R)) + r16(16) + r16(6 * (size_t)g.Cgm * g.WPL * sizeof(R)) +
-         2 * r16((size_t)(K + 1) * g.Cgm * sizeof(R)) + r16(KC * sizeof(R)) +
-         r16((size_t)g.Cgm * C * sizeof(R));
+         2 * r16((size_t)(K + 1) * g.Cgm * sizeof(R)) + r16(KC * sizeof(R)) + r16((size_t)g.Cgm * C * sizeof(R));
 }
 
 template <typename T>
@@ -161,27 +173,26 @@ __device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
 
 template <typename R>
 __device__ void carve_fwd(unsigned char*& p, int K, int C, const Geometry& g, FwdSmem<R>& s) {
-  s.ring_hi = carve<R>(p, (size_t)K * g.Cgm);
-  s.ring_lo = carve<R>(p, (size_t)K * g.Cgm);
+  using R2 = typename Vec2<R>::T;
+  s.ring = carve<R2>(p, (size_t)K * g.Cgm);
   s.B2 = carve<R>(p, (size_t)K * g.Cgm);
   s.T2c = carve<R>(p, (size_t)C * g.Cgm);
   s.Tcmax = carve<R>(p, g.Cgm);
   s.a_all = carve<R>(p, 2 * (size_t)C);
   s.a_bar = carve<uint64_t>(p, 2);
-  s.part_m = carve<R>(p, 2 * (size_t)g.Cgm * g.WPL);
-  s.part_s = carve<R>(p, 2 * (size_t)g.Cgm * g.WPL);
+  s.part = carve<R>(p, 4 * (size_t)g.Cgm * g.WPL);
 }
 
 template <typename R>
 __device__ void carve_bwd(unsigned char*& p, int K, int C, const Geometry& g, BwdSmem<R>& s) {
-  s.vr_hi = carve<R>(p, (size_t)K * g.Cgm);
-  s.vr_lo = carve<R>(p, (size_t)K * g.Cgm);
+  using R2 = typename Vec2<R>::T;
+  s.vr = carve<R2>(p, (size_t)K * g.Cgm);
   s.T2r = carve<R>(p, (size_t)g.Cgm * C);
   s.T2o = carve<R>(p, (size_t)g.Cgm * C);
   s.Trmax = carve<R>(p, g.Cgm);
   s.d_all = carve<R>(p, 2 * (size_t)C);
   s.d_bar = carve<uint64_t>(p, 2);
-  s.bpart = carve<R>(p, 2 * 3 * (size_t)g.Cgm * g.WPL);
+  s.bpart = carve<R>(p, 6 * (size_t)g.Cgm * g.WPL);
   s.end_acc = carve<R>(p, (size_t)(K + 1) * g.Cgm);
   s.end1 = carve<R>(p, (size_t)(K + 1) * g.Cgm);
   s.gBs = carve<R>(p, (size_t)K * g.Cgm);
@@ -202,7 +213,8 @@ __device__ Ctx make_ctx(const Args<R>& a, const cg::cluster_group& cl) {
   x.j = x.tid % g.TPL;
   x.lane = x.tid & 31;
   x.warp = x.tid >> 5;
-  x.jj = x.j;  // meaningful when glane
+  x.wl = x.j >> 5;
+  x.jj = x.j;
   x.active = x.cl < x.Cg;
   x.cls = x.active ? x.cl : 0;
   x.gl = x.j < g.GW;
@@ -219,10 +231,9 @@ __device__ void load_fwd_tables(const Args<R>& a, const Ctx& x, FwdSmem<R>& s) {
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C;
   for (int i = x.tid; i < K * g.Cgm; i += g.NT) {
-    int k = i / g.Cgm, c = i % g.Cgm;
-    s.B2[i] = (c < x.Cg) ? (R)(a.dur[(size_t)k * C + x.c0 + c] * kLog2e) : (R)0;
+    const int cc = i / K, k = i % K;
+    s.B2[i] = (cc < x.Cg) ? (R)(a.dur[(size_t)k * C + x.c0 + cc] * kLog2e) : (R)0;
   }
-  // column max of T for own labels
   for (int c = x.tid; c < g.Cgm; c += g.NT) {
     double m = -CUDART_INF;
     if (c < x.Cg)
@@ -231,7 +242,7 @@ __device__ void load_fwd_tables(const Args<R>& a, const Ctx& x, FwdSmem<R>& s) {
   }
   __syncthreads();
   for (int i = x.tid; i < C * g.Cgm; i += g.NT) {
-    int cp = i / g.Cgm, c = i % g.Cgm;
+    const int cp = i / g.Cgm, c = i % g.Cgm;
     s.T2c[i] = (c < x.Cg) ? (R)(a.trans[(size_t)cp * C + x.c0 + c] * kLog2e) - s.Tcmax[c] : (R)0;
   }
 }
@@ -248,8 +259,8 @@ __device__ void load_bwd_tables(const Args<R>& a, const Ctx& x, BwdSmem<R>& s) {
   }
   __syncthreads();
   for (int i = x.tid; i < g.Cgm * C; i += g.NT) {
-    int r = i / C, c = i % C;
-    R t2 = (r < x.Cg) ? (R)(a.trans[(size_t)(x.c0 + r) * C + c] * kLog2e) : (R)0;
+    const int r = i / C, c = i % C;
+    const R t2 = (r < x.Cg) ? (R)(a.trans[(size_t)(x.c0 + r) * C + c] * kLog2e) : (R)0;
     s.T2o[i] = t2;
     s.T2r[i] = (r < x.Cg) ? t2 - s.Trmax[r] : (R)0;
     s.gTs[i] = (R)0;
@@ -261,8 +272,7 @@ __device__ void load_bwd_tables(const Args<R>& a, const Ctx& x, BwdSmem<R>& s) {
   for (int i = x.tid; i < K * g.Cgm; i += g.NT) s.gBs[i] = (R)0;
 }
 
-// gamma-tilde of own label `cl` from exchanged alpha-hat values (relative, <= 0).
-// Executed by the label's first lane group (width GW); result valid in all its lanes.
+// gamma-tilde of own label `cl` from alpha-hat values (<= 0), by the label's first lane group.
 template <typename R>
 __device__ __forceinline__ R gamma_from_alpha(const R* ahat, const R* T2c, const R* Tcmax, int C, int Cgm, int cl,
                                               int jj, int GW) {
@@ -282,62 +292,96 @@ __device__ __forceinline__ R gamma_from_alpha(const R* ahat, const R* T2c, const
   return Tcmax[cl] + Mth<R>::lg2(s);
 }
 
-// Bulk (durations k >= 2) partial for target `tt` of own label: thread j owns k = 1 + j + i*TPL.
+// ----------------------------------------------------------------------------
+// bulk (durations k >= 2) partial of one target / source
+//
+// Thread j of a label owns durations k = 2 + j + i*TPL. All threads share the
+// reference m_ref = term(k = 2). Returns the lane-group-reduced (m, s[, msum]):
+// m == m_ref on the fast path.
+
 template <typename R>
-__device__ __forceinline__ void fwd_bulk(const Args<R>& a, const Ctx& x, const FwdSmem<R>& s, int tt, R e_hi, R e_lo,
-                                         R& m_out, R& s_out) {
-  const Geometry& g = a.geo;
-  const int K = a.K, Cgm = g.Cgm;
-  const int kmax = min(K, tt);
-  R m = Mth<R>::ninf(), sum = 0;
-  int k0 = 1 + x.j;
-  if (k0 == 1) k0 += g.TPL;  // k = 1 is the critical term
-  if (x.active && k0 <= kmax) {
-    const int step = g.TPL % K;
-    int slot0 = (tt - k0) % K;
-    int slot = slot0;
-    for (int k = k0; k <= kmax; k += g.TPL) {
-      R v = (s.ring_hi[slot * Cgm + x.cl] + e_hi) + (s.ring_lo[slot * Cgm + x.cl] + e_lo) + s.B2[(k - 1) * Cgm + x.cl];
-      m = fmax(m, v);
-      slot -= step;
-      if (slot < 0) slot += K;
-    }
-    if (m != Mth<R>::ninf()) {
-      slot = slot0;
-      for (int k = k0; k <= kmax; k += g.TPL) {
-        R v = (s.ring_hi[slot * Cgm + x.cl] + e_hi) + (s.ring_lo[slot * Cgm + x.cl] + e_lo) + s.B2[(k - 1) * Cgm + x.cl];
-        sum += Mth<R>::ex2(v - m);
-        slot -= step;
-        if (slot < 0) slot += K;
-      }
-    }
-  }
-  group_ms(m, sum, g.GW);
-  m_out = m;
-  s_out = sum;
+__device__ __forceinline__ R fwd_term(const typename Vec2<R>::T& r, R e_hi, R e_lo, R b2) {
+  return (r.x + e_hi) + (r.y + e_lo) + b2;
 }
 
 template <typename R>
-__device__ __forceinline__ void store_part(const Geometry& g, const Ctx& x, R* pm, R* ps, int par, R m, R s) {
-  // called by all threads after group reduction; one lane per (label, warp) stores
-  if (!x.active) return;
-  const int wl = x.j / 32;
-  const bool first = (g.TPL >= 32) ? (x.lane == 0) : (x.j == 0);
-  if (first) {
-    size_t i = ((size_t)par * g.Cgm + x.cl) * g.WPL + wl;
-    pm[i] = m;
-    ps[i] = s;
+__device__ __forceinline__ void fwd_bulk(const Args<R>& a, const Ctx& x, const FwdSmem<R>& s, int tt, int slot2,
+                                         R e_hi, R e_lo, R& m_out, R& s_out) {
+  using R2 = typename Vec2<R>::T;
+  const Geometry& g = a.geo;
+  const int K = a.K;
+  const int kmax = min(K, tt);
+  const R2* rg = s.ring + (size_t)x.cls * K;
+  const R* b2 = s.B2 + (size_t)x.cls * K;
+  R mref = Mth<R>::ninf(), sum = 0, dmax = Mth<R>::ninf();
+  bool slow = false;
+  const int k0 = 2 + x.j;
+  const int stepK = g.TPL % K;
+  int slot0 = slot2 - x.j % K;
+  if (slot0 < 0) slot0 += K;
+  if (kmax >= 2) {
+    mref = fwd_term<R>(rg[slot2], e_hi, e_lo, b2[1]);
+    slow = (mref == Mth<R>::ninf());
+    if (x.active && !slow && k0 <= kmax) {
+      int slot = slot0;
+      R acc0 = 0, acc1 = 0;
+      int k = k0;
+      for (; k + g.TPL <= kmax; k += 2 * g.TPL) {
+        const R x0 = fwd_term<R>(rg[slot], e_hi, e_lo, b2[k - 1]) - mref;
+        slot -= stepK;
+        if (slot < 0) slot += K;
+        const R x1 = fwd_term<R>(rg[slot], e_hi, e_lo, b2[k + g.TPL - 1]) - mref;
+        slot -= stepK;
+        if (slot < 0) slot += K;
+        dmax = fmax(dmax, fmax(x0, x1));
+        acc0 += Mth<R>::ex2(x0);
+        acc1 += Mth<R>::ex2(x1);
+      }
+      if (k <= kmax) {
+        const R x0 = fwd_term<R>(rg[slot], e_hi, e_lo, b2[k - 1]) - mref;
+        dmax = fmax(dmax, x0);
+        acc0 += Mth<R>::ex2(x0);
+      }
+      sum = acc0 + acc1;
+      slow = dmax > (R)kRefSlack;
+    }
   }
+  R m = mref;
+  if (__any_sync(0xffffffffu, slow)) {
+    // exact path: own maximum over the thread's durations
+    m = Mth<R>::ninf();
+    sum = 0;
+    if (x.active && k0 <= kmax) {
+      int slot = slot0;
+      for (int k = k0; k <= kmax; k += g.TPL) {
+        m = fmax(m, fwd_term<R>(rg[slot], e_hi, e_lo, b2[k - 1]));
+        slot -= stepK;
+        if (slot < 0) slot += K;
+      }
+      if (m != Mth<R>::ninf()) {
+        slot = slot0;
+        for (int k = k0; k <= kmax; k += g.TPL) {
+          sum += Mth<R>::ex2(fwd_term<R>(rg[slot], e_hi, e_lo, b2[k - 1]) - m);
+          slot -= stepK;
+          if (slot < 0) slot += K;
+        }
+      }
+    }
+    group_ms(m, sum, g.GW);
+  } else {
+    sum = group_sum(sum, g.GW);
+  }
+  m_out = m;
+  s_out = sum;
 }
 
 // ----------------------------------------------------------------------------
 // per-position input staging
 //
 // Every position needs a handful of fp64 inputs per own label (prefix sums and
-// projections, and in the backward the replayed window values). Loading them on
-// the critical path costs a full HBM/L2 round trip per position, so they are
-// staged in chunks of P positions: chunk q+2 is loaded into registers while chunk
-// q is consumed, then parked in one of two shared-memory chunk buffers.
+// projections, and in the backward the replayed window values). They are staged
+// in chunks of P positions: chunk q+2 is loaded into registers while chunk q is
+// consumed, then parked in one of two shared-memory chunk buffers.
 //   E0[t,c] = S2[t,c] + Pe2[t-1,c]     (forward target term, backward v[t] base)
 //   G0[t,c] = -S2[t,c] + Ps2[t,c]      (forward g[t] base, backward w[t] base)
 // backward only: gam[t,c] = gamma~, ahat[t,c] = alpha-hat, n[t] (window store).
@@ -377,7 +421,7 @@ __device__ void carve_stage(unsigned char*& p, const Geometry& g, StageSmem<R>& 
 
 template <typename R, bool BWD>
 struct Stager {
-  int P, tb, dir, win_t0;
+  int P, lgP, tb, dir, win_t0;
   double rE[kStageMax], rG[kStageMax], rn[2];
   R rg[kStageMax], ra[kStageMax];
 
@@ -407,9 +451,8 @@ struct Stager {
         }
       }
     }
-    // per-position normaliser: P <= 64 <= 2 * NT positions, at most two per thread
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 2; ++r) {  // P <= 64 <= 2 * NT positions
       rn[r] = 0.0;
       const int i = x.tid + r * a.geo.NT;
       if (BWD && i < P) {
@@ -445,21 +488,17 @@ struct Stager {
     }
   }
 
-  // shared-memory index of (t, own label cl) / of position t
-  __device__ __forceinline__ size_t idx(int t, int cl, int Cgm) const {
+  // shared-memory row of position t (P is a power of two)
+  __device__ __forceinline__ int row(int t) const {
     const int d = dir * (t - tb);
-    const int q = d / P, i = d - q * P;
-    return ((size_t)(q & 1) * P + i) * Cgm + cl;
+    return (((d >> lgP) & 1) << lgP) + (d & (P - 1));
   }
-  __device__ __forceinline__ int nidx(int t) const {
-    const int d = dir * (t - tb);
-    const int q = d / P, i = d - q * P;
-    return (q & 1) * P + i;
-  }
+  __device__ __forceinline__ size_t idx(int t, int cl, int Cgm) const { return (size_t)row(t) * Cgm + cl; }
 
   // prime chunks 0 and 1 in shared memory and chunk 2 in registers (ends with a barrier)
   __device__ void begin(const Args<R>& a, const Ctx& x, StageSmem<R>& st, int tb_, int dir_, int win) {
     P = stage_chunk(a.geo);
+    lgP = 31 - __clz(P);
     tb = tb_;
     dir = dir_;
     win_t0 = win;
@@ -474,8 +513,8 @@ struct Stager {
   // call at the top of the iteration that processes position t (before any use)
   __device__ __forceinline__ void advance(const Args<R>& a, const Ctx& x, StageSmem<R>& st, int t) {
     const int d = dir * (t - tb);
-    if (d > 0 && d % P == 0) {
-      const int q = d / P;
+    if (d > 0 && (d & (P - 1)) == 0) {
+      const int q = d >> lgP;
       store(a, x, st, q + 1);
       load(a, x, q + 2);
     }
@@ -493,28 +532,76 @@ struct FwdBook {
   int dead_at;
 };
 
+template <typename R>
+__device__ __forceinline__ void store_part(const Geometry& g, const Ctx& x, R* part, int par, R m, R s) {
+  if (!x.active) return;
+  const bool first = (g.TPL >= 32) ? (x.lane == 0) : (x.j == 0);
+  if (first) {
+    const size_t i = (((size_t)par * g.Cgm + x.cl) * g.WPL + x.wl) * 2;
+    part[i] = m;
+    part[i + 1] = s;
+  }
+}
+
+// merge of the stored per-warp partials by the label's first lane group
+template <typename R>
+__device__ __forceinline__ void merge_parts(const Geometry& g, const Ctx& x, const R* part, int par, R& m, R& s) {
+  m = Mth<R>::ninf();
+  s = 0;
+  if (x.active && x.jj < g.WPL) {
+    const size_t i = (((size_t)par * g.Cgm + x.cl) * g.WPL + x.jj) * 2;
+    m = part[i];
+    s = part[i + 1];
+  }
+  if (g.WPL > 1) {
+    // fast path: every warp used the shared reference
+    const R m0 = __shfl_sync(0xffffffffu, m, 0, g.GW);
+    const bool same = (x.jj >= g.WPL) || (m == m0);
+    if (__all_sync(0xffffffffu, same)) {
+      s = group_sum(s, g.GW);
+      m = m0;
+    } else {
+      group_ms(m, s, g.GW);
+    }
+  }
+}
+
+// log2(exp2(m) * s + exp2(x1)) without overflow
+template <typename R>
+__device__ __forceinline__ R add_term(R m, R s, R x1) {
+  if (m == Mth<R>::ninf() || !(s > (R)0)) return x1;
+  if (x1 == Mth<R>::ninf()) return m + Mth<R>::lg2(s);
+  const R d = x1 - m;
+  if (d <= (R)kRefSlack) return m + Mth<R>::lg2(s + Mth<R>::ex2(d));
+  return x1 + Mth<R>::lg2((R)1 + s * Mth<R>::ex2(-d));
+}
+
 // Runs targets t = t_begin+1 .. t_end. Preconditions: ring holds g[s] for
 // s in (t_begin-K, t_begin]; Fcur = frame of target t_begin+1; n_prev = n_{t_begin}.
 template <typename R, int MODE>
-__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSmem<R>& st, Xchg<R>& xa,
-                          int t_begin, int t_end, double Fcur, double n_prev, FwdBook& bk, int win_t0) {
+__device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSmem<R>& st, Xchg<R>& xa, int t_begin,
+                          int t_end, double Fcur, double n_prev, FwdBook& bk, int win_t0) {
+  using R2 = typename Vec2<R>::T;
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm;
-  const int c = x.c0 + (x.active ? x.cl : 0);
+  const int c = x.c0 + x.cls;
   if (t_end <= t_begin) return;
   Stager<R, false> sg;
   sg.begin(a, x, st, t_begin, +1, 0);
+  R2* ring = s.ring + (size_t)x.cls * K;
 
-  // e for target t_begin+1
+  // slots of positions t-1 and t-2 for the current target t (incremental mod K)
+  int sl1 = t_begin % K;            // (t-1) mod K for t = t_begin+1
+  int sl2 = (t_begin + K - 1) % K;  // (t-2) mod K
+  int next_ck = (t_begin / a.delta + 1) * a.delta;
+
+  // e for target t_begin+1, bulk partial for it
   R e_hi, e_lo;
-  {
-    double e = st.E0[sg.idx(t_begin + 1, x.cls, Cgm)] - Fcur;
-    split(e, e_hi, e_lo);
-  }
+  split(st.E0[sg.idx(t_begin + 1, x.cls, Cgm)] - Fcur, e_hi, e_lo);
   {
     R m, sm;
-    fwd_bulk(a, x, s, t_begin + 1, e_hi, e_lo, m, sm);
-    store_part(g, x, s.part_m, s.part_s, (t_begin + 1) & 1, m, sm);
+    fwd_bulk(a, x, s, t_begin + 1, sl2, e_hi, e_lo, m, sm);
+    store_part(g, x, s.part, (t_begin + 1) & 1, m, sm);
   }
   __syncthreads();
 
@@ -522,30 +609,22 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
     const int par = t & 1;
     sg.advance(a, x, st, t);
     if (x.tid == 0) xa.arm(par);
-    // (A) critical: merge bulk partials (lane-parallel tree) with the k = 1 term, publish a[t]
+    // (A) critical: bulk partials + the k = 1 term -> a[t]; send it to the cluster
     if (x.gl) {
-      R m = Mth<R>::ninf(), sm = 0;
-      if (x.active && x.jj < g.WPL) {
-        size_t i = ((size_t)par * Cgm + x.cl) * g.WPL + x.jj;
-        m = s.part_m[i];
-        sm = s.part_s[i];
-      }
-      group_ms(m, sm, g.GW);
-      const int slot = (t - 1) % K;
-      R v1 = (s.ring_hi[slot * Cgm + x.cls] + e_hi) + (s.ring_lo[slot * Cgm + x.cls] + e_lo) + s.B2[x.cls];
-      ms_merge(m, sm, v1, (R)1);
-      R av = ms_value(m, sm);
+      R m, sm;
+      merge_parts(g, x, s.part, par, m, sm);
+      const R x1 = fwd_term<R>(ring[sl1], e_hi, e_lo, s.B2[(size_t)x.cls * K]);
+      const R av = add_term(m, sm, x1);
       if (x.active) xa.send(par, c, av, x.jj, g.GW, g.G);
     }
-    // (C) bulk for target t+1 (frame n_{t-1} = n_prev)
+    // (C) bulk for target t+1 (frame n_{t-1} = n_prev) while the exchange is in flight
     const double Fnext = n_prev;
     R en_hi = 0, en_lo = 0;
     if (t < t_end) {
-      double e = st.E0[sg.idx(t + 1, x.cls, Cgm)] - Fnext;
-      split(e, en_hi, en_lo);
+      split(st.E0[sg.idx(t + 1, x.cls, Cgm)] - Fnext, en_hi, en_lo);
       R m, sm;
-      fwd_bulk(a, x, s, t + 1, en_hi, en_lo, m, sm);
-      store_part(g, x, s.part_m, s.part_s, (t + 1) & 1, m, sm);
+      fwd_bulk(a, x, s, t + 1, sl1, en_hi, en_lo, m, sm);
+      store_part(g, x, s.part, (t + 1) & 1, m, sm);
     }
     // (E) normaliser, gamma, ring write
     const R* aa = xa.wait(par);
@@ -554,13 +633,11 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
     amax = group_max(amax, 32);
     const bool dead = (amax == Mth<R>::ninf());
     const double n_t = dead ? Fcur : Fcur + (double)amax;
+    const int slt = (sl1 + 1 == K) ? 0 : sl1 + 1;  // t mod K
     if (x.gl) {
-      R ahat_own = dead ? Mth<R>::ninf() : aa[c] - amax;
-      R gam;
-      if (dead) {
-        gam = Mth<R>::ninf();
-      } else {
-        // alpha-hat row in registers is read straight from the exchange buffer
+      const R ahat_own = dead ? Mth<R>::ninf() : aa[c] - amax;
+      R gam = Mth<R>::ninf();
+      if (!dead) {
         R ssum = 0;
         for (int cp = x.jj; cp < C; cp += g.GW) ssum += Mth<R>::ex2((aa[cp] - amax) + s.T2c[(size_t)cp * Cgm + x.cls]);
         ssum = group_sum(ssum, g.GW);
@@ -579,14 +656,12 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
         }
       }
       if (x.active && x.jj == 0) {
-        double gv = (gam == Mth<R>::ninf()) ? -CUDART_INF : n_t + (double)gam + st.G0[sg.idx(t, x.cl, Cgm)];
-        R hi, lo;
-        split(gv, hi, lo);
-        const int slot = t % K;
-        s.ring_hi[slot * Cgm + x.cl] = hi;
-        s.ring_lo[slot * Cgm + x.cl] = lo;
+        const double gv = (gam == Mth<R>::ninf()) ? -CUDART_INF : n_t + (double)gam + st.G0[sg.idx(t, x.cl, Cgm)];
+        R2 v;
+        split(gv, v.x, v.y);
+        ring[slt] = v;
         if (MODE == MODE_FWD) {
-          a.tail_alpha[((size_t)x.b * K + slot) * C + c] = ahat_own;
+          a.tail_alpha[((size_t)x.b * K + slt) * C + c] = ahat_own;
         } else {
           const size_t r = (size_t)x.b * (a.delta + 1) + (t - win_t0);
           a.ws_alpha[r * C + c] = ahat_own;
@@ -594,15 +669,17 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
         }
       }
     }
+    const bool at_ck = (t == next_ck);
+    if (at_ck) next_ck += a.delta;
     if (MODE == MODE_REPLAY && x.tid == 0) a.ws_n[((size_t)x.b * g.G + x.rank) * (a.delta + 1) + (t - win_t0)] = n_t;
     if (MODE == MODE_FWD && x.rank == 0) {
       if (x.tid == 0) {
-        a.tail_n[(size_t)x.b * K + t % K] = n_t;
+        a.tail_n[(size_t)x.b * K + slt] = n_t;
         // reference bookkeeping in nats: shifted-frame dead check and checkpoint shift
         const double amax_abs = dead ? -CUDART_INF : n_t * kLn2;
         if (bk.dead_at < 0 && !(amax_abs - bk.N_cur > kGuard)) bk.dead_at = t;
-        if (t % a.delta == 0 && amax_abs - bk.N_cur > kGuard) bk.N_cur = amax_abs;
-        if (t % a.delta == 0 && t / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + t / a.delta] = bk.N_cur;
+        if (at_ck && amax_abs - bk.N_cur > kGuard) bk.N_cur = amax_abs;
+        if (at_ck && t / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + t / a.delta] = bk.N_cur;
       }
       if (t == x.L && x.warp == 0) {
         R ssum = 0;
@@ -610,8 +687,7 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
           for (int i = x.lane; i < C; i += 32) ssum += Mth<R>::ex2(aa[i] - amax);
         ssum = group_sum(ssum, 32);
         if (x.lane == 0) {
-          double lz2 = dead ? -CUDART_INF : n_t + (double)Mth<R>::lg2(ssum);
-          double lz = lz2 * kLn2;
+          const double lz = (dead ? -CUDART_INF : n_t + (double)Mth<R>::lg2(ssum)) * kLn2;
           a.logZ[x.b] = lz;
           if (!(lz - bk.N_cur > kGuard) && bk.dead_at < 0) bk.dead_at = x.L;
         }
@@ -621,16 +697,19 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
     n_prev = n_t;
     e_hi = en_hi;
     e_lo = en_lo;
+    sl2 = sl1;
+    sl1 = slt;
     __syncthreads();
-    if (MODE == MODE_FWD && t % a.delta == 0 && t / a.delta < a.n_ckpt) {
+    if (MODE == MODE_FWD && at_ck && t / a.delta < a.n_ckpt) {
       // snapshot ring + tail for checkpoint i = t / delta
       const int i = t / a.delta;
       const size_t base = ck_off(a, x.b, i);
       for (int q = x.tid; q < K * x.Cg; q += g.NT) {
-        int slot = q / x.Cg, cc = q % x.Cg;
-        size_t gi = (base * K + slot) * C + x.c0 + cc;
-        a.ck.g_hi[gi] = s.ring_hi[slot * Cgm + cc];
-        a.ck.g_lo[gi] = s.ring_lo[slot * Cgm + cc];
+        const int slot = q / x.Cg, cc = q % x.Cg;
+        const size_t gi = (base * K + slot) * C + x.c0 + cc;
+        const R2 v = s.ring[(size_t)cc * K + slot];
+        a.ck.g_hi[gi] = v.x;
+        a.ck.g_lo[gi] = v.y;
         a.ck.alpha[gi] = a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc];
       }
       if (x.rank == 0) {
@@ -649,7 +728,24 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
 // forward kernel
 
 template <typename R>
+__device__ void ck_copy_ring(const Args<R>& a, const Ctx& x, const FwdSmem<R>& s, int i, bool alpha_from_tail) {
+  using R2 = typename Vec2<R>::T;
+  const int K = a.K, C = a.C;
+  const size_t base = ck_off(a, x.b, i);
+  for (int q = x.tid; q < K * x.Cg; q += a.geo.NT) {
+    const int slot = q / x.Cg, cc = q % x.Cg;
+    const size_t gi = (base * K + slot) * C + x.c0 + cc;
+    const R2 v = s.ring[(size_t)cc * K + slot];
+    a.ck.g_hi[gi] = v.x;
+    a.ck.g_lo[gi] = v.y;
+    a.ck.alpha[gi] = alpha_from_tail ? a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc]
+                                     : (slot == 0 ? (R)0 : Mth<R>::ninf());
+  }
+}
+
+template <typename R>
 __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
+  using R2 = typename Vec2<R>::T;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* p = smem_raw;
@@ -663,49 +759,42 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   load_fwd_tables(a, x, s);
   // tail: position 0 has alpha = 0, every other slot is "never written"
   for (int q = x.tid; q < K * x.Cg; q += g.NT) {
-    int slot = q / x.Cg, cc = q % x.Cg;
+    const int slot = q / x.Cg, cc = q % x.Cg;
     a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc] = slot == 0 ? (R)0 : Mth<R>::ninf();
   }
   if (x.rank == 0)
     for (int q = x.tid; q < K; q += g.NT) a.tail_n[(size_t)x.b * K + q] = q == 0 ? 0.0 : -CUDART_INF;
   for (int q = x.tid; q < K * Cgm; q += g.NT) {
-    s.ring_hi[q] = Mth<R>::ninf();
-    s.ring_lo[q] = 0;
+    R2 v;
+    v.x = Mth<R>::ninf();
+    v.y = 0;
+    s.ring[q] = v;
   }
   __syncthreads();
   // position 0: alpha = 0 for every label (virtual source)
-  const int c = x.c0 + (x.active ? x.cl : 0);
+  const int c = x.c0 + x.cls;
   if (x.gl) {
     R ssum = 0;
     for (int cp = x.jj; cp < C; cp += g.GW) ssum += Mth<R>::ex2((R)0 + s.T2c[(size_t)cp * Cgm + x.cls]);
     ssum = group_sum(ssum, g.GW);
-    R gam = s.Tcmax[x.cls] + Mth<R>::lg2(ssum);
+    const R gam = s.Tcmax[x.cls] + Mth<R>::lg2(ssum);
     if (x.active && x.jj == 0) {
-      double gv = (double)gam - S2(x, C, 0, c) + PS2(x, C, 0, c);
-      R hi, lo;
-      split(gv, hi, lo);
-      s.ring_hi[x.cl] = hi;
-      s.ring_lo[x.cl] = lo;
+      const double gv = (double)gam - S2(x, C, 0, c) + PS2(x, C, 0, c);
+      R2 v;
+      split(gv, v.x, v.y);
+      s.ring[(size_t)x.cl * K] = v;
     }
   }
   __syncthreads();
   // checkpoint 0 = initial ring
-  {
+  ck_copy_ring(a, x, s, 0, false);
+  if (x.rank == 0) {
     const size_t base = ck_off(a, x.b, 0);
-    for (int q = x.tid; q < K * x.Cg; q += g.NT) {
-      int slot = q / x.Cg, cc = q % x.Cg;
-      size_t gi = (base * K + slot) * C + x.c0 + cc;
-      a.ck.g_hi[gi] = s.ring_hi[slot * Cgm + cc];
-      a.ck.g_lo[gi] = s.ring_lo[slot * Cgm + cc];
-      a.ck.alpha[gi] = slot == 0 ? (R)0 : Mth<R>::ninf();
-    }
-    if (x.rank == 0) {
-      for (int q = x.tid; q < K; q += g.NT) a.ck.n[base * K + q] = q == 0 ? 0.0 : -CUDART_INF;
-      if (x.tid == 0) {
-        a.ck.hdr[base * 2 + 0] = 0.0;
-        a.ck.hdr[base * 2 + 1] = 0.0;
-        a.N[(size_t)x.b * a.n_ckpt] = 0.0;
-      }
+    for (int q = x.tid; q < K; q += g.NT) a.ck.n[base * K + q] = q == 0 ? 0.0 : -CUDART_INF;
+    if (x.tid == 0) {
+      a.ck.hdr[base * 2 + 0] = 0.0;
+      a.ck.hdr[base * 2 + 1] = 0.0;
+      a.N[(size_t)x.b * a.n_ckpt] = 0.0;
     }
   }
   FwdBook bk;
@@ -719,17 +808,10 @@ __global__ void __launch_bounds__(1024) fwd_kernel(Args<R> a) {
   cl.sync();
   fwd_sweep<R, MODE_FWD>(a, x, s, st, xa, 0, x.L, 0.0, 0.0, bk, 0);
   // checkpoints past the sequence end hold the frozen ring at L
-  const int i_first = x.L / a.delta + 1;
-  for (int i = i_first; i < a.n_ckpt; ++i) {
-    const size_t base = ck_off(a, x.b, i);
-    for (int q = x.tid; q < K * x.Cg; q += g.NT) {
-      int slot = q / x.Cg, cc = q % x.Cg;
-      size_t gi = (base * K + slot) * C + x.c0 + cc;
-      a.ck.g_hi[gi] = s.ring_hi[slot * Cgm + cc];
-      a.ck.g_lo[gi] = s.ring_lo[slot * Cgm + cc];
-      a.ck.alpha[gi] = a.tail_alpha[((size_t)x.b * K + slot) * C + x.c0 + cc];
-    }
+  for (int i = x.L / a.delta + 1; i < a.n_ckpt; ++i) {
+    ck_copy_ring(a, x, s, i, true);
     if (x.rank == 0) {
+      const size_t base = ck_off(a, x.b, i);
       for (int q = x.tid; q < K; q += g.NT) a.ck.n[base * K + q] = a.tail_n[(size_t)x.b * K + q];
       if (x.tid == 0) a.N[(size_t)x.b * a.n_ckpt + i] = bk.N_cur;
     }
@@ -747,16 +829,16 @@ __device__ void flush_grads(const Args<R>& a, const Ctx& x, BwdSmem<R>& sb) {
   const int K = a.K, C = a.C;
   __syncthreads();
   for (int q = x.tid; q < K * x.Cg; q += g.NT) {
-    int k = q / x.Cg, cc = q % x.Cg;
-    R v = sb.gBs[k * g.Cgm + cc];
+    const int cc = q / K, k = q % K;
+    const R v = sb.gBs[(size_t)cc * K + k];
     if (v != (R)0) {
       a.gB_part[((size_t)x.b * K + k) * C + x.c0 + cc] += (double)v;
-      sb.gBs[k * g.Cgm + cc] = (R)0;
+      sb.gBs[(size_t)cc * K + k] = (R)0;
     }
   }
   for (int q = x.tid; q < x.Cg * C; q += g.NT) {
-    int r = q / C, cc = q % C;
-    R v = sb.gTs[r * C + cc];
+    const int r = q / C, cc = q % C;
+    const R v = sb.gTs[r * C + cc];
     if (v != (R)0) {
       a.gT_part[((size_t)x.b * C + x.c0 + r) * C + cc] += (double)v;
       sb.gTs[r * C + cc] = (R)0;
@@ -765,50 +847,101 @@ __device__ void flush_grads(const Args<R>& a, const Ctx& x, BwdSmem<R>& sb) {
   __syncthreads();
 }
 
-// Per-source values of own label: w = -S2[t] + Ps2[t] - F', Gam = (F' + n_t - logZ2) + gamma~[t]
+// Per-source values of own label: w = G0[t] - F'; Gam = (F' + n_t - logZ2) + gamma~[t]
 template <typename R>
 struct SrcVals {
   R w_hi, w_lo, gam;
 };
 
-// bulk for source ts (durations k >= 2, k <= min(K, L - ts))
 template <typename R>
-__device__ __forceinline__ void bwd_bulk(const Args<R>& a, const Ctx& x, BwdSmem<R>& sb, const R* B2, int ts,
-                                         const SrcVals<R>& v, R& m_out, R& s_out, R& ms_out) {
+__device__ __forceinline__ R bwd_term(const typename Vec2<R>::T& v, const SrcVals<R>& s, R b2) {
+  return (v.x + s.w_hi) + (v.y + s.w_lo) + b2;
+}
+
+// bulk for source ts (durations 2 <= k <= min(K, L - ts)); vslot2 = (ts+2) mod K,
+// eslot2 = (ts+2) mod (K+1). Consumes every M[ts,k,c] (grad_B, end accumulators).
+template <typename R>
+__device__ __forceinline__ void bwd_bulk(const Args<R>& a, const Ctx& x, BwdSmem<R>& sb, const R* B2all, int ts,
+                                         int vslot2, int eslot2, const SrcVals<R>& v, R& m_out, R& s_out, R& ms_out) {
+  using R2 = typename Vec2<R>::T;
   const Geometry& g = a.geo;
-  const int K = a.K, Cgm = g.Cgm;
+  const int K = a.K;
   const int kmax = min(K, x.L - ts);
-  R m = Mth<R>::ninf(), sum = 0, msum = 0;
-  int k0 = 1 + x.j;
-  if (k0 == 1) k0 += g.TPL;
-  if (x.active && k0 <= kmax) {
-    const int step = g.TPL % K;
-    const int stepE = g.TPL % (K + 1);
-    const int slot0 = (ts + k0) % K;
-    const int eslot0 = (ts + k0) % (K + 1);
-    int slot = slot0;
-    for (int k = k0; k <= kmax; k += g.TPL) {
-      R y = (sb.vr_hi[slot * Cgm + x.cl] + v.w_hi) + (sb.vr_lo[slot * Cgm + x.cl] + v.w_lo) + B2[(k - 1) * Cgm + x.cl];
-      m = fmax(m, y);
-      slot += step;
-      if (slot >= K) slot -= K;
-    }
-    slot = slot0;
-    int eslot = eslot0;
-    for (int k = k0; k <= kmax; k += g.TPL) {
-      R y = (sb.vr_hi[slot * Cgm + x.cl] + v.w_hi) + (sb.vr_lo[slot * Cgm + x.cl] + v.w_lo) + B2[(k - 1) * Cgm + x.cl];
-      if (m != Mth<R>::ninf()) sum += Mth<R>::ex2(y - m);
-      R M = Mth<R>::ex2(y + v.gam);
-      msum += M;
-      sb.gBs[(k - 1) * Cgm + x.cl] += M;
-      sb.end_acc[eslot * Cgm + x.cl] += M;
-      slot += step;
-      if (slot >= K) slot -= K;
-      eslot += stepE;
-      if (eslot >= K + 1) eslot -= K + 1;
+  const R2* vr = sb.vr + (size_t)x.cls * K;
+  const R* b2 = B2all + (size_t)x.cls * K;
+  R* gB = sb.gBs + (size_t)x.cls * K;
+  R* ea = sb.end_acc + (size_t)x.cls * (K + 1);
+  R mref = Mth<R>::ninf(), sum = 0, msum = 0, dmax = Mth<R>::ninf();
+  bool slow = false;
+  const int k0 = 2 + x.j;
+  const int stepK = g.TPL % K, stepE = g.TPL % (K + 1);
+  int slot0 = vslot2 + x.j % K;
+  if (slot0 >= K) slot0 -= K;
+  int eslot0 = eslot2 + x.j % (K + 1);
+  if (eslot0 >= K + 1) eslot0 -= K + 1;
+  if (kmax >= 2) {
+    mref = bwd_term<R>(vr[vslot2], v, b2[1]);
+    slow = (mref == Mth<R>::ninf());
+    if (x.active && !slow && k0 <= kmax) {
+      // pass 1 (no stores): largest exponent relative to the shared reference
+      int slot = slot0;
+      for (int k = k0; k <= kmax; k += g.TPL) {
+        dmax = fmax(dmax, bwd_term<R>(vr[slot], v, b2[k - 1]) - mref);
+        slot += stepK;
+        if (slot >= K) slot -= K;
+      }
+      slow = dmax > (R)kRefSlack;
     }
   }
-  group_ms(m, sum, g.GW);
+  const bool any_slow = __any_sync(0xffffffffu, slow);
+  if (x.active && k0 <= kmax) {
+    if (!slow) {
+      const R F = Mth<R>::ex2(mref + v.gam);
+      int slot = slot0, es = eslot0;
+      for (int k = k0; k <= kmax; k += g.TPL) {
+        const R e = Mth<R>::ex2(bwd_term<R>(vr[slot], v, b2[k - 1]) - mref);
+        const R M = e * F;
+        sum += e;
+        msum += M;
+        gB[k - 1] += M;
+        ea[es] += M;
+        slot += stepK;
+        if (slot >= K) slot -= K;
+        es += stepE;
+        if (es >= K + 1) es -= K + 1;
+      }
+    } else {
+      // exact path: own maximum, direct marginals
+      R m = Mth<R>::ninf();
+      int slot = slot0;
+      for (int k = k0; k <= kmax; k += g.TPL) {
+        m = fmax(m, bwd_term<R>(vr[slot], v, b2[k - 1]));
+        slot += stepK;
+        if (slot >= K) slot -= K;
+      }
+      slot = slot0;
+      int es = eslot0;
+      for (int k = k0; k <= kmax; k += g.TPL) {
+        const R y = bwd_term<R>(vr[slot], v, b2[k - 1]);
+        if (m != Mth<R>::ninf()) sum += Mth<R>::ex2(y - m);
+        const R M = Mth<R>::ex2(y + v.gam);
+        msum += M;
+        gB[k - 1] += M;
+        ea[es] += M;
+        slot += stepK;
+        if (slot >= K) slot -= K;
+        es += stepE;
+        if (es >= K + 1) es -= K + 1;
+      }
+      mref = m;
+    }
+  }
+  R m = mref;
+  if (any_slow) {
+    group_ms(m, sum, g.GW);
+  } else {
+    sum = group_sum(sum, g.GW);
+  }
   msum = group_sum(msum, g.GW);
   m_out = m;
   s_out = sum;
@@ -818,10 +951,9 @@ __device__ __forceinline__ void bwd_bulk(const Args<R>& a, const Ctx& x, BwdSmem
 template <typename R>
 __device__ __forceinline__ void store_bpart(const Geometry& g, const Ctx& x, R* bp, int par, R m, R s, R ms) {
   if (!x.active) return;
-  const int wl = x.j / 32;
   const bool first = (g.TPL >= 32) ? (x.lane == 0) : (x.j == 0);
   if (first) {
-    size_t i = (((size_t)par * g.Cgm + x.cl) * g.WPL + wl) * 3;
+    const size_t i = (((size_t)par * g.Cgm + x.cl) * g.WPL + x.wl) * 3;
     bp[i] = m;
     bp[i + 1] = s;
     bp[i + 2] = ms;
@@ -830,6 +962,7 @@ __device__ __forceinline__ void store_bpart(const Geometry& g, const Ctx& x, R* 
 
 template <typename R>
 __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
+  using R2 = typename Vec2<R>::T;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* p = smem_raw;
@@ -842,7 +975,7 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
   Ctx x = make_ctx(a, cl);
   const Geometry& g = a.geo;
   const int K = a.K, C = a.C, Cgm = g.Cgm, L = x.L;
-  const int c = x.c0 + (x.active ? x.cl : 0);
+  const int c = x.c0 + x.cls;
   load_fwd_tables(a, x, s);
   load_bwd_tables(a, x, sb);
   Xchg<R> xa, xd;
@@ -857,15 +990,13 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
   __syncthreads();
   cl.sync();
   const double logZ2 = a.logZ_in[x.b] * kLog2e;
-  const double up = a.upstream ? a.upstream[x.b] : 1.0;
+  R2* vr = sb.vr + (size_t)x.cls * K;
 
   // beta ring: only v[L] is live initially (beta[L] = 0)
   if (x.active && x.j == 0) {
-    double vL = S2(x, C, L, c) + PE2(x, C, L - 1, c);
-    R hi, lo;
-    split(vL, hi, lo);
-    sb.vr_hi[(L % K) * Cgm + x.cl] = hi;
-    sb.vr_lo[(L % K) * Cgm + x.cl] = lo;
+    R2 v;
+    split(S2(x, C, L, c) + PE2(x, C, L - 1, c), v.x, v.y);
+    vr[L % K] = v;
   }
   double Fp_cur = 0.0;   // frame of source t (= nd_{t+2})
   double nd_prev = 0.0;  // nd_{t+1}
@@ -882,21 +1013,23 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     const size_t base = ck_off(a, x.b, i);
     __syncthreads();
     for (int q = x.tid; q < K * Cgm; q += g.NT) {
-      int slot = q / Cgm, cc = q % Cgm;
+      const int cc = q / K, slot = q % K;
       if (cc < x.Cg) {
-        size_t gi = (base * K + slot) * C + x.c0 + cc;
-        s.ring_hi[q] = a.ck.g_hi[gi];
-        s.ring_lo[q] = a.ck.g_lo[gi];
+        const size_t gi = (base * K + slot) * C + x.c0 + cc;
+        R2 v;
+        v.x = a.ck.g_hi[gi];
+        v.y = a.ck.g_lo[gi];
+        s.ring[q] = v;
       }
     }
     // alpha-hat at t0 for all labels (into the exchange buffer, parity of t0)
-    for (int q = x.tid; q < C; q += g.NT) s.a_all[(t0 & 1) * C + q] = (R)a.ck.alpha[(base * K + (t0 % K)) * C + q];
+    for (int q = x.tid; q < C; q += g.NT) s.a_all[(t0 & 1) * C + q] = a.ck.alpha[(base * K + (t0 % K)) * C + q];
     __syncthreads();
     const double n_t0 = a.ck.hdr[base * 2 + 1];
     const double n_t0m1 = a.ck.hdr[base * 2 + 0];
     if (x.gl) {
       const R* ah = s.a_all + (t0 & 1) * C;
-      R gam = gamma_from_alpha(ah, s.T2c, s.Tcmax, C, Cgm, x.cls, x.jj, g.GW);
+      const R gam = gamma_from_alpha(ah, s.T2c, s.Tcmax, C, Cgm, x.cls, x.jj, g.GW);
       if (x.active && x.jj == 0) {
         const size_t r = (size_t)x.b * (a.delta + 1);
         a.ws_alpha[r * C + c] = ah[c];
@@ -907,7 +1040,6 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
     __syncthreads();
     fwd_sweep<R, MODE_REPLAY>(a, x, s, st, xa, t0, t1, (t0 == 0) ? 0.0 : n_t0m1, n_t0, bk, t0);
     __syncthreads();
-    // all CTAs must finish the replay (they exchange through a_all) before we reuse barriers
     cl.sync();
 
     // ---- beta sweep over sources t = t1-1 .. t0
@@ -917,13 +1049,16 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
       SrcVals<R> v;
       const size_t k = sg.idx(ts, x.cls, Cgm);
       split(st.G0[k] - Fp, v.w_hi, v.w_lo);
-      v.gam = (R)(Fp + st.n[sg.nidx(ts)] - logZ2) + st.gam[k];
+      v.gam = (R)(Fp + st.n[sg.row(ts)] - logZ2) + st.gam[k];
       return v;
     };
+    // slots of t+1, t+2 in the beta ring (mod K) and the end ring (mod K+1), source t = t1-1
+    int vs1 = t1 % K, vs2 = (t1 + 1) % K;
+    int es1 = t1 % (K + 1), es2 = (t1 + 1) % (K + 1);
     SrcVals<R> cur = src(t1 - 1, Fp_cur);
     {
       R m, sm, ms;
-      bwd_bulk(a, x, sb, s.B2, t1 - 1, cur, m, sm, ms);
+      bwd_bulk(a, x, sb, s.B2, t1 - 1, vs2, es2, cur, m, sm, ms);
       store_bpart(g, x, sb.bpart, (t1 - 1) & 1, m, sm, ms);
     }
     __syncthreads();
@@ -935,32 +1070,38 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
       if (x.gl) {
         R m = Mth<R>::ninf(), sm = 0, ms = 0;
         if (x.active && x.jj < g.WPL) {
-          size_t q = (((size_t)par * Cgm + x.cl) * g.WPL + x.jj) * 3;
+          const size_t q = (((size_t)par * Cgm + x.cl) * g.WPL + x.jj) * 3;
           m = sb.bpart[q];
           sm = sb.bpart[q + 1];
           ms = sb.bpart[q + 2];
         }
-        group_ms(m, sm, g.GW);
-        ms = group_sum(ms, g.GW);
-        const int slot = (t + 1) % K;
-        R y1 = (sb.vr_hi[slot * Cgm + x.cls] + cur.w_hi) + (sb.vr_lo[slot * Cgm + x.cls] + cur.w_lo) + s.B2[x.cls];
-        R M1 = Mth<R>::ex2(y1 + cur.gam);
-        ms_merge(m, sm, y1, (R)1);
-        ms += M1;
-        R dv = ms_value(m, sm);
+        if (g.WPL > 1) {
+          const R m0 = __shfl_sync(0xffffffffu, m, 0, g.GW);
+          const bool same = (x.jj >= g.WPL) || (m == m0);
+          if (__all_sync(0xffffffffu, same)) {
+            sm = group_sum(sm, g.GW);
+            m = m0;
+          } else {
+            group_ms(m, sm, g.GW);
+          }
+          ms = group_sum(ms, g.GW);
+        }
+        const R y1 = bwd_term<R>(vr[vs1], cur, s.B2[(size_t)x.cls * K]);
+        const R M1 = Mth<R>::ex2(y1 + cur.gam);
+        const R dv = add_term(m, sm, y1);
         if (x.active && x.jj == 0) {
-          sb.end1[((t + 1) % (K + 1)) * Cgm + x.cl] = M1;
-          sb.gBs[x.cl] += M1;
-          a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = ms;
+          sb.end1[(size_t)x.cl * (K + 1) + es1] = M1;
+          sb.gBs[(size_t)x.cl * K] += M1;
+          a.start_g[((size_t)x.b * (a.T + 1) + t) * C + c] = ms + M1;
         }
         if (x.active) xd.send(par, c, dv, x.jj, g.GW, g.G);
       }
-      // (C) bulk for source t-1 (frame nd_{t+1})
+      // (C) bulk for source t-1 (frame nd_{t+1}) while the exchange is in flight
       SrcVals<R> nxt = cur;
       if (t - 1 >= t0) {
         nxt = src(t - 1, nd_prev);
         R m, sm, ms;
-        bwd_bulk(a, x, sb, s.B2, t - 1, nxt, m, sm, ms);
+        bwd_bulk(a, x, sb, s.B2, t - 1, vs1, es1, nxt, m, sm, ms);
         store_bpart(g, x, sb.bpart, (t - 1) & 1, m, sm, ms);
       }
       // (E) beta at t, grad_T, v[t], end emission
@@ -970,16 +1111,19 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
       dmax = group_max(dmax, 32);
       const bool dead = (dmax == Mth<R>::ninf());
       const double nd_t = dead ? Fp_cur : Fp_cur + (double)dmax;
+      const int vs0 = (vs1 == 0) ? K - 1 : vs1 - 1;  // t mod K
+      const int es0 = (es1 == 0) ? K : es1 - 1;      // t mod (K+1)
       if (x.gl && !dead) {
         const size_t k = sg.idx(t, x.cls, Cgm);
-        const double n_t = st.n[sg.nidx(t)];
+        const double n_t = st.n[sg.row(t)];
         const R Zt = (R)(n_t + nd_t - logZ2);
         const R ahat = st.ahat[k];
         R ssum = 0;
         for (int q = x.jj; q < C; q += g.GW) {
           const R dh = dd[q] - dmax;
           ssum += Mth<R>::ex2(sb.T2r[(size_t)x.cls * C + q] + dh);
-          if (x.active && ahat != Mth<R>::ninf()) sb.gTs[(size_t)x.cls * C + q] += Mth<R>::ex2(ahat + sb.T2o[(size_t)x.cls * C + q] + dh + Zt);
+          if (x.active && ahat != Mth<R>::ninf())
+            sb.gTs[(size_t)x.cls * C + q] += Mth<R>::ex2(ahat + sb.T2o[(size_t)x.cls * C + q] + dh + Zt);
         }
         ssum = group_sum(ssum, g.GW);
         R bt;
@@ -996,24 +1140,28 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
           bt = sb.Trmax[x.cls] + Mth<R>::lg2(ssum);
         }
         if (x.active && x.jj == 0 && t >= 1) {
-          double vv = (bt == Mth<R>::ninf()) ? -CUDART_INF : st.E0[k] + nd_t + (double)bt;
-          R hi, lo;
-          split(vv, hi, lo);
-          sb.vr_hi[(t % K) * Cgm + x.cl] = hi;
-          sb.vr_lo[(t % K) * Cgm + x.cl] = lo;
+          const double vv = (bt == Mth<R>::ninf()) ? -CUDART_INF : st.E0[k] + nd_t + (double)bt;
+          R2 v;
+          split(vv, v.x, v.y);
+          vr[vs0] = v;
         }
       }
       if (x.active && x.j == 0) {
-        const int e = t + K;
+        const int e = t + K;  // complete after source t: emit
         if (e <= L) {
-          const int es = e % (K + 1);
-          a.end_g[((size_t)x.b * (a.T + 1) + e) * C + c] = sb.end_acc[es * Cgm + x.cl] + sb.end1[es * Cgm + x.cl];
-          sb.end_acc[es * Cgm + x.cl] = (R)0;
+          const int es = (es0 == 0) ? K : es0 - 1;  // (t + K) mod (K+1) = (t - 1) mod (K+1)
+          R* ea = sb.end_acc + (size_t)x.cl * (K + 1);
+          a.end_g[((size_t)x.b * (a.T + 1) + e) * C + c] = ea[es] + sb.end1[(size_t)x.cl * (K + 1) + es];
+          ea[es] = (R)0;
         }
       }
       Fp_cur = nd_prev;
       nd_prev = nd_t;
       cur = nxt;
+      vs2 = vs1;
+      vs1 = vs0;
+      es2 = es1;
+      es1 = es0;
       __syncthreads();
       if (++steps_since_flush >= 256) {
         flush_grads(a, x, sb);
@@ -1027,11 +1175,11 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
   if (x.active && x.j == 0) {
     for (int e = 1; e <= min(K - 1, L); ++e) {
       const int es = e % (K + 1);
-      a.end_g[((size_t)x.b * (a.T + 1) + e) * C + c] = sb.end_acc[es * Cgm + x.cl] + sb.end1[es * Cgm + x.cl];
+      a.end_g[((size_t)x.b * (a.T + 1) + e) * C + c] =
+          sb.end_acc[(size_t)x.cl * (K + 1) + es] + sb.end1[(size_t)x.cl * (K + 1) + es];
     }
   }
   flush_grads(a, x, sb);
-  (void)up;
   cl.sync();
 }
 
@@ -1041,12 +1189,11 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
 // One thread per (b, c): sequential fp64 scan over t (coverage cumsum).
 
 template <typename R>
-__global__ void finalize_kernel(const R* start_g, const R* end_g, const int64_t* lengths,
-                                const double* upstream, int B, int T, int C, double* grad_S, double* grad_Ps,
-                                double* grad_Pe, double* pos) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void finalize_kernel(const R* start_g, const R* end_g, const int64_t* lengths, const double* upstream, int B,
+                                int T, int C, double* grad_S, double* grad_Ps, double* grad_Pe, double* pos) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * C) return;
-  int b = idx / C, c = idx % C;
+  const int b = idx / C, c = idx % C;
   const int L = (int)lengths[b];
   const double up = upstream ? upstream[b] : 1.0;
   const size_t rb = (size_t)b * (T + 1);
@@ -1058,8 +1205,7 @@ __global__ void finalize_kernel(const R* start_g, const R* end_g, const int64_t*
     if (t < T) {
       if (grad_Ps) grad_Ps[((size_t)b * T + t) * C + c] = up * st;
       cov += st - en;
-      double pm = (t < L) ? fmin(fmax(cov, 0.0), 1.0) : 0.0;
-      pos[((size_t)b * T + t) * C + c] = pm;
+      pos[((size_t)b * T + t) * C + c] = (t < L) ? fmin(fmax(cov, 0.0), 1.0) : 0.0;
     }
     if (t >= 1 && grad_Pe) grad_Pe[((size_t)b * T + t - 1) * C + c] = up * en;
   }
@@ -1092,7 +1238,7 @@ __global__ void boundary_kernel(const R* start_g, const int64_t* lengths, int B,
 
 // fixed-order batch reduction of per-sequence partials (bit-reproducible)
 __global__ void reduce_partials_kernel(const double* part, const double* upstream, int B, size_t n, double* out) {
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double acc = 0.0;
   for (int b = 0; b < B; ++b) acc += (upstream ? upstream[b] : 1.0) * part[(size_t)b * n + i];
