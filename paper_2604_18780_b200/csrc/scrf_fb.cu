@@ -563,6 +563,10 @@ __device__ __forceinline__ void merge_parts(const Geometry& g, const Ctx& x, con
     } else {
       group_ms(m, s, g.GW);
     }
+  } else {
+    // single partial per label: every lane of the group needs it (each sends to other ranks)
+    m = __shfl_sync(0xffffffffu, m, 0, g.GW);
+    s = __shfl_sync(0xffffffffu, s, 0, g.GW);
   }
 }
 
@@ -1085,6 +1089,10 @@ __global__ void __launch_bounds__(1024) bwd_kernel(Args<R> a) {
             group_ms(m, sm, g.GW);
           }
           ms = group_sum(ms, g.GW);
+        } else {
+          m = __shfl_sync(0xffffffffu, m, 0, g.GW);
+          sm = __shfl_sync(0xffffffffu, sm, 0, g.GW);
+          ms = __shfl_sync(0xffffffffu, ms, 0, g.GW);
         }
         const R y1 = bwd_term<R>(vr[vs1], cur, s.B2[(size_t)x.cls * K]);
         const R M1 = Mth<R>::ex2(y1 + cur.gam);
