@@ -114,6 +114,10 @@ int scrf_last_launch_count(void);
  * dominant kernel live (no profiler). */
 void scrf_profile_events(void* start, void* stop);
 
+/* Debug: if non-NULL, the next forward writes clock64() phase timestamps of its
+ * first 256 positions (CTA 0, thread 0) into buf (int64 [256][8]). */
+void scrf_debug_trace(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

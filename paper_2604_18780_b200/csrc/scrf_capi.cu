@@ -19,6 +19,7 @@ thread_local int g_launches = 0;
 // optional events recorded around the next main kernel launch (forward / backward / Viterbi)
 thread_local cudaEvent_t g_ev_start = nullptr;
 thread_local cudaEvent_t g_ev_stop = nullptr;
+thread_local long long* g_trace = nullptr;  // debug: phase timestamps of the forward
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -261,6 +262,7 @@ int run_forward(const scrf_problem* p, int64_t delta, double* logZ, double* N, i
   if (rc) return rc;
   Args<R> a;
   fill_args(a, p, delta, g, ckpt);
+  a.trace = g_trace;
   a.logZ = logZ;
   a.N = N;
   a.dead_at = dead_at;
@@ -480,6 +482,8 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
 }
 
 int scrf_last_launch_count(void) { return g_launches; }
+
+void scrf_debug_trace(void* buf) { g_trace = (long long*)buf; }
 
 void scrf_profile_events(void* start, void* stop) {
   g_ev_start = (cudaEvent_t)start;

@@ -88,6 +88,7 @@ struct Args {
   R* end_g;       // [B][T+1][C]  mass of segments ending at t
   double* gT_part;  // [B][C][C]
   double* gB_part;  // [B][K][C]
+  long long* trace;  // optional [256][8] phase timestamps of CTA 0, thread 0 (debug builds)
 };
 
 template <typename R>
@@ -611,16 +612,20 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
 
   for (int t = t_begin + 1; t <= t_end; ++t) {
     const int par = t & 1;
+    long long* tr = (a.trace && blockIdx.x == 0 && x.tid == 0 && t - t_begin <= 256) ? a.trace + (t - t_begin - 1) * 8 : nullptr;
+    if (tr) tr[0] = clock64();
     sg.advance(a, x, st, t);
     if (x.tid == 0) xa.arm(par);
     // (A) critical: bulk partials + the k = 1 term -> a[t]; send it to the cluster
     if (x.gl) {
       R m, sm;
       merge_parts(g, x, s.part, par, m, sm);
+      if (tr) tr[1] = clock64();
       const R x1 = fwd_term<R>(ring[sl1], e_hi, e_lo, s.B2[(size_t)x.cls * K]);
       const R av = add_term(m, sm, x1);
       if (x.active) xa.send(par, c, av, x.jj, g.GW, g.G);
     }
+    if (tr) tr[2] = clock64();
     // (C) bulk for target t+1 (frame n_{t-1} = n_prev) while the exchange is in flight
     const double Fnext = n_prev;
     R en_hi = 0, en_lo = 0;
@@ -631,10 +636,13 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
       store_part(g, x, s.part, (t + 1) & 1, m, sm);
     }
     // (E) normaliser, gamma, ring write
+    if (tr) tr[3] = clock64();
     const R* aa = xa.wait(par);
+    if (tr) tr[4] = clock64();
     R amax = Mth<R>::ninf();
     for (int i = x.lane; i < C; i += 32) amax = fmax(amax, aa[i]);
     amax = group_max(amax, 32);
+    if (tr) tr[5] = clock64();
     const bool dead = (amax == Mth<R>::ninf());
     const double n_t = dead ? Fcur : Fcur + (double)amax;
     const int slt = (sl1 + 1 == K) ? 0 : sl1 + 1;  // t mod K
@@ -659,6 +667,7 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
           gam = s.Tcmax[x.cls] + Mth<R>::lg2(ssum);
         }
       }
+      if (tr) tr[6] = clock64();
       if (x.active && x.jj == 0) {
         const double gv = (gam == Mth<R>::ninf()) ? -CUDART_INF : n_t + (double)gam + st.G0[sg.idx(t, x.cl, Cgm)];
         R2 v;
@@ -703,6 +712,7 @@ __device__ void fwd_sweep(const Args<R>& a, const Ctx& x, FwdSmem<R>& s, StageSm
     e_lo = en_lo;
     sl2 = sl1;
     sl1 = slt;
+    if (tr) tr[7] = clock64();
     __syncthreads();
     if (MODE == MODE_FWD && at_ck && t / a.delta < a.n_ckpt) {
       // snapshot ring + tail for checkpoint i = t / delta
