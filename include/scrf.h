@@ -8,6 +8,8 @@
  *   scrf_forward   <- streaming_forward   (streaming.py:155-229) + forward_logZ (:707-722)
  *   scrf_backward  <- streaming_backward  (streaming.py:264-408) incl. recompute_alpha
  *                     (:232-261) and finalize_marginals (diagnostics.py:54-79)
+ *   scrf_posterior <- posterior           (streaming.py:725-746): forward + backward fused, the
+ *                     alpha and beta sweeps run concurrently in one launch
  *   scrf_viterbi   <- streaming_viterbi   (streaming.py:411-470) + decode (:749-762)
  *   scrf_export_checkpoints <- the CheckpointSet(omega, N, delta) view (streaming.py:49-67)
  *
@@ -82,6 +84,19 @@ int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const dou
                   double* position_marginals, double* boundary_posterior,
                   double* expected_segment_count, void* work, size_t work_bytes, void* stream);
 
+/* posterior(cum, params, delta, upstream) in one call: the forward outputs of
+ * scrf_forward (logZ, N, dead_at, ckpt) and the backward outputs of scrf_backward.
+ * The alpha and beta message sweeps are independent and run concurrently. */
+int scrf_posterior(const scrf_problem* p, int64_t delta, int precision, const double* upstream,
+                   double* logZ, double* N, int32_t* dead_at, void* ckpt, size_t ckpt_bytes,
+                   double* grad_S, double* grad_T, double* grad_B, double* grad_P_start,
+                   double* grad_P_end, double* position_marginals, double* boundary_posterior,
+                   double* expected_segment_count, void* work, size_t work_bytes, void* stream);
+
+/* logZ recomputed from the beta sweep (LSE_c beta[0,c]; virtual source), (B,) nats:
+ * a consistency value for tests, copied out of `work` after scrf_backward/posterior. */
+int scrf_beta_logz(const scrf_problem* p, int precision, const void* work, double* logZb, void* stream);
+
 /* Per-sequence (unreduced) transition / duration gradient partials, for the
  * multi-GPU path that reduces across ranks in a fixed order: after
  * scrf_backward, copies (B, C, C) and (B, K, C) fp64 partials out of `work`. */
@@ -114,8 +129,8 @@ int scrf_last_launch_count(void);
  * dominant kernel live (no profiler). */
 void scrf_profile_events(void* start, void* stop);
 
-/* Debug: if non-NULL, the next forward writes clock64() phase timestamps of its
- * first 256 positions (CTA 0, thread 0) into buf (int64 [256][8]). */
+/* Debug: if non-NULL, the next sweep writes clock64() phase stamps of cluster 0 for
+ * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);
 
 #ifdef __cplusplus

@@ -45,6 +45,7 @@ from .streaming import (
     decode,
     device_backward,
     device_forward,
+    device_posterior,
     device_viterbi,
     dispatch,
     forward_logZ,
@@ -64,7 +65,7 @@ __all__ = [
     "CumulativeScores", "DeviceProblem", "EmissionBatch", "GradientSet", "MarginalSet", "MemoryLedger",
     "NEG_INF", "RingAudit", "RunStats", "Segmentation", "SemiCRFParams", "CONFIGS", "boundary_entropy",
     "build_cumulative", "build_scores", "center_emissions", "choose_checkpoint_interval", "decode",
-    "device_backward", "device_forward", "device_viterbi", "dispatch", "edge_potential",
+    "device_backward", "device_forward", "device_posterior", "device_viterbi", "dispatch", "edge_potential",
     "equivalence_instance", "finalize_marginals", "fold_scalar_boundaries", "forward_logZ", "log_partition",
     "nll", "position_marginals", "posterior", "recompute_alpha", "score_segmentation", "segment_path_score",
     "self_consistency_report", "set_precision", "streaming_backward", "streaming_forward",

@@ -58,6 +58,9 @@ _SIGS = {
     "scrf_forward": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _sz, _vp]),
     "scrf_backward_work_bytes": (_int, [_P, _i64, _int, _psz]),
     "scrf_backward": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "scrf_posterior": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _sz, _vp]),
+    "scrf_beta_logz": (_int, [_P, _int, _vp, _vp, _vp]),
     "scrf_backward_partials": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
     "scrf_viterbi_work_bytes": (_int, [_P, _psz]),
     "scrf_viterbi": (_int, [_P, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libscrf.so")
 SOURCES = ["scrf_capi.cu"]
-DEPS = ["scrf_capi.cu", "scrf_fb.cu", "scrf_viterbi.cu", "scrf_common.cuh",
+DEPS = ["scrf_capi.cu", "scrf_sweep.cuh", "scrf_post.cuh", "scrf_viterbi.cu", "scrf_common.cuh",
         os.path.join("..", "..", "include", "scrf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

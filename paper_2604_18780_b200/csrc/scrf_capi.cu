@@ -8,7 +8,8 @@
 #include <string.h>
 
 #include "../../include/scrf.h"
-#include "scrf_fb.cu"
+#include "scrf_sweep.cuh"
+#include "scrf_post.cuh"
 #include "scrf_viterbi.cu"
 
 using namespace scrf;
@@ -19,7 +20,7 @@ thread_local int g_launches = 0;
 // optional events recorded around the next main kernel launch (forward / backward / Viterbi)
 thread_local cudaEvent_t g_ev_start = nullptr;
 thread_local cudaEvent_t g_ev_stop = nullptr;
-thread_local long long* g_trace = nullptr;  // debug: phase timestamps of the forward
+thread_local long long* g_trace = nullptr;  // debug: clock64 phase stamps of the next sweep
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -77,37 +78,6 @@ Geometry make_geo(int G, int K, int C) {
   return g;
 }
 
-size_t fb_smem(const Geometry& g, int K, int C, int precision) {
-  return precision ? fwd_smem_bytes<double>(K, C, g) + bwd_extra_smem_bytes<double>(K, C, g) + stage_smem_bytes<double>(g)
-                   : fwd_smem_bytes<float>(K, C, g) + bwd_extra_smem_bytes<float>(K, C, g) + stage_smem_bytes<float>(g);
-}
-
-// Geometry shared by forward and backward (the replay must re-execute the forward
-// bit for bit, so both kernels use the same label slices and thread mapping).
-int choose_fb_geo(int B, int K, int C, int precision, Geometry* out) {
-  const size_t limit = (size_t)smem_optin();
-  int forced = env_int("SCRF_G", 0);
-  const int cands[] = {1, 2, 4, 8, 16};
-  int gmin = 0;
-  for (int G : cands) {
-    if (G > C && G > 1) break;
-    if (forced && G != forced) continue;
-    Geometry g = make_geo(G, K, C);
-    if (g.NT <= 1024 && fb_smem(g, K, C, precision) <= limit) {
-      gmin = G;
-      break;
-    }
-  }
-  if (!gmin) return SCRF_ECONFIG;
-  int G = gmin;
-  if (!forced) {
-    // widen the cluster while the batch still fits on the chip (portable sizes)
-    while (G * 2 <= 8 && G * 2 <= C && (long long)B * G * 2 <= num_sms()) G *= 2;
-  }
-  *out = make_geo(G, K, C);
-  return SCRF_OK;
-}
-
 int choose_vit_geo(int B, int K, int C, bool has_ps, Geometry* out) {
   const size_t limit = (size_t)smem_optin();
   int forced = env_int("SCRF_G", 0);
@@ -139,96 +109,176 @@ int check_problem(const scrf_problem* p) {
 
 int64_t n_ckpt_of(int64_t T, int64_t delta) { return (T + delta - 1) / delta; }
 
-// checkpoint buffer layout (offsets in bytes, 256-aligned)
-struct CkLayout {
-  size_t hdr_geo, g_hi, g_lo, alpha, n, hdr, tail_alpha, tail_n, total;
-};
-
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-CkLayout ck_layout(const scrf_problem* p, int64_t delta, int precision) {
-  CkLayout L;
-  const size_t rs = precision ? 8 : 4;
-  const size_t nck = (size_t)n_ckpt_of(p->T, delta);
-  const size_t ring = (size_t)p->B * nck * p->K * p->C;
+// ---------------------------------------------------------------------------
+// sweep geometry (scrf_sweep.cuh): head-only CTA when the duration range is small,
+// otherwise a head + label-slice tails cluster sized to one wave of the chip.
+
+int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
+  const size_t limit = (size_t)smem_optin();
+  SweepGeo g;
+  memset(&g, 0, sizeof(g));
+  g.NCW = (C + 31) / 32;
+  if (g.NCW > 4) return SCRF_ECONFIG;  // C <= 128 (head roles fit one 512-thread CTA)
+  g.Msm = (size_t)C * C * (prec ? 8 : 4) <= 65536 ? 1 : 0;
+  const int maxg = (16 - 2 * g.NCW) / 2;  // warps per near group (two groups)
+  auto near_gw = [&](int terms) {
+    int gw = pow2_ceil((terms + 3) / 4 > 0 ? (terms + 3) / 4 : 1);
+    if (gw > 32) gw = 32;
+    while (gw > 1 && (C * gw + 31) / 32 > maxg) gw >>= 1;
+    return gw;
+  };
+  const int forced = env_int("SCRF_SWEEP_G", 0);
+  bool one = (long long)K * C <= 6144 || K <= kNear + 1;
+  if (forced) one = (forced == 1) || K <= kNear + 1;
+  if (one) {
+    g.G = 1;
+    g.kc = K;
+    g.KRm = pow2_ceil(K) - 1;
+    g.KTm = 0;
+    g.GWn = near_gw(K > 4 ? K - 4 : 1);
+    g.NNW = 2 * ((C * g.GWn + 31) / 32);
+    g.NT = (2 * g.NCW + g.NNW) * 32;
+    size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
+    if (g.NNW <= 2 * maxg && sm <= limit) {
+      *out = g;
+      return SCRF_OK;
+    }
+    if (K <= kNear + 1) return SCRF_ECONFIG;
+  }
+  g.kc = kNear;
+  g.KRm = pow2_ceil(kNear) - 1;
+  g.KTm = pow2_ceil(K) - 1;
+  g.GWn = near_gw(kNear - 4);
+  g.NNW = 2 * ((C * g.GWn + 31) / 32);
+  int tails = forced > 1 ? forced - 1 : (int)(((long long)K * C + 3499) / 3500);
+  const int maxt = C < 15 ? C : 15;
+  if (tails > maxt) tails = maxt;
+  if (tails < 1) tails = 1;
+  if (!forced)
+    while (tails > 1 && (long long)B * ndirs * (1 + tails) > num_sms()) --tails;
+  for (;; ++tails) {
+    if (tails > maxt) return SCRF_ECONFIG;
+    g.G = 1 + tails;
+    g.CgMax = (C + tails - 1) / tails;
+    g.NWt = g.CgMax < 16 ? g.CgMax : 16;
+    const int head_nt = (2 * g.NCW + g.NNW) * 32;
+    g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
+    size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
+    if (sm <= limit) break;
+  }
+  *out = g;
+  return SCRF_OK;
+}
+
+// forward state ("checkpoint buffer"): per-position alpha-side messages
+struct FLayout {
+  size_t Y, X, n, total;
+};
+FLayout f_layout(const scrf_problem* p, int prec) {
+  FLayout L;
+  const size_t rs = prec ? 8 : 4;
+  const size_t npos = (size_t)p->B * (p->T + 1);
   size_t o = 0;
-  L.hdr_geo = o;
-  o += al(sizeof(Geometry) + 64);
-  L.g_hi = o;
-  o += al(ring * rs);
-  L.g_lo = o;
-  o += al(ring * rs);
-  L.alpha = o;
-  o += al(ring * rs);
+  L.Y = o;
+  o += al(npos * p->C * rs);
+  L.X = o;
+  o += al(npos * p->C * rs);
   L.n = o;
-  o += al((size_t)p->B * nck * p->K * 8);
-  L.hdr = o;
-  o += al((size_t)p->B * nck * 2 * 8);
-  L.tail_alpha = o;
-  o += al((size_t)p->B * p->K * p->C * rs);
-  L.tail_n = o;
-  o += al((size_t)p->B * p->K * 8);
+  o += al(npos * 8);
   L.total = o;
   return L;
 }
 
-struct WorkLayout {
-  size_t ws_alpha, ws_gamma, ws_n, start, end, gT, gB, total;
+struct PostGeo {
+  int CH, nch, CGB, SCB, nchB;
 };
 
-WorkLayout work_layout(const scrf_problem* p, int64_t delta, const Geometry& g, int precision) {
-  WorkLayout W;
+PostGeo post_geo(const scrf_problem* p, int prec) {
+  PostGeo q;
+  const int C = (int)p->C, K = (int)p->K, T = (int)p->T, B = (int)p->B;
+  q.CH = post_chunk(C);
+  q.nch = (T + 1 + q.CH - 1) / q.CH;
+  int cg = 4096 / K;
+  if (cg < 1) cg = 1;
+  if (cg > C) cg = C;
+  const size_t limit = (size_t)smem_optin();
+  while (cg > 1 && (prec ? post_gradB_smem<double>(K, cg) : post_gradB_smem<float>(K, cg)) > limit) --cg;
+  q.CGB = cg;
+  const int ngc = (C + cg - 1) / cg;
+  long long want = 4LL * num_sms();
+  long long per = (want + (long long)ngc * B - 1) / ((long long)ngc * B);
+  if (per < 1) per = 1;
+  int scb = (int)((T + per - 1) / per);
+  scb = (scb + kGBSub - 1) / kGBSub * kGBSub;
+  if (scb < kGBSub) scb = kGBSub;
+  q.SCB = scb;
+  q.nchB = (T + scb - 1) / scb;
+  return q;
+}
+
+// backward work buffer: beta-side messages + partials
+struct BLayout {
+  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, total;
+};
+BLayout b_layout(const scrf_problem* p, int prec) {
+  BLayout L;
+  const size_t rs = prec ? 8 : 4;
+  const size_t B = p->B, C = p->C, K = p->K;
+  const size_t npos = B * (p->T + 1);
+  const PostGeo q = post_geo(p, prec);
   size_t o = 0;
-  const size_t win = (size_t)p->B * (delta + 1) * p->C;
-  const size_t rs = precision ? 8 : 4;
-  W.ws_alpha = o;
-  o += al(win * rs);
-  W.ws_gamma = o;
-  o += al(win * rs);
-  W.ws_n = o;
-  o += al((size_t)p->B * g.G * (delta + 1) * 8);
-  W.start = o;
-  o += al((size_t)p->B * (p->T + 1) * p->C * rs);
-  W.end = o;
-  o += al((size_t)p->B * (p->T + 1) * p->C * rs);
-  W.gT = o;
-  o += al((size_t)p->B * p->C * p->C * 8);
-  W.gB = o;
-  o += al((size_t)p->B * p->K * p->C * 8);
-  W.total = o;
-  return W;
+  L.Y = o;     o += al(npos * C * rs);
+  L.X = o;     o += al(npos * C * rs);
+  L.n = o;     o += al(npos * 8);
+  L.logZb = o; o += al(B * 8);
+  L.tot = o;   o += al(B * q.nch * C * 8);
+  L.cntp = o;  o += al(B * q.nch * 8);
+  L.gTp = o;   o += al(B * q.nch * C * C * 8);
+  L.gBp = o;   o += al(B * q.nchB * K * C * 8);
+  L.gTs = o;   o += al(B * C * C * 8);
+  L.gBs = o;   o += al(B * K * C * 8);
+  L.total = o;
+  return L;
 }
 
 template <typename Kern, typename ArgT>
-cudaError_t launch_cluster(Kern kern, const Geometry& g, int B, size_t smem, cudaStream_t st, ArgT arg) {
+cudaError_t launch_cl(Kern kern, int G, int nclusters, int NT, size_t smem, cudaStream_t st, ArgT arg, bool record) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (g.G > 8) {
+  if (G > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(B * g.G, 1, 1);
-  cfg.blockDim = dim3(g.NT, 1, 1);
+  cfg.gridDim = dim3(nclusters * G, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = g.G;
+  attr[0].val.clusterDim.x = G;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ++g_launches;
-  if (g_ev_start) cudaEventRecord(g_ev_start, st);
+  if (record && g_ev_start) cudaEventRecord(g_ev_start, st);
   e = cudaLaunchKernelEx(&cfg, kern, arg);
-  if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
+  if (record && g_ev_stop) cudaEventRecord(g_ev_stop, st);
   return e;
 }
 
 template <typename R>
-void fill_args(Args<R>& a, const scrf_problem* p, int64_t delta, const Geometry& g, void* ckpt) {
+int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate, void* work, double* logZ, double* N,
+              int32_t* dead_at, cudaStream_t st) {
+  const int nd = dirs == 3 ? 2 : 1;
+  SweepGeo g;
+  int rc = choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, nd, &g);
+  if (rc) return rc;
+  SweepArgs<R> a;
   memset(&a, 0, sizeof(a));
   a.S = p->S;
   a.lengths = p->lengths;
@@ -240,97 +290,136 @@ void fill_args(Args<R>& a, const scrf_problem* p, int64_t delta, const Geometry&
   a.T = (int)p->T;
   a.K = (int)p->K;
   a.C = (int)p->C;
+  a.geo = g;
+  a.dirs = dirs;
+  const FLayout F = f_layout(p, sizeof(R) == 8);
+  unsigned char* fb = (unsigned char*)fstate;
+  a.Y[0] = (R*)(fb + F.Y);
+  a.X[0] = (R*)(fb + F.X);
+  a.n[0] = (double*)(fb + F.n);
+  if (work) {
+    const BLayout W = b_layout(p, sizeof(R) == 8);
+    unsigned char* wb = (unsigned char*)work;
+    a.Y[1] = (R*)(wb + W.Y);
+    a.X[1] = (R*)(wb + W.X);
+    a.n[1] = (double*)(wb + W.n);
+    a.logZb = (double*)(wb + W.logZb);
+  }
+  a.logZ = logZ;
+  a.dead_at = dead_at;
+  a.N = N;
   a.delta = (int)delta;
   a.n_ckpt = (int)n_ckpt_of(p->T, delta);
-  a.geo = g;
-  CkLayout L = ck_layout(p, delta, sizeof(R) == 8);
-  unsigned char* base = (unsigned char*)ckpt;
-  a.ck.g_hi = (R*)(base + L.g_hi);
-  a.ck.g_lo = (R*)(base + L.g_lo);
-  a.ck.alpha = (R*)(base + L.alpha);
-  a.ck.n = (double*)(base + L.n);
-  a.ck.hdr = (double*)(base + L.hdr);
-  a.tail_alpha = (R*)(base + L.tail_alpha);
-  a.tail_n = (double*)(base + L.tail_n);
-}
-
-template <typename R>
-int run_forward(const scrf_problem* p, int64_t delta, double* logZ, double* N, int32_t* dead_at, void* ckpt,
-                cudaStream_t st) {
-  Geometry g;
-  int rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, &g);
-  if (rc) return rc;
-  Args<R> a;
-  fill_args(a, p, delta, g, ckpt);
   a.trace = g_trace;
-  a.logZ = logZ;
-  a.N = N;
-  a.dead_at = dead_at;
-  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g) + stage_smem_bytes<R>(g);
-  return (int)launch_cluster(fwd_kernel<R>, g, a.B, smem, st, a);
+  const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
+  const bool tails = g.G > 1, cw1 = g.NCW == 1;
+  if (tails && cw1) return (int)launch_cl(sweep_kernel<R, true, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  if (tails) return (int)launch_cl(sweep_kernel<R, true, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  if (cw1) return (int)launch_cl(sweep_kernel<R, false, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  return (int)launch_cl(sweep_kernel<R, false, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
 }
 
 template <typename R>
-int run_backward(const scrf_problem* p, int64_t delta, const double* logZ, const void* ckpt, const double* upstream,
-                 double* grad_S, double* grad_T, double* grad_B, double* gPs, double* gPe, double* pos, double* bnd,
-                 double* cnt, void* work, size_t work_bytes, cudaStream_t st) {
-  Geometry g;
-  int rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, &g);
-  if (rc) return rc;
-  WorkLayout W = work_layout(p, delta, g, sizeof(R) == 8);
-  if (work_bytes < W.total) return SCRF_EWORK;
-  Args<R> a;
-  fill_args(a, p, delta, g, (void*)ckpt);
-  unsigned char* w = (unsigned char*)work;
-  a.logZ_in = logZ;
+int run_post(const scrf_problem* p, const void* fstate, void* work, const double* logZ, const double* upstream,
+             double* grad_S, double* grad_T, double* grad_B, double* gPs, double* gPe, double* pos, double* bnd,
+             double* cnt, cudaStream_t st) {
+  const PostGeo q = post_geo(p, sizeof(R) == 8);
+  const FLayout F = f_layout(p, sizeof(R) == 8);
+  const BLayout W = b_layout(p, sizeof(R) == 8);
+  const unsigned char* fb = (const unsigned char*)fstate;
+  unsigned char* wb = (unsigned char*)work;
+  PostArgs<R> a;
+  memset(&a, 0, sizeof(a));
+  a.S = p->S;
+  a.lengths = p->lengths;
+  a.trans = p->transition;
+  a.dur = p->duration_bias;
+  a.ps = p->proj_start;
+  a.pe = p->proj_end;
   a.upstream = upstream;
-  a.ws_alpha = (R*)(w + W.ws_alpha);
-  a.ws_gamma = (R*)(w + W.ws_gamma);
-  a.ws_n = (double*)(w + W.ws_n);
-  a.start_g = (R*)(w + W.start);
-  a.end_g = (R*)(w + W.end);
-  a.gT_part = (double*)(w + W.gT);
-  a.gB_part = (double*)(w + W.gB);
-  cudaError_t e = cudaMemsetAsync(w + W.start, 0, W.total - W.start, st);
-  if (e != cudaSuccess) return (int)e;
-  size_t smem = fwd_smem_bytes<R>(a.K, a.C, g) + bwd_extra_smem_bytes<R>(a.K, a.C, g) + stage_smem_bytes<R>(g);
-  e = launch_cluster(bwd_kernel<R>, g, a.B, smem, st, a);
-  if (e != cudaSuccess) return (int)e;
-  const int B = a.B, T = a.T, C = a.C, K = a.K;
+  a.logZ = logZ;
+  a.B = (int)p->B;
+  a.T = (int)p->T;
+  a.K = (int)p->K;
+  a.C = (int)p->C;
+  a.Ya = (const R*)(fb + F.Y);
+  a.Xa = (const R*)(fb + F.X);
+  a.na = (const double*)(fb + F.n);
+  a.Yb = (const R*)(wb + W.Y);
+  a.Xb = (const R*)(wb + W.X);
+  a.nb = (const double*)(wb + W.n);
+  a.grad_S = grad_S;
+  a.grad_Ps = gPs;
+  a.grad_Pe = gPe;
+  a.pos = pos;
+  a.bnd = bnd;
+  a.CH = q.CH;
+  a.nch = q.nch;
+  a.tot = (double*)(wb + W.tot);
+  a.cntp = (double*)(wb + W.cntp);
+  a.gTp = (double*)(wb + W.gTp);
+  a.SCB = q.SCB;
+  a.nchB = q.nchB;
+  a.CGB = q.CGB;
+  a.gBp = (double*)(wb + W.gBp);
+  const int B = a.B, C = a.C, K = a.K, T = a.T;
+  cudaError_t e;
   {
-    int n = B * C, blk = 128;
+    const size_t sm = post_pos_smem<R>(C, q.CH);
+    e = cudaFuncSetAttribute(post_pos_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    finalize_kernel<R><<<(n + blk - 1) / blk, blk, 0, st>>>(a.start_g, a.end_g, p->lengths, upstream, B, T, C, grad_S, gPs,
-                                                         gPe, pos);
+    post_pos_kernel<R><<<dim3(q.nch, B), 256, sm, st>>>(a);
     ++g_launches;
-    boundary_kernel<R><<<B, 256, 0, st>>>(a.start_g, p->lengths, B, T, C, bnd, cnt);
-    size_t nT = (size_t)C * C, nB = (size_t)K * C;
+    post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
+  }
+  {
+    const size_t sm = post_gradB_smem<R>(K, q.CGB);
+    e = cudaFuncSetAttribute(post_gradB_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    reduce_partials_kernel<<<(unsigned)((nT + 255) / 256), 256, 0, st>>>(a.gT_part, upstream, B, nT, grad_T);
+    post_gradB_kernel<R><<<dim3(q.nchB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(a);
+  }
+  {
+    const int nT = C * C, nB = K * C;
     ++g_launches;
-    reduce_partials_kernel<<<(unsigned)((nB + 255) / 256), 256, 0, st>>>(a.gB_part, upstream, B, nB, grad_B);
+    post_reduce_kernel<<<(nT + 255) / 256, 256, 0, st>>>(B, nT, q.nch, a.gTp, upstream, (double*)(wb + W.gTs), grad_T);
+    ++g_launches;
+    post_reduce_kernel<<<(nB + 255) / 256, 256, 0, st>>>(B, nB, q.nchB, a.gBp, upstream, (double*)(wb + W.gBs), grad_B);
+    ++g_launches;
+    post_count_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, q.nch, a.cntp, cnt);
   }
   return (int)cudaGetLastError();
 }
 
-template <typename A>
-__global__ void export_kernel(const A* alpha, const double* n, const double* N, int B, int nck, int K, int C,
-                              double* omega) {
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  size_t total = (size_t)B * nck * K * C;
+// reference-format checkpoint view (streaming.py:49-67): ring after the shift at i*delta
+template <typename R>
+__global__ void export_kernel(const R* Ya, const double* na, const double* N, const int64_t* lengths, int B, int T,
+                              int nck, int K, int C, int delta, double* omega) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)B * nck * K * C;
   if (i >= total) return;
-  size_t bi = i / ((size_t)K * C);  // (b, ckpt)
-  size_t slot = (i / C) % K;
-  A av = alpha[i];
-  double nv = n[bi * K + slot];
-  if (!(av > -INFINITY) || !(nv > -INFINITY)) {
+  const int c = (int)(i % C);
+  const int slot = (int)((i / C) % K);
+  const int ck = (int)((i / ((size_t)C * K)) % nck);
+  const int b = (int)(i / ((size_t)C * K * nck));
+  const int L = (int)lengths[b];
+  long long e = (long long)ck * delta;
+  if (e > L) e = L;
+  long long s = e - (((e - slot) % K) + K) % K;
+  if (s < 0) {
     omega[i] = kNegInfRef;
     return;
   }
-  double v = ((double)av + nv) * kLn2 - N[bi];
+  const size_t o = ((size_t)b * (T + 1) + s);
+  const R y = Ya[o * C + c];
+  if (!(y > -INFINITY)) {
+    omega[i] = kNegInfRef;
+    return;
+  }
+  const double v = (na[o] + (double)y) * kLn2 - N[(size_t)b * nck + ck];
   omega[i] = v <= kGuard ? kNegInfRef : v;
 }
-
 }  // namespace
 
 extern "C" {
@@ -347,7 +436,7 @@ int scrf_checkpoint_bytes(const scrf_problem* p, int64_t delta, int precision, s
   int rc = check_problem(p);
   if (rc) return rc;
   if (delta < 1) return SCRF_EDELTA;
-  *bytes = ck_layout(p, delta, precision).total;
+  *bytes = f_layout(p, precision).total;
   return SCRF_OK;
 }
 
@@ -358,20 +447,26 @@ int scrf_forward(const scrf_problem* p, int64_t delta, int precision, double* lo
   if (rc) return rc;
   if (delta < 1) return SCRF_EDELTA;
   if (!logZ || !N || !dead_at || !ckpt) return SCRF_ENULL;
-  if (ckpt_bytes < ck_layout(p, delta, precision).total) return SCRF_EWORK;
+  if (ckpt_bytes < f_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  return precision ? run_forward<double>(p, delta, logZ, N, dead_at, ckpt, st)
-                   : run_forward<float>(p, delta, logZ, N, dead_at, ckpt, st);
+  return precision ? run_sweep<double>(p, 1, delta, ckpt, nullptr, logZ, N, dead_at, st)
+                   : run_sweep<float>(p, 1, delta, ckpt, nullptr, logZ, N, dead_at, st);
 }
 
 int scrf_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes) {
   int rc = check_problem(p);
   if (rc) return rc;
   if (delta < 1) return SCRF_EDELTA;
-  Geometry g;
-  rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, precision, &g);
+  *bytes = b_layout(p, precision).total;
+  return SCRF_OK;
+}
+
+static int check_bwd_args(const scrf_problem* p, int64_t delta, const double* logZ, const void* ckpt, double* grad_S,
+                          double* grad_T, double* grad_B, double* pos, double* bnd, double* cnt, void* work) {
+  int rc = check_problem(p);
   if (rc) return rc;
-  *bytes = work_layout(p, delta, g, precision).total;
+  if (delta < 1) return SCRF_EDELTA;
+  if (!logZ || !ckpt || !grad_S || !grad_T || !grad_B || !pos || !bnd || !cnt || !work) return SCRF_ENULL;
   return SCRF_OK;
 }
 
@@ -380,35 +475,63 @@ int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const dou
                   double* grad_P_end, double* position_marginals, double* boundary_posterior,
                   double* expected_segment_count, void* work, size_t work_bytes, void* stream) {
   g_launches = 0;
-  int rc = check_problem(p);
+  int rc = check_bwd_args(p, delta, logZ, ckpt, grad_S, grad_T, grad_B, position_marginals, boundary_posterior,
+                          expected_segment_count, work);
   if (rc) return rc;
-  if (delta < 1) return SCRF_EDELTA;
-  if (!logZ || !ckpt || !grad_S || !grad_T || !grad_B || !position_marginals || !boundary_posterior ||
-      !expected_segment_count || !work)
-    return SCRF_ENULL;
+  if (work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  return precision ? run_backward<double>(p, delta, logZ, ckpt, upstream, grad_S, grad_T, grad_B, grad_P_start,
-                                          grad_P_end, position_marginals, boundary_posterior, expected_segment_count,
-                                          work, work_bytes, st)
-                   : run_backward<float>(p, delta, logZ, ckpt, upstream, grad_S, grad_T, grad_B, grad_P_start,
-                                         grad_P_end, position_marginals, boundary_posterior, expected_segment_count,
-                                         work, work_bytes, st);
+  rc = precision ? run_sweep<double>(p, 2, delta, ckpt, work, nullptr, nullptr, nullptr, st)
+                 : run_sweep<float>(p, 2, delta, ckpt, work, nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
+  return precision ? run_post<double>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
+                                      position_marginals, boundary_posterior, expected_segment_count, st)
+                   : run_post<float>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
+                                     position_marginals, boundary_posterior, expected_segment_count, st);
+}
+
+int scrf_posterior(const scrf_problem* p, int64_t delta, int precision, const double* upstream, double* logZ, double* N,
+                   int32_t* dead_at, void* ckpt, size_t ckpt_bytes, double* grad_S, double* grad_T, double* grad_B,
+                   double* grad_P_start, double* grad_P_end, double* position_marginals, double* boundary_posterior,
+                   double* expected_segment_count, void* work, size_t work_bytes, void* stream) {
+  g_launches = 0;
+  int rc = check_bwd_args(p, delta, logZ, ckpt, grad_S, grad_T, grad_B, position_marginals, boundary_posterior,
+                          expected_segment_count, work);
+  if (rc) return rc;
+  if (!N || !dead_at) return SCRF_ENULL;
+  if (ckpt_bytes < f_layout(p, precision).total || work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = precision ? run_sweep<double>(p, 3, delta, ckpt, work, logZ, N, dead_at, st)
+                 : run_sweep<float>(p, 3, delta, ckpt, work, logZ, N, dead_at, st);
+  if (rc) return rc;
+  const int n0 = g_launches;
+  rc = precision ? run_post<double>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
+                                    position_marginals, boundary_posterior, expected_segment_count, st)
+                 : run_post<float>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
+                                   position_marginals, boundary_posterior, expected_segment_count, st);
+  (void)n0;
+  return rc;
 }
 
 int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, const void* work,
                            double* grad_T_partial, double* grad_B_partial, void* stream) {
   int rc = check_problem(p);
   if (rc) return rc;
-  Geometry g;
-  rc = choose_fb_geo((int)p->B, (int)p->K, (int)p->C, precision, &g);
-  if (rc) return rc;
-  WorkLayout W = work_layout(p, delta, g, precision);
+  (void)delta;
+  const BLayout W = b_layout(p, precision);
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned char* w = (const unsigned char*)work;
-  cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + W.gT, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
+  cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + W.gTs, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(grad_B_partial, w + W.gB, (size_t)p->B * p->K * p->C * 8, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(grad_B_partial, w + W.gBs, (size_t)p->B * p->K * p->C * 8, cudaMemcpyDeviceToDevice, st);
   return (int)e;
+}
+
+int scrf_beta_logz(const scrf_problem* p, int precision, const void* work, double* logZb, void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  const BLayout W = b_layout(p, precision);
+  return (int)cudaMemcpyAsync(logZb, (const unsigned char*)work + W.logZb, (size_t)p->B * 8, cudaMemcpyDeviceToDevice,
+                              (cudaStream_t)stream);
 }
 
 static size_t vit_dvr_bytes(const scrf_problem* p, const Geometry& g) { return al((size_t)p->B * g.G * p->K * p->C * 8); }
@@ -457,7 +580,7 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
   a.seg_label = seg_label;
   a.seg_count = seg_count;
   size_t smem = vit_smem_bytes(a.K, a.C, g, a.ps != nullptr);
-  cudaError_t e = launch_cluster(vit_kernel, g, a.B, smem, (cudaStream_t)stream, a);
+  cudaError_t e = launch_cl(vit_kernel, g.G, a.B, g.NT, smem, (cudaStream_t)stream, a, true);
   return (int)e;
 }
 
@@ -466,18 +589,20 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
   int rc = check_problem(p);
   if (rc) return rc;
   if (delta < 1) return SCRF_EDELTA;
-  CkLayout L = ck_layout(p, delta, precision);
+  const FLayout F = f_layout(p, precision);
   const unsigned char* base = (const unsigned char*)ckpt;
   const int nck = (int)n_ckpt_of(p->T, delta);
   size_t total = (size_t)p->B * nck * p->K * p->C;
   ++g_launches;
   const unsigned grid = (unsigned)((total + 255) / 256);
   if (precision)
-    export_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        (const double*)(base + L.alpha), (const double*)(base + L.n), N, (int)p->B, nck, (int)p->K, (int)p->C, omega);
+    export_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)(base + F.Y), (const double*)(base + F.n), N,
+                                                                  p->lengths, (int)p->B, (int)p->T, nck, (int)p->K,
+                                                                  (int)p->C, (int)delta, omega);
   else
-    export_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        (const float*)(base + L.alpha), (const double*)(base + L.n), N, (int)p->B, nck, (int)p->K, (int)p->C, omega);
+    export_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)(base + F.Y), (const double*)(base + F.n), N,
+                                                                 p->lengths, (int)p->B, (int)p->T, nck, (int)p->K,
+                                                                 (int)p->C, (int)delta, omega);
   return (int)cudaGetLastError();
 }
 

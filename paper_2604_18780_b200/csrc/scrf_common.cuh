@@ -49,6 +49,17 @@ struct Mth<double> {
   static __device__ __forceinline__ double tiny() { return 1e-290; }
 };
 
+template <typename R>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using T = float2;
+};
+template <>
+struct Vec2<double> {
+  using T = double2;
+};
+
 // (hi, lo) split of an fp64 value into the working type.
 template <typename R>
 __device__ __forceinline__ void split(double v, R& hi, R& lo) {

@@ -1,0 +1,291 @@
+// Posterior passes on B200 (sm_100a): everything the reference's backward derives from
+// the joint segment marginals mu[b,s,k,c,c'] (pkg/src/streamcrf/streaming.py:357-395,
+// diagnostics.py:54-79), computed data-parallel from the per-position messages the two
+// sweeps stored (scrf_sweep.cuh). Exact identities used (log2 units, Z = logZ):
+//   end mass   E[t,c] = sum_{k,c'} mu(seg ending at t)  = 2^(alpha[t,c] + beta[t,c] - Z)
+//   start mass A[t,c] = sum_{k,c'} mu(seg starting at t) = 2^(gamma[t,c] + delta[t,c] - Z)
+//   grad_T[c',c] = sum_t 2^(alpha[t,c'] + T[c',c] + delta[t,c] - Z)
+//   grad_B[k,c]  = sum_s 2^(ra[s,c] + rb[s+k,c] - Z + B[k-1,c])
+// with ra = gamma - S + Ps (alpha-side source value) and rb = beta + S + Pe (beta side).
+// grad_S[t] = E[t] - A[t]; grad_Ps[t] = A[t]; grad_Pe[t-1] = E[t]; position marginals are
+// the running sum of A - E (coverage difference array); boundary posterior = sum_c A[t,c].
+// All batch/segment reductions are fixed-order (bit-reproducible), as in the reference.
+#pragma once
+
+#include "scrf_common.cuh"
+
+namespace scrf {
+
+template <typename R>
+struct PostArgs {
+  const double* S;
+  const int64_t* lengths;
+  const double* trans;
+  const double* dur;
+  const double* ps;
+  const double* pe;
+  const double* upstream;  // (B,) or null
+  const double* logZ;      // (B,) nats
+  int B, T, K, C;
+  const R *Ya, *Xa, *Yb, *Xb;  // [B][T+1][C]
+  const double *na, *nb;       // [B][T+1]
+  // outputs
+  double* grad_S;  // (B, T+1, C)
+  double* grad_Ps; // (B, T, C) or null
+  double* grad_Pe; // (B, T, C) or null
+  double* pos;     // (B, T, C)
+  double* bnd;     // (B, T)
+  // chunk partials
+  int CH, nch;        // positions per chunk, chunks per sequence
+  double* tot;        // [B][nch][C]  chunk totals of (A - E)
+  double* cntp;       // [B][nch]
+  double* gTp;        // [B][nch][C][C]
+  int SCB, nchB;      // grad_B: sources per CTA, CTAs per sequence
+  int CGB;            // labels per grad_B CTA
+  double* gBp;        // [B][nchB][K][C]
+};
+
+__host__ __device__ inline int post_chunk(int C) {
+  int ch = 256;
+  while (ch > 16 && (size_t)ch * C > 4096) ch >>= 1;
+  return ch;
+}
+
+// pass 1: per (b, chunk) of CH positions: masses, grad_S / grad_P, local coverage scan,
+// boundary posterior, chunk totals, count and grad_T partials.
+template <typename R>
+__global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.y, ch = blockIdx.x;
+  const int C = a.C, T = a.T, CH = a.CH;
+  const int L = (int)a.lengths[b];
+  const int t0 = ch * CH;
+  const int nt = min(CH, T + 1 - t0);
+  double* dA = (double*)sm;                 // [CH][C] start mass
+  double* dE = dA + (size_t)CH * C;         // [CH][C] end mass
+  R* sYa = (R*)(dE + (size_t)CH * C);       // [CH][C]
+  R* sYb = sYa + (size_t)CH * C;            // [CH][C]
+  double* sf = (double*)(sm + ((2 * (size_t)CH * C * sizeof(double) + 2 * (size_t)CH * C * sizeof(R) + 15) & ~(size_t)15));
+  __shared__ double red[256];
+  const double Z2 = a.logZ[b] * kLog2e;
+  const double up = a.upstream ? a.upstream[b] : 1.0;
+  const size_t rb = (size_t)b * (T + 1);
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int t = t0 + i;
+    sf[i] = (t <= L) ? a.na[rb + t] + a.nb[rb + t] - Z2 : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nt * C; e += blockDim.x) {
+    const int i = e / C, c = e % C, t = t0 + i;
+    const size_t o = (rb + t) * C + c;
+    double A = 0.0, E = 0.0;
+    R ya = Mth<R>::ninf(), yb = Mth<R>::ninf();
+    if (t <= L) {
+      const R f = (R)sf[i];
+      ya = a.Ya[o];
+      if (t < L) {
+        yb = a.Yb[o];
+        A = (double)Mth<R>::ex2(f + a.Xa[o] + yb);
+      }
+      if (t >= 1) E = (double)Mth<R>::ex2(f + ya + a.Xb[o]);
+    }
+    dA[e] = A;
+    dE[e] = E;
+    sYa[e] = ya;
+    sYb[e] = yb;
+    a.grad_S[o] = up * (E - A);
+    if (t < T) {
+      if (a.grad_Ps) a.grad_Ps[((size_t)b * T + t) * C + c] = up * A;
+    }
+    if (t >= 1 && a.grad_Pe) a.grad_Pe[((size_t)b * T + t - 1) * C + c] = up * E;
+  }
+  __syncthreads();
+  // boundary posterior and count
+  double cnt = 0.0;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int t = t0 + i;
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += dA[(size_t)i * C + c];
+    cnt += s;
+    if (t < T) a.bnd[(size_t)b * T + t] = (t < L) ? fmin(fmax(s, 0.0), 1.0) : 0.0;
+  }
+  red[threadIdx.x] = cnt;
+  // local coverage scan per label (sequential over the chunk, fp64)
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    double cov = 0.0;
+    for (int i = 0; i < nt; ++i) {
+      const int t = t0 + i;
+      cov += dA[(size_t)i * C + c] - dE[(size_t)i * C + c];
+      if (t < T) a.pos[((size_t)b * T + t) * C + c] = cov;  // carried in pass 2
+    }
+    a.tot[((size_t)b * a.nch + ch) * C + c] = cov;
+  }
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.cntp[(size_t)b * a.nch + ch] = red[0];
+  // grad_T partial: sum over t < L of 2^(f_t + Ya[t,c'] + T2[c',c] + Yb[t,c])
+  for (int pidx = threadIdx.x; pidx < C * C; pidx += blockDim.x) {
+    const int cp = pidx / C, c = pidx % C;
+    const R t2 = (R)(a.trans[pidx] * kLog2e);
+    R acc0 = 0, acc1 = 0;
+    int i = 0;
+    for (; i + 1 < nt; i += 2) {
+      acc0 += Mth<R>::ex2((R)sf[i] + sYa[(size_t)i * C + cp] + t2 + sYb[(size_t)i * C + c]);
+      acc1 += Mth<R>::ex2((R)sf[i + 1] + sYa[(size_t)(i + 1) * C + cp] + t2 + sYb[(size_t)(i + 1) * C + c]);
+    }
+    if (i < nt) acc0 += Mth<R>::ex2((R)sf[i] + sYa[(size_t)i * C + cp] + t2 + sYb[(size_t)i * C + c]);
+    a.gTp[((size_t)b * a.nch + ch) * C * C + pidx] = (double)(acc0 + acc1);
+  }
+}
+
+template <typename R>
+__host__ __device__ inline size_t post_pos_smem(int C, int CH) {
+  return ((2 * (size_t)CH * C * sizeof(double) + 2 * (size_t)CH * C * sizeof(R) + 15) & ~(size_t)15) +
+         (size_t)CH * sizeof(double);
+}
+
+// pass 2: add the carry of the preceding chunks to the local coverage, clip, zero padding
+__global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, int CH, int nch, const double* tot,
+                                  double* pos) {
+  const int b = blockIdx.y, ch = blockIdx.x;
+  const int L = (int)lengths[b];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    double carry = 0.0;
+    for (int q = 0; q < ch; ++q) carry += tot[((size_t)b * nch + q) * C + c];
+    const int t0 = ch * CH;
+    for (int i = 0; i < CH; ++i) {
+      const int t = t0 + i;
+      if (t >= T) break;
+      double* p = pos + ((size_t)b * T + t) * C + c;
+      *p = (t < L) ? fmin(fmax(*p + carry, 0.0), 1.0) : 0.0;
+    }
+  }
+}
+
+// grad_B partial: CTA (b, source range, label group); thread owns (label, duration) pairs.
+// ra[s] / rb[u] are staged per sub-chunk of 128 sources as (hi, lo) pairs in the
+// working type; terms are (ra_hi + rb_hi) + (ra_lo + rb_lo) + B2[k-1].
+constexpr int kGBSub = 128;
+
+template <typename R>
+__global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
+  using R2 = typename Vec2<R>::T;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.z, cg = blockIdx.y, sb = blockIdx.x;
+  const int C = a.C, T = a.T, K = a.K, CG = a.CGB;
+  const int L = (int)a.lengths[b];
+  const int c0 = cg * CG;
+  const int Cn = min(CG, C - c0);
+  const int nU = kGBSub + K;
+  R2* sa = (R2*)sm;                      // [CG][kGBSub]
+  R2* sbv = sa + (size_t)CG * kGBSub;    // [CG][nU]  rb for u = s0+1 .. s0+kGBSub+K
+  R* B2 = (R*)(sbv + (size_t)CG * nU);   // [CG][K]
+  const double Z2 = a.logZ[b] * kLog2e;
+  const size_t rb0 = (size_t)b * (T + 1);
+  for (int i = threadIdx.x; i < Cn * K; i += blockDim.x) {
+    const int cl = i / K, k = i % K;
+    B2[i] = (R)(a.dur[(size_t)k * C + c0 + cl] * kLog2e);
+  }
+  // accumulators: thread owns pairs (cl, k) = idx, idx + blockDim, ...
+  constexpr int MAXP = 8;
+  double acc[MAXP];
+#pragma unroll
+  for (int q = 0; q < MAXP; ++q) acc[q] = 0.0;
+  const int npairs = Cn * K;
+  const int sbeg = sb * a.SCB;
+  const int send = min(sbeg + a.SCB, L);  // sources s < L
+  for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
+    __syncthreads();
+    const int ns = min(kGBSub, send - s0);
+    for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
+      const int cl = i / kGBSub, si = i % kGBSub, s = s0 + si, c = c0 + cl;
+      R2 v;
+      v.x = Mth<R>::ninf();
+      v.y = 0;
+      if (si < ns) {
+        const size_t o = (rb0 + s) * C + c;
+        const double ra = a.na[rb0 + s] + (double)a.Xa[o] - a.S[o] * kLog2e +
+                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
+        split2(ra, v.x, v.y);
+      }
+      sa[(size_t)cl * kGBSub + si] = v;
+    }
+    for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
+      const int cl = i / nU, ui = i % nU, u = s0 + 1 + ui, c = c0 + cl;
+      R2 v;
+      v.x = Mth<R>::ninf();
+      v.y = 0;
+      if (u <= L) {
+        const size_t o = (rb0 + u) * C + c;
+        const double rv = a.nb[rb0 + u] + (double)a.Xb[o] + a.S[o] * kLog2e +
+                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
+        split2(rv, v.x, v.y);
+      }
+      sbv[(size_t)cl * nU + ui] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q) {
+      const int idx = threadIdx.x + q * blockDim.x;
+      if (idx < npairs) {
+        const int cl = idx / K, k = idx % K + 1;
+        const R2* A = sa + (size_t)cl * kGBSub;
+        const R2* Bv = sbv + (size_t)cl * nU + (k - 1);  // u = s + k -> ui = si + k - 1
+        const R bk = B2[(size_t)cl * K + k - 1];
+        R s0a = 0, s1a = 0;
+        int si = 0;
+        for (; si + 1 < ns; si += 2) {
+          const R2 x0 = A[si], y0 = Bv[si], x1 = A[si + 1], y1 = Bv[si + 1];
+          s0a += Mth<R>::ex2(((x0.x + y0.x) + (x0.y + y0.y)) + bk);
+          s1a += Mth<R>::ex2(((x1.x + y1.x) + (x1.y + y1.y)) + bk);
+        }
+        if (si < ns) {
+          const R2 x0 = A[si], y0 = Bv[si];
+          s0a += Mth<R>::ex2(((x0.x + y0.x) + (x0.y + y0.y)) + bk);
+        }
+        acc[q] += (double)(s0a + s1a);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXP; ++q) {
+    const int idx = threadIdx.x + q * blockDim.x;
+    if (idx < npairs) {
+      const int cl = idx / K, k = idx % K;
+      a.gBp[(((size_t)b * a.nchB + sb) * K + k) * C + c0 + cl] = acc[q];
+    }
+  }
+}
+
+template <typename R>
+__host__ __device__ inline size_t post_gradB_smem(int K, int CG) {
+  return (size_t)CG * kGBSub * 2 * sizeof(R) + (size_t)CG * (kGBSub + K) * 2 * sizeof(R) + (size_t)CG * K * sizeof(R) + 16;
+}
+
+// fixed-order reductions: per-sequence partials (unscaled) and batch totals (upstream-weighted)
+__global__ void post_reduce_kernel(int B, int n, int nparts, const double* parts, const double* upstream,
+                                   double* per_seq, double* total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double tot = 0.0;
+  for (int b = 0; b < B; ++b) {
+    double s = 0.0;
+    for (int q = 0; q < nparts; ++q) s += parts[((size_t)b * nparts + q) * n + i];
+    if (per_seq) per_seq[(size_t)b * n + i] = s;
+    tot += (upstream ? upstream[b] : 1.0) * s;
+  }
+  if (total) total[i] = tot;
+}
+
+__global__ void post_count_kernel(int B, int nch, const double* cntp, double* count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int q = 0; q < nch; ++q) s += cntp[(size_t)b * nch + q];
+  count[b] = s;
+}
+
+}  // namespace scrf

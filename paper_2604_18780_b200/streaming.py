@@ -199,29 +199,76 @@ def device_backward(prob: DeviceProblem, fwd: DeviceForward, upstream: torch.Ten
     lib = _lib.load()
     prec = PRECISIONS[fwd.precision]
     p = prob.c_struct()
+    bw = _alloc_backward(prob, prec, fwd.delta, want_proj_grads)
+    if upstream is not None:
+        upstream = upstream.to(device=prob.S.device, dtype=torch.float64).contiguous()
+    rc = lib.scrf_backward(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.ckpt), _lib.ptr(upstream),
+                           _lib.ptr(bw.grad_S), _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B), _lib.ptr(bw.grad_P_start),
+                           _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals), _lib.ptr(bw.boundary_posterior),
+                           _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work), bw.work.numel(),
+                           _lib.stream_handle())
+    _lib.check(rc, "scrf_backward")
+    return bw
+
+
+def _alloc_backward(prob: DeviceProblem, prec: int, delta: int, want_proj_grads: bool | None):
+    lib = _lib.load()
+    p = prob.c_struct()
     nbytes = ctypes_size()
-    _lib.check(lib.scrf_backward_work_bytes(p, fwd.delta, prec, nbytes), "scrf_backward_work_bytes")
+    _lib.check(lib.scrf_backward_work_bytes(p, delta, prec, nbytes), "scrf_backward_work_bytes")
     dev = prob.S.device
     B, T, K, C = prob.B, prob.T, prob.K, prob.C
     f64 = dict(dtype=torch.float64, device=dev)
-    work = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
-    gS = torch.empty((B, T + 1, C), **f64)
-    gT = torch.empty((C, C), **f64)
-    gB = torch.empty((K, C), **f64)
     if want_proj_grads is None:
         want_proj_grads = prob.proj_start is not None or prob.proj_end is not None
-    gPs = torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_start is not None else None
-    gPe = torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_end is not None else None
-    pos = torch.empty((B, T, C), **f64)
-    bnd = torch.empty((B, T), **f64)
-    cnt = torch.empty((B,), **f64)
+    return DeviceBackward(
+        grad_S=torch.empty((B, T + 1, C), **f64), grad_T=torch.empty((C, C), **f64),
+        grad_B=torch.empty((K, C), **f64),
+        grad_P_start=torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_start is not None else None,
+        grad_P_end=torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_end is not None else None,
+        position_marginals=torch.empty((B, T, C), **f64), boundary_posterior=torch.empty((B, T), **f64),
+        expected_segment_count=torch.empty((B,), **f64),
+        work=torch.empty(nbytes.value, dtype=torch.uint8, device=dev))
+
+
+def device_posterior(prob: DeviceProblem, delta: int | None = None, upstream: torch.Tensor | None = None,
+                     precision: str | None = None, want_proj_grads: bool | None = None):
+    """Forward + backward in one call (alpha and beta sweeps run concurrently); no host sync."""
+    lib = _lib.load()
+    precision = precision or _default_precision
+    prec = PRECISIONS[precision]
+    delta = choose_checkpoint_interval(prob.T, prob.K) if delta is None else int(delta)
+    if delta < 1:
+        raise ValueError(f"checkpoint interval must be >= 1, got {delta}")
+    p = prob.c_struct()
+    nbytes = ctypes_size()
+    _lib.check(lib.scrf_checkpoint_bytes(p, delta, prec, nbytes), "scrf_checkpoint_bytes")
+    dev = prob.S.device
+    n_ckpt = -(-prob.T // delta)
+    fwd = DeviceForward(torch.empty(prob.B, dtype=torch.float64, device=dev),
+                        torch.empty((prob.B, n_ckpt), dtype=torch.float64, device=dev),
+                        torch.empty(prob.B, dtype=torch.int32, device=dev),
+                        torch.empty(nbytes.value, dtype=torch.uint8, device=dev), delta, precision)
+    bw = _alloc_backward(prob, prec, delta, want_proj_grads)
     if upstream is not None:
         upstream = upstream.to(device=dev, dtype=torch.float64).contiguous()
-    rc = lib.scrf_backward(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.ckpt), _lib.ptr(upstream),
-                           _lib.ptr(gS), _lib.ptr(gT), _lib.ptr(gB), _lib.ptr(gPs), _lib.ptr(gPe), _lib.ptr(pos),
-                           _lib.ptr(bnd), _lib.ptr(cnt), _lib.ptr(work), nbytes.value, _lib.stream_handle())
-    _lib.check(rc, "scrf_backward")
-    return DeviceBackward(gS, gT, gB, gPs, gPe, pos, bnd, cnt, work)
+    rc = lib.scrf_posterior(p, delta, prec, _lib.ptr(upstream), _lib.ptr(fwd.logZ), _lib.ptr(fwd.N),
+                            _lib.ptr(fwd.dead_at), _lib.ptr(fwd.ckpt), fwd.ckpt.numel(), _lib.ptr(bw.grad_S),
+                            _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B), _lib.ptr(bw.grad_P_start),
+                            _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals),
+                            _lib.ptr(bw.boundary_posterior), _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work),
+                            bw.work.numel(), _lib.stream_handle())
+    _lib.check(rc, "scrf_posterior")
+    return fwd, bw
+
+
+def device_beta_logz(prob: DeviceProblem, fwd: DeviceForward, bw: DeviceBackward) -> torch.Tensor:
+    """logZ recomputed from the beta sweep (consistency check of the two sweeps)."""
+    lib = _lib.load()
+    out = torch.empty(prob.B, dtype=torch.float64, device=prob.S.device)
+    _lib.check(lib.scrf_beta_logz(prob.c_struct(), PRECISIONS[fwd.precision], _lib.ptr(bw.work), _lib.ptr(out),
+                                  _lib.stream_handle()), "scrf_beta_logz")
+    return out
 
 
 def device_grad_partials(prob: DeviceProblem, fwd: DeviceForward, bwd: DeviceBackward):
@@ -367,14 +414,20 @@ def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts
     bw = device_backward(prob, fwd_used, up_t)
     if ledger is not None:
         ledger.record("workspace", bw.work)
-    grads = GradientSet(
+    return _grads_to_host(bw), _marg_to_host(bw, cum)
+
+
+def _grads_to_host(bw: DeviceBackward) -> GradientSet:
+    return GradientSet(
         grad_S=bw.grad_S.cpu().numpy(), grad_T=bw.grad_T.cpu().numpy(), grad_B=bw.grad_B.cpu().numpy(),
         grad_P_start=None if bw.grad_P_start is None else bw.grad_P_start.cpu().numpy(),
         grad_P_end=None if bw.grad_P_end is None else bw.grad_P_end.cpu().numpy(),
     )
-    marg = MarginalSet(bw.position_marginals.cpu().numpy(), bw.boundary_posterior.cpu().numpy(),
+
+
+def _marg_to_host(bw: DeviceBackward, cum: CumulativeScores) -> MarginalSet:
+    return MarginalSet(bw.position_marginals.cpu().numpy(), bw.boundary_posterior.cpu().numpy(),
                        bw.expected_segment_count.cpu().numpy(), np.asarray(cum.lengths))
-    return grads, marg
 
 
 def _segments_to_host(v: DeviceViterbi) -> list[Segmentation]:
@@ -403,10 +456,27 @@ def forward_logZ(cum, params, delta=None, backend=None, *, ledger=None, stats=No
 
 
 def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None):
-    """(logZ, GradientSet, MarginalSet) — streaming.py:725-746."""
-    logZ, ck = streaming_forward(cum, params, delta, ledger=ledger, stats=stats)
-    grads, marg = streaming_backward(cum, params, logZ, ck, upstream, ledger=ledger, stats=stats)
-    return logZ, grads, marg
+    """(logZ, GradientSet, MarginalSet) — streaming.py:725-746.
+
+    One fused device call (scrf_posterior): the alpha and beta sweeps run concurrently.
+    """
+    _check_labels(cum, params)
+    if delta is not None and int(delta) < 1:
+        raise ValueError(f"checkpoint interval must be >= 1, got {int(delta)}")
+    B = cum.batch_size
+    up_t = None
+    if upstream is not None:
+        up = np.asarray(upstream, dtype=np.float64)
+        if up.shape != (B,):
+            raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
+        up_t = torch.as_tensor(up)
+    prob = DeviceProblem.from_host(cum, params)
+    fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device))
+    _raise_if_dead(fwd)
+    if ledger is not None:
+        ledger.record("checkpoints", fwd.ckpt)
+        ledger.record("workspace", bw.work)
+    return fwd.logZ.cpu().numpy(), _grads_to_host(bw), _marg_to_host(bw, cum)
 
 
 def decode(cum, params, backend=None, *, ledger=None):
