@@ -1,5 +1,5 @@
 // C ABI of libscrf.so (declared in include/scrf.h): geometry selection, buffer
-// layout and kernel launches. Host code only; kernels live in scrf_fb.cu and
+// layout and kernel launches. Host code only; kernels live in scrf_sweep.cuh, scrf_post.cuh and
 // scrf_viterbi.cu (compiled into this translation unit so templates instantiate once).
 #include <cuda_runtime.h>
 #include <math.h>
@@ -137,6 +137,8 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
     g.kc = K;
     g.KRm = pow2_ceil(K) - 1;
     g.KTm = 0;
+    g.WPL = 1;
+    g.TBlk = 0;
     g.GWn = near_gw(K > 4 ? K - 4 : 1);
     g.NNW = 2 * ((C * g.GWn + 31) / 32);
     g.NT = (2 * g.NCW + g.NNW) * 32;
@@ -152,7 +154,10 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
   g.KTm = pow2_ceil(K) - 1;
   g.GWn = near_gw(kNear - 4);
   g.NNW = 2 * ((C * g.GWn + 31) / 32);
-  int tails = forced > 1 ? forced - 1 : (int)(((long long)K * C + 3499) / 3500);
+  // blocked tails (one warp per label, <= 8 labels per tail) when the duration range allows
+  const bool blk = env_int("SCRF_TAIL_EXACT", 0) == 0 && K >= kNear + 33 && K <= 1024 + kNear;
+  g.TBlk = blk ? 1 : 0;
+  int tails = forced > 1 ? forced - 1 : (blk ? (C + 7) / 8 : (int)(((long long)K * C + 3499) / 3500));
   const int maxt = C < 15 ? C : 15;
   if (tails > maxt) tails = maxt;
   if (tails < 1) tails = 1;
@@ -162,7 +167,18 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
     if (tails > maxt) return SCRF_ECONFIG;
     g.G = 1 + tails;
     g.CgMax = (C + tails - 1) / tails;
-    g.NWt = g.CgMax < 16 ? g.CgMax : 16;
+    g.WPL = 1;
+    if (g.TBlk) {
+      if (g.CgMax > 16) {  // blocked tails need one warp per label
+        g.TBlk = 0;
+        g.KTm = pow2_ceil(K) - 1;
+      } else {
+        g.KTm = 63;
+      }
+    }
+    if (!g.TBlk)
+      while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
+    g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
     const int head_nt = (2 * g.NCW + g.NNW) * 32;
     g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
     size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);

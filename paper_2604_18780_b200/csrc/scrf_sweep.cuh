@@ -104,7 +104,9 @@ struct SweepGeo {
   int NCW;    // chain warps (ceil(C/32)); aux warps = NCW
   int NNW;    // near warps
   int GWn;    // near threads per label (power of two <= 32)
-  int NWt;    // tail warps (one label per warp at a time)
+  int NWt;    // tail warps
+  int WPL;    // tail warps per label (each pushes its own partial)
+  int TBlk;   // 1: blocked tails (exp-space source blocks, FMA); 0: exact per-term tails
   int CgMax;  // max labels per tail
   int NT;     // block size (max over roles)
   int Msm;    // exp-space transition matrix staged in shared memory
@@ -143,8 +145,12 @@ struct HeadLayout {
   size_t M, Xmax, B2, ring, stg, oq, own, pubY, pubX, pubA, nring, part, hh, h3, ew, wmax, tpart, tbar, total;
 };
 struct TailLayout {
-  size_t ring, B2, nslot, tbar, stg, total;
+  size_t ring, B2, nslot, tbar, stg, wtab, bx, total;
 };
+
+// blocked tails: exp-space source blocks of 32 held in registers (one block per lane)
+constexpr int kBlk = 32;
+__host__ __device__ inline int blk_wlen(int kc) { return (1024 + 64 + kc + 1) & ~1; }
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -169,7 +175,7 @@ __host__ __device__ inline HeadLayout head_layout(int K, int C, const SweepGeo& 
   L.h3 = o;    o += a16((size_t)8 * C * sizeof(R));
   L.ew = o;    o += a16(Cw * sizeof(R));
   L.wmax = o;  o += a16(32 * sizeof(R));
-  L.tpart = o; o += a16((size_t)kSlots * C * 2 * sizeof(R));
+  L.tpart = o; o += a16((size_t)kSlots * g.WPL * C * 2 * sizeof(R));
   L.tbar = o;  o += a16(kSlots * sizeof(uint64_t));
   L.total = o;
   return L;
@@ -180,10 +186,12 @@ __host__ __device__ inline TailLayout tail_layout(int K, int C, const SweepGeo& 
   TailLayout L;
   size_t o = 0;
   L.ring = o;  o += a16((size_t)g.CgMax * (g.KTm + 1) * 2 * sizeof(R));
-  L.B2 = o;    o += a16((size_t)g.CgMax * K * sizeof(R));
+  L.B2 = o;    o += g.TBlk ? 0 : a16((size_t)g.CgMax * K * sizeof(R));
   L.nslot = o; o += a16(kSlots * sizeof(double));
   L.tbar = o;  o += a16(kSlots * sizeof(uint64_t));
   L.stg = o;   o += a16((size_t)kStage * 2 * g.CgMax * sizeof(double));
+  L.wtab = o;  o += g.TBlk ? a16((size_t)g.CgMax * 2 * blk_wlen(g.kc) * sizeof(R)) : 0;
+  L.bx = o;    o += g.TBlk ? a16((size_t)g.CgMax * (kBlk + 1) * sizeof(R)) : 0;
   L.total = o;
   return L;
 }
@@ -239,27 +247,34 @@ __device__ __forceinline__ R lse3(R m, R s, R x2, R x1) {
 template <typename R>
 __device__ __forceinline__ void ring_sum(const typename Vec2<R>::T* rg, int mask, const R* b2, int k0, int kstep,
                                          int kmax, int slot0, R e_hi, R e_lo, R mref, R& sum, R& dmax) {
-  R a0 = 0, a1 = 0, d0 = Mth<R>::ninf(), d1 = Mth<R>::ninf();
+  R a0 = 0, a1 = 0, a2 = 0, a3 = 0, d0 = Mth<R>::ninf(), d1 = Mth<R>::ninf();
   int k = k0, slot = slot0;
-  for (; k + kstep <= kmax; k += 2 * kstep) {
+  const R c_lo = e_lo - mref;  // (r.x + e_hi) + (r.y + e_lo - mref) + b
+  for (; k + 3 * kstep <= kmax; k += 4 * kstep) {
     const auto r0 = rg[slot];
-    slot = (slot - kstep) & mask;
-    const auto r1 = rg[slot];
-    slot = (slot - kstep) & mask;
-    const R x0 = ((r0.x + e_hi) + (r0.y + e_lo) + b2[k - 1]) - mref;
-    const R x1 = ((r1.x + e_hi) + (r1.y + e_lo) + b2[k + kstep - 1]) - mref;
-    d0 = fmax(d0, x0);
-    d1 = fmax(d1, x1);
+    const auto r1 = rg[(slot - kstep) & mask];
+    const auto r2 = rg[(slot - 2 * kstep) & mask];
+    const auto r3 = rg[(slot - 3 * kstep) & mask];
+    slot = (slot - 4 * kstep) & mask;
+    const R x0 = ((r0.x + e_hi) + (r0.y + c_lo)) + b2[k - 1];
+    const R x1 = ((r1.x + e_hi) + (r1.y + c_lo)) + b2[k + kstep - 1];
+    const R x2 = ((r2.x + e_hi) + (r2.y + c_lo)) + b2[k + 2 * kstep - 1];
+    const R x3 = ((r3.x + e_hi) + (r3.y + c_lo)) + b2[k + 3 * kstep - 1];
+    d0 = fmax(d0, fmax(x0, x1));
+    d1 = fmax(d1, fmax(x2, x3));
     a0 += Mth<R>::ex2(x0);
     a1 += Mth<R>::ex2(x1);
+    a2 += Mth<R>::ex2(x2);
+    a3 += Mth<R>::ex2(x3);
   }
-  if (k <= kmax) {
+  for (; k <= kmax; k += kstep) {
     const auto r0 = rg[slot];
-    const R x0 = ((r0.x + e_hi) + (r0.y + e_lo) + b2[k - 1]) - mref;
+    slot = (slot - kstep) & mask;
+    const R x0 = ((r0.x + e_hi) + (r0.y + c_lo)) + b2[k - 1];
     d0 = fmax(d0, x0);
     a0 += Mth<R>::ex2(x0);
   }
-  sum += a0 + a1;
+  sum += (a0 + a1) + (a2 + a3);
   dmax = fmax(dmax, fmax(d0, d1));
 }
 
@@ -675,6 +690,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       if (act) {
         r4 = source(q);
         split2(oqc[(size_t)(p & (kStage - 1)) * C].x - n_q, e_hi, e_lo);
+        if (tr) tr[7] = clock64();
         if (j == 0) {
           ringc[q & KRm] = r4;
           if (q >= 1) ringc[(q - 1) & KRm] = source(q - 1);
@@ -697,15 +713,19 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     if (TAILS && p >= kc + 1) {
       const int pi = p - kc - 1;
       const int sl = pi & (kSlots - 1);
+      if (tr) tr[5] = clock64();
       mbar_wait(smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1));
-      if (act) {
-        const R2 tp = tpartc[(size_t)sl * C];
+      if (tr) tr[6] = clock64();
+      if (act && j == 0) {
         const double d = n_q - h.nring[pi & (kSlots - 1)];  // tail frame n_{p-kc-1} -> n_{p-4}
         R d_hi, d_lo;
         split2(d, d_hi, d_lo);
-        lse_merge(m, s, (tp.x - d_hi) - d_lo, tp.y);
+        const R2* tp = tpartc + (size_t)sl * g.WPL * C;
+        R tm = tp[0].x, ts = tp[0].y;
+        for (int w = 1; w < g.WPL; ++w) lse_merge(tm, ts, tp[w * C].x, tp[w * C].y);
+        lse_merge(m, s, (tm - d_hi) - d_lo, ts);
       }
-      if (gtid == 0 && p + kSlots <= L) mbar_expect(smem_u32(&h.tbar[sl]), (uint32_t)(C * 2 * sizeof(R)));
+      if (gtid == 0 && p + kSlots <= L) mbar_expect(smem_u32(&h.tbar[sl]), (uint32_t)(g.WPL * C * 2 * sizeof(R)));
     }
     if (act && j == 0) {
       R2 pm;
@@ -858,7 +878,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     }
     if (TAILS && tid == 0) {
       mbar_fence_init();
-      for (int q = 0; q < kSlots; ++q) mbar_expect(smem_u32(&h.tbar[q]), (uint32_t)(C * 2 * sizeof(R)));
+      for (int q = 0; q < kSlots; ++q) mbar_expect(smem_u32(&h.tbar[q]), (uint32_t)(g.WPL * C * 2 * sizeof(R)));
     }
   }
   __syncthreads();
@@ -899,10 +919,14 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     else
       d[1] = 0.0;
   };
+  const int WPL = g.WPL;
+  const int part = warp % WPL;         // k sub-range of this warp
+  const int cl0 = warp / WPL;          // first label of this warp
+  const int lstep = g.NWt / WPL;       // label stride across warps
   const int u0 = kc + 1;
   for (int i = 0; i < kAhead; ++i) {
     if (lane == 0 && u0 + i <= L)
-      for (int cl = warp; cl < Cg; cl += g.NWt) stage(u0 + i, cl);
+      for (int cl = cl0; cl < Cg; cl += lstep) stage(u0 + i, cl);
     cp_async_commit();
   }
   const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
@@ -910,14 +934,18 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   int sn = 0;  // ring slot of the newest source s_new = u - kc - 1
   for (int u = u0; u <= L; ++u) {
     const int s_new = u - kc - 1;
+    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= 64 && u < 64 + 256) ? a.trace + 256 * 16 + (u - 64) * 16 : nullptr;
+    if (tr) tr[0] = clock64();
     cp_async_wait<kAhead - 1>();
     __syncwarp();
+    if (tr) tr[1] = clock64();
     mbar_wait(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1));
+    if (tr) tr[2] = clock64();
     if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
       mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
     const double F = nslot[s_new & (kSlots - 1)];
     const int kmax = min(K, u);
-    for (int cl = warp; cl < Cg; cl += g.NWt) {
+    for (int cl = cl0; cl < Cg; cl += lstep) {
       const R2* rg = ring + (size_t)cl * (KTm + 1);
       const R* b2 = B2 + (size_t)cl * K;
       const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
@@ -928,16 +956,153 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       const R2 r0 = rg[sn];
       const R mref = (r0.x + e_hi) + (r0.y + e_lo) + b2[kc];
       R m, s;
-      ring_lse<R>(rg, KTm, b2, kc + 2 + lane, 32, kmax, (sn - 1 - lane) & KTm, e_hi, e_lo, mref, lane == 0, 32, m, s);
+      const int ko = lane + 32 * part;
+      ring_lse<R>(rg, KTm, b2, kc + 2 + ko, 32 * WPL, kmax, (sn - 1 - ko) & KTm, e_hi, e_lo, mref, ko == 0, 32, m, s);
+      if (tr) tr[3] = clock64();
       if (lane == 0) {
-        const uint32_t off = (uint32_t)(((size_t)(s_new & (kSlots - 1)) * C + lo + cl) * 2 * sizeof(R));
+        const uint32_t off = (uint32_t)((((size_t)(s_new & (kSlots - 1)) * WPL + part) * C + lo + cl) * 2 * sizeof(R));
         st_async_pair<R>(hpart + off, m, s, hbar + (uint32_t)((s_new & (kSlots - 1)) * sizeof(uint64_t)));
       }
     }
     if (lane == 0 && u + kAhead <= L)
-      for (int cl = warp; cl < Cg; cl += g.NWt) stage(u + kAhead, cl);
+      for (int cl = cl0; cl < Cg; cl += lstep) stage(u + kAhead, cl);
     cp_async_commit();
     sn = (sn + 1) & KTm;
+  }
+  cp_async_wait<0>();
+}
+
+
+// Blocked tail (TBlk): for target u the durations kc+1..K are the sources
+// s in [u-K, u-kc-1]. Sources are grouped in blocks of 32 (block j = [32j, 32j+31]).
+// When block j completes, its values become z[i] = 2^(r[32j+i] - G_j) (G_j = block max)
+// held in 32 registers of lane j % 32, and the block's contribution to target u is
+//   2^(G_j + e[u] + Bmax) * sum_i z[i] * w[u - 32j - i],   w[k] = 2^(B[k-1] - Bmax) (0 outside kc+1..K)
+// a 32-term FMA dot product against a sliding window of w (two shifted copies in SMEM
+// so every window is an aligned 8-byte load). The newest, incomplete block is summed
+// term by term. Requires kc + 32 <= K and K <= 1024 + kc (one block per lane).
+template <typename R>
+__device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
+                                  const TailLayout& TL, int lo, int Cg) {
+  using R2 = typename Vec2<R>::T;
+  const SweepGeo& g = a.geo;
+  const int K = a.K, C = a.C, T = a.T, L = x.L, kc = g.kc, KTm = g.KTm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = warp;  // one label per warp
+  const R2* rg = (const R2*)(smem + TL.ring) + (size_t)cl * (KTm + 1);
+  const double* nslot = (const double*)(smem + TL.nslot);
+  uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
+  double* stg = (double*)(smem + TL.stg);
+  const int WLEN = blk_wlen(kc);
+  const R* wt = (const R*)(smem + TL.wtab) + (size_t)cl * 2 * WLEN;
+  const R* bx = (const R*)(smem + TL.bx) + (size_t)cl * (kBlk + 1);
+  const R bmax = bx[kBlk];
+  auto stage = [&](int u) {
+    const int t = x.tpos(u), c = lo + cl;
+    double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
+    cp_async8(d, x.S + (size_t)t * C + c);
+    if (x.dir == 0 && x.pe && t >= 1)
+      cp_async8(d + 1, x.pe + (size_t)(t - 1) * C + c);
+    else if (x.dir == 1 && x.ps && t < T)
+      cp_async8(d + 1, x.ps + (size_t)t * C + c);
+    else
+      d[1] = 0.0;
+  };
+  const int u0 = kc + 1;
+  for (int i = 0; i < kAhead; ++i) {
+    if (lane == 0 && u0 + i <= L) stage(u0 + i);
+    cp_async_commit();
+  }
+  const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
+  const uint32_t hpart = mapa_u32(smem_u32(smem + HL.tpart), 0);
+  R zr[kBlk];
+#pragma unroll
+  for (int i = 0; i < kBlk; ++i) zr[i] = 0;
+  R Gh = Mth<R>::ninf(), Gl = 0;
+  int jown = -1;
+  for (int u = u0; u <= L; ++u) {
+    const int s_new = u - kc - 1;
+    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= 64 && u < 64 + 256) ? a.trace + 256 * 16 + (u - 64) * 16 : nullptr;
+    if (tr) tr[0] = clock64();
+    cp_async_wait<kAhead - 1>();
+    __syncwarp();
+    if (tr) tr[1] = clock64();
+    mbar_wait(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1));
+    if (tr) tr[2] = clock64();
+    if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
+      mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
+    const double F = nslot[s_new & (kSlots - 1)];
+    R e_hi, e_lo;
+    {
+      const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
+      const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
+      split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - F, e_hi, e_lo);
+    }
+    const int inb = s_new & (kBlk - 1);
+    if (inb == kBlk - 1) {
+      // block jb = s_new / 32 completes: frame = its largest source, z into the owner lane
+      const int jb = s_new >> 5;
+      const R2 r = rg[(jb * kBlk + lane) & KTm];
+      const R gh = warp_max(r.x);
+      const unsigned bal = __ballot_sync(0xffffffffu, r.x == gh);
+      const R gl = __shfl_sync(0xffffffffu, r.y, __ffs(bal) - 1);
+      const R z = (gh == Mth<R>::ninf() || r.x == Mth<R>::ninf()) ? (R)0 : Mth<R>::ex2((r.x - gh) + (r.y - gl));
+      const bool own = lane == (jb & 31);
+#pragma unroll
+      for (int i = 0; i < kBlk; ++i) {
+        const R v = __shfl_sync(0xffffffffu, z, i);
+        if (own) zr[i] = v;
+      }
+      if (own) {
+        Gh = gh;
+        Gl = gl;
+        jown = jb;
+      }
+    }
+    // contribution of the lane's complete block
+    R xb = Mth<R>::ninf(), pb = 0;
+    if (jown >= 0 && Gh != Mth<R>::ninf()) {
+      const int dd = u - jown * kBlk;  // duration of the block's source 0
+      const int base = dd - (kBlk - 1);
+      if (base <= K) {
+        const int m = base & 1;
+        const typename Vec2<R>::T* wp = (const typename Vec2<R>::T*)(wt + (size_t)m * WLEN + base + m);
+        R p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+#pragma unroll
+        for (int i2 = 0; i2 < kBlk / 2; i2 += 2) {
+          const auto w01 = wp[i2];      // w[base + 2*i2], w[base + 2*i2 + 1]
+          const auto w23 = wp[i2 + 1];  // w[base + 2*i2 + 2], w[base + 2*i2 + 3]
+          // source i has duration dd - i = base + (31 - i)
+          p0 += zr[31 - 2 * i2] * w01.x;
+          p1 += zr[30 - 2 * i2] * w01.y;
+          p2 += zr[29 - 2 * i2] * w23.x;
+          p3 += zr[28 - 2 * i2] * w23.y;
+        }
+        pb = (p0 + p1) + (p2 + p3);
+        if (pb > (R)0) xb = (Gh + e_hi) + (Gl + e_lo) + bmax;
+      }
+    }
+    // the newest incomplete block, term by term (durations kc+1 .. kc+32)
+    R xe = Mth<R>::ninf();
+    if (inb != kBlk - 1 && lane <= inb) {
+      const int sidx = s_new - inb + lane;
+      const R2 r = rg[sidx & KTm];
+      xe = (r.x + e_hi) + (r.y + e_lo) + bx[u - sidx - kc - 1];
+    }
+    if (tr) tr[3] = clock64();
+    const R M = warp_max(fmax(xb, xe));
+    R sum = 0;
+    if (M != Mth<R>::ninf()) {
+      if (xb != Mth<R>::ninf()) sum += pb * Mth<R>::ex2(xb - M);
+      if (xe != Mth<R>::ninf()) sum += Mth<R>::ex2(xe - M);
+    }
+    sum = gsum(sum, 32);
+    if (lane == 0) {
+      const uint32_t off = (uint32_t)(((size_t)(s_new & (kSlots - 1)) * C + lo + cl) * 2 * sizeof(R));
+      st_async_pair<R>(hpart + off, M, sum, hbar + (uint32_t)((s_new & (kSlots - 1)) * sizeof(uint64_t)));
+      if (u + kAhead <= L) stage(u + kAhead);
+    }
+    cp_async_commit();
   }
   cp_async_wait<0>();
 }
@@ -951,9 +1116,35 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   const int lo = tail_lo(x.rank, C, g.G), Cg = tail_lo(x.rank + 1, C, g.G) - lo;
   R* B2 = (R*)(smem + TL.B2);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
-  for (int i = tid; i < Cg * K; i += blockDim.x) {
-    const int cl = i / K, k = i % K;
-    B2[i] = (R)(a.dur[(size_t)k * C + lo + cl] * kLog2e);
+  if (g.TBlk) {
+    const int WLEN = blk_wlen(g.kc);
+    R* bx = (R*)(smem + TL.bx);
+    R* wt = (R*)(smem + TL.wtab);
+    for (int cl = tid; cl < Cg; cl += blockDim.x) {  // per-label max duration bias and near-duration table
+      double m = -CUDART_INF;
+      for (int k = g.kc + 1; k <= K; ++k) m = fmax(m, a.dur[(size_t)(k - 1) * C + lo + cl] * kLog2e);
+      bx[(size_t)cl * (kBlk + 1) + kBlk] = (R)m;
+      for (int i = 0; i < kBlk; ++i) {
+        const int k = g.kc + 1 + i;
+        bx[(size_t)cl * (kBlk + 1) + i] = k <= K ? (R)(a.dur[(size_t)(k - 1) * C + lo + cl] * kLog2e) : Mth<R>::ninf();
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < Cg * 2 * WLEN; i += blockDim.x) {
+      const int cl = i / (2 * WLEN), r = i % (2 * WLEN), m = r / WLEN, y = r % WLEN;
+      const int k = y - m;  // copy m holds w[y - m]
+      R v = 0;
+      if (k >= g.kc + 1 && k <= K) {
+        const R bm = bx[(size_t)cl * (kBlk + 1) + kBlk];
+        v = Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + lo + cl] * kLog2e) - bm);
+      }
+      wt[i] = v;
+    }
+  } else {
+    for (int i = tid; i < Cg * K; i += blockDim.x) {
+      const int cl = i / K, k = i % K;
+      B2[i] = (R)(a.dur[(size_t)k * C + lo + cl] * kLog2e);
+    }
   }
   if (tid < kSlots) mbar_init(smem_u32(&tbar[tid]), 1);
   __syncthreads();
@@ -963,7 +1154,12 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   }
   __syncthreads();
   cluster_sync_all();
-  if ((tid >> 5) < g.NWt) tail_loop<R>(a, x, smem, HL, TL, lo, Cg);
+  if ((tid >> 5) < g.NWt) {
+    if (g.TBlk)
+      tail_loop_blocked<R>(a, x, smem, HL, TL, lo, Cg);
+    else
+      tail_loop<R>(a, x, smem, HL, TL, lo, Cg);
+  }
 }
 
 // ----------------------------------------------------------------------------
