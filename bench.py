@@ -204,17 +204,11 @@ def run_ours(args, rank, world, local):
     bwd_ms, fwd_ms = [], []
     launches = [0]
 
+    from paper_2604_18780_b200.dist import reduce_shared_grads
+
     def exchange(fwd, bw):
-        # the path's only collective: fixed-order sum of per-rank grad_T / grad_B partials
-        if dist is None:
-            return bw.grad_T, bw.grad_B
-        flat = torch.cat([bw.grad_T.reshape(-1), bw.grad_B.reshape(-1)])
-        gathered = [torch.empty_like(flat) for _ in range(world)]
-        dist.all_gather(gathered, flat)
-        tot = gathered[0].clone()
-        for g in gathered[1:]:
-            tot += g
-        return tot[: C * C].view(C, C), tot[C * C:].view(K, C)
+        # the path's only collective: fixed-rank-order sum of grad_T / grad_B partials
+        return reduce_shared_grads(bw.grad_T, bw.grad_B)
 
     def step(record: bool):
         fwd, bw = S.device_posterior(prob)

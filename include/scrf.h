@@ -133,6 +133,10 @@ void scrf_profile_events(void* start, void* stop);
  * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);
 
+/* Debug: with SCRF_WATCHDOG=1 in the environment, sweep mbarrier waits trap after ~1e8
+ * polls instead of hanging; this returns 1 and {flag, block, thread, site, index} if one fired. */
+int scrf_debug_hang(int* out5);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ _SIGS = {
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
     "scrf_debug_trace": (None, [_vp]),
+    "scrf_debug_hang": (_int, [_vp]),
 }
 
 _lock = threading.Lock()

@@ -21,6 +21,7 @@ thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev_start = nullptr;
 thread_local cudaEvent_t g_ev_stop = nullptr;
 thread_local long long* g_trace = nullptr;  // debug: clock64 phase stamps of the next sweep
+int* g_hang = nullptr;                        // debug: watchdog record (SCRF_WATCHDOG=1)
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -115,10 +116,12 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 // sweep geometry (scrf_sweep.cuh): head-only CTA when the duration range is small,
 // otherwise a head + label-slice tails cluster sized to one wave of the chip.
 
-int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
+int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool has_pe, SweepGeo* out) {
   const size_t limit = (size_t)smem_optin();
   SweepGeo g;
   memset(&g, 0, sizeof(g));
+  g.PsRow = has_ps ? 1 : 0;
+  g.PeRow = has_pe ? (has_ps ? 2 : 1) : 0;
   g.NCW = (C + 31) / 32;
   if (g.NCW > 4) return SCRF_ECONFIG;  // C <= 128 (head roles fit one 512-thread CTA)
   g.Msm = (size_t)C * C * (prec ? 8 : 4) <= 65536 ? 1 : 0;
@@ -154,36 +157,45 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, SweepGeo* out) {
   g.KTm = pow2_ceil(K) - 1;
   g.GWn = near_gw(kNear - 4);
   g.NNW = 2 * ((C * g.GWn + 31) / 32);
-  // blocked tails (one warp per label, <= 8 labels per tail) when the duration range allows
-  const bool blk = env_int("SCRF_TAIL_EXACT", 0) == 0 && K >= kNear + 33 && K <= 1024 + kNear;
-  g.TBlk = blk ? 1 : 0;
-  int tails = forced > 1 ? forced - 1 : (blk ? (C + 7) / 8 : (int)(((long long)K * C + 3499) / 3500));
-  const int maxt = C < 15 ? C : 15;
-  if (tails > maxt) tails = maxt;
-  if (tails < 1) tails = 1;
-  if (!forced)
-    while (tails > 1 && (long long)B * ndirs * (1 + tails) > num_sms()) --tails;
-  for (;; ++tails) {
-    if (tails > maxt) return SCRF_ECONFIG;
-    g.G = 1 + tails;
-    g.CgMax = (C + tails - 1) / tails;
-    g.WPL = 1;
-    if (g.TBlk) {
-      if (g.CgMax > 16) {  // blocked tails need one warp per label
-        g.TBlk = 0;
-        g.KTm = pow2_ceil(K) - 1;
-      } else {
-        g.KTm = 63;
+  // blocked tails (one warp per label, <= 16 labels per tail) when the duration range allows;
+  // clusters of >= 12 CTAs hang with the blocked tails on this part (root cause open), so
+  // at most 8 tails (8 x 16 labels covers C <= 128)
+  bool blk = env_int("SCRF_TAIL_EXACT", 0) == 0 && K >= kNear + 33 && K <= 1024 + kNear;
+  const int maxt = C < 8 ? C : 8;
+  auto start_tails = [&](bool blocked) {
+    int t = forced > 1 ? forced - 1 : (blocked ? (C + 7) / 8 : (int)(((long long)K * C + 3499) / 3500));
+    if (t > maxt) t = maxt;
+    if (t < 1) t = 1;
+    if (!forced)
+      while (t > 1 && (long long)B * ndirs * (1 + t) > num_sms()) --t;
+    return t;
+  };
+  bool found = false;
+  for (int pass = 0; pass < 2 && !found; ++pass) {
+    // pass 0: blocked tails if eligible; pass 1: exact per-term tails
+    if (pass == 1) {
+      if (!blk) break;
+      blk = false;
+    }
+    for (int tails = start_tails(blk); tails <= maxt; ++tails) {
+      g.G = 1 + tails;
+      g.CgMax = (C + tails - 1) / tails;
+      g.WPL = 1;
+      g.TBlk = (blk && g.CgMax <= 16) ? 1 : 0;
+      g.KTm = g.TBlk ? 63 : pow2_ceil(K) - 1;
+      if (!g.TBlk)
+        while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
+      g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
+      const int head_nt = (2 * g.NCW + g.NNW) * 32;
+      g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
+      size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
+      if (sm <= limit) {
+        found = true;
+        break;
       }
     }
-    if (!g.TBlk)
-      while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
-    g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
-    const int head_nt = (2 * g.NCW + g.NNW) * 32;
-    g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
-    size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
-    if (sm <= limit) break;
   }
+  if (!found) return SCRF_ECONFIG;
   *out = g;
   return SCRF_OK;
 }
@@ -292,7 +304,8 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
               int32_t* dead_at, cudaStream_t st) {
   const int nd = dirs == 3 ? 2 : 1;
   SweepGeo g;
-  int rc = choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, nd, &g);
+  int rc = choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, nd, p->proj_start != nullptr,
+                            p->proj_end != nullptr, &g);
   if (rc) return rc;
   SweepArgs<R> a;
   memset(&a, 0, sizeof(a));
@@ -327,6 +340,14 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   a.delta = (int)delta;
   a.n_ckpt = (int)n_ckpt_of(p->T, delta);
   a.trace = g_trace;
+  a.trace_from = env_int("SCRF_TRACE_FROM", 64);
+  if (env_int("SCRF_WATCHDOG", 0)) {
+    if (!g_hang) {
+      cudaMallocManaged(&g_hang, 8 * sizeof(int));
+      memset(g_hang, 0, 8 * sizeof(int));
+    }
+    a.hang = g_hang;
+  }
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
   if (tails && cw1) return (int)launch_cl(sweep_kernel<R, true, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
@@ -623,6 +644,12 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
 }
 
 int scrf_last_launch_count(void) { return g_launches; }
+
+int scrf_debug_hang(int* out5) {
+  if (!g_hang) return 0;
+  for (int i = 0; i < 5; ++i) out5[i] = g_hang[i];
+  return g_hang[0];
+}
 
 void scrf_debug_trace(void* buf) { g_trace = (long long*)buf; }
 

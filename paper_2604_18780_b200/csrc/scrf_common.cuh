@@ -147,14 +147,27 @@ __device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity);
+
+// Spin in C++ around try_wait (acquire at cluster scope: the data arrives through
+// st.async from peer CTAs). A spin loop written inside one asm block deadlocked for
+// clusters of >= 12 CTAs on B200; this form does not.
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  while (!mbar_try(a, parity)) {
+  }
+}
+
+// bounded wait (debug builds of the sweep): returns false after ~2^spin polls
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "SCRF_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra SCRF_WAIT_%=;\n}" ::"r"(a),
-      "r"(parity)
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
       : "memory");
+  return ok != 0;
 }
 
 __device__ __forceinline__ void st_async(uint32_t dst, float v, uint32_t bar) {

@@ -34,8 +34,9 @@
 namespace scrf {
 
 constexpr int kSlots = 16;      // head <-> tail mbarrier ring depth (power of two, > kNear)
-constexpr int kNear = 10;       // durations handled by the head when the cluster has tails
+constexpr int kNear = 16;       // durations handled by the head when the cluster has tails
 constexpr int kStage = 16;      // staged positions (power of two)
+constexpr int kNring = 64;      // chain normaliser ring n_p (power of two, > kNear + 8)
 constexpr int kAhead = 12;      // staging distance (positions)
 constexpr float kSlack = 60.f;  // shared-reference LSE slack (log2 units)
 
@@ -107,6 +108,8 @@ struct SweepGeo {
   int NWt;    // tail warps
   int WPL;    // tail warps per label (each pushes its own partial)
   int TBlk;   // 1: blocked tails (exp-space source blocks, FMA); 0: exact per-term tails
+  int PsRow;  // staged row holding Ps[t] (0 = no proj_start)
+  int PeRow;  // staged row holding Pe[t-1] (0 = no proj_end)
   int CgMax;  // max labels per tail
   int NT;     // block size (max over roles)
   int Msm;    // exp-space transition matrix staged in shared memory
@@ -133,7 +136,29 @@ struct SweepArgs {
   double* N;         // [B][n_ckpt] reference checkpoint normalisers
   int delta, n_ckpt;
   long long* trace;  // debug: [256][16] clock64 stamps of cluster 0 (chain lane 0: 0..7, near thread 0: 8..15)
+  int trace_from;    // first traced position
+  int* hang;         // debug: watchdog record {block, thread, site, index} (first writer wins), or null
 };
+
+// mbarrier wait with an optional watchdog (a.hang != null): after ~1e8 polls record where
+// and trap instead of hanging the device.
+template <typename A>
+__device__ __forceinline__ void sweep_wait(const A& a, uint32_t bar, uint32_t parity, int site, int idx) {
+  if (!a.hang) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  for (long long i = 0; i < 100000000LL; ++i)
+    if (mbar_try(bar, parity)) return;
+  if (atomicCAS(a.hang, 0, 1) == 0) {
+    a.hang[1] = blockIdx.x;
+    a.hang[2] = threadIdx.x;
+    a.hang[3] = site;
+    a.hang[4] = idx;
+    __threadfence_system();
+  }
+  __trap();
+}
 
 // per-label row strides padded to an odd number of elements (conflict-free across labels)
 __host__ __device__ inline int ring_stride(int mask) { return mask + 2; }
@@ -151,8 +176,23 @@ struct TailLayout {
 // blocked tails: exp-space source blocks of 32 held in registers (one block per lane)
 constexpr int kBlk = 32;
 __host__ __device__ inline int blk_wlen(int kc) { return (1024 + 64 + kc + 1) & ~1; }
+// w is stored in rows of 32 elements with a row stride of 34: lanes read windows that start
+// 32*j elements apart, which the skew spreads over all banks (pairs never straddle a row)
+__host__ __device__ inline int blk_wrow() { return 34; }
+__host__ __device__ inline int blk_wphys(int e) { return (e >> 5) * 34 + (e & 31); }
+__host__ __device__ inline int blk_wsize(int kc) { return (blk_wlen(kc) / 32 + 2) * 34; }
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// tail staging slots per position: one per (warp, label the warp handles) for the exact
+// tails (warps sharing a label run at different paces), one per label for the blocked tails
+__host__ __device__ inline int tail_lpw(const SweepGeo& g) {
+  const int lstep = g.NWt / (g.WPL > 0 ? g.WPL : 1);
+  return lstep > 0 ? (g.CgMax + lstep - 1) / lstep : 1;
+}
+__host__ __device__ inline int tail_stage_slots(const SweepGeo& g) {
+  return g.TBlk ? g.CgMax : g.NWt * tail_lpw(g);
+}
 
 template <typename R>
 __host__ __device__ inline HeadLayout head_layout(int K, int C, const SweepGeo& g) {
@@ -163,13 +203,13 @@ __host__ __device__ inline HeadLayout head_layout(int K, int C, const SweepGeo& 
   L.Xmax = o;  o += a16((size_t)C * sizeof(R));
   L.B2 = o;    o += a16((size_t)C * b2_stride(g.kc) * sizeof(R));
   L.ring = o;  o += a16((size_t)2 * C * ring_stride(g.KRm) * 2 * sizeof(R));  // one ring per near group
-  L.stg = o;   o += a16((size_t)kStage * 3 * C * sizeof(double));
+  L.stg = o;   o += a16((size_t)kStage * (1 + (g.PsRow > 0) + (g.PeRow > 0)) * C * sizeof(double));
   L.oq = o;    o += a16((size_t)kStage * C * 2 * sizeof(double));
   L.own = o;   o += a16((size_t)C * sizeof(int2));
   L.pubY = o;  o += a16((size_t)8 * C * sizeof(R));
   L.pubX = o;  o += a16((size_t)8 * C * sizeof(R));
   L.pubA = o;  o += a16(8 * sizeof(R));
-  L.nring = o; o += a16(kSlots * sizeof(double));
+  L.nring = o; o += a16(kNring * sizeof(double));
   L.part = o;  o += a16((size_t)4 * C * 2 * sizeof(R));
   L.hh = o;    o += a16((size_t)8 * C * 2 * sizeof(R));
   L.h3 = o;    o += a16((size_t)8 * C * sizeof(R));
@@ -189,8 +229,8 @@ __host__ __device__ inline TailLayout tail_layout(int K, int C, const SweepGeo& 
   L.B2 = o;    o += g.TBlk ? 0 : a16((size_t)g.CgMax * K * sizeof(R));
   L.nslot = o; o += a16(kSlots * sizeof(double));
   L.tbar = o;  o += a16(kSlots * sizeof(uint64_t));
-  L.stg = o;   o += a16((size_t)kStage * 2 * g.CgMax * sizeof(double));
-  L.wtab = o;  o += g.TBlk ? a16((size_t)g.CgMax * 2 * blk_wlen(g.kc) * sizeof(R)) : 0;
+  L.stg = o;   o += a16((size_t)kStage * 2 * tail_stage_slots(g) * sizeof(double));
+  L.wtab = o;  o += g.TBlk ? a16((size_t)g.CgMax * 2 * blk_wsize(g.kc) * sizeof(R)) : 0;
   L.bx = o;    o += g.TBlk ? a16((size_t)g.CgMax * (kBlk + 1) * sizeof(R)) : 0;
   L.total = o;
   return L;
@@ -406,29 +446,41 @@ __device__ HeadPtr<R> head_ptrs(unsigned char* base, const HeadLayout& L) {
   return h;
 }
 
+// staged rows per position: S[t], then Ps[t] and Pe[t-1] when present
+__host__ __device__ inline int stg_rows(const SweepGeo& g) { return 1 + (g.PsRow > 0) + (g.PeRow > 0); }
+
 // fp64 (O, Q) of label c at sweep position p from the raw staged rows (log2 units)
-__device__ __forceinline__ double2 oq_of(const SweepCtx& x, int C, const double* stg, int p, int c) {
-  const double* d = stg + (size_t)(p & (kStage - 1)) * 3 * C;
-  const double s = d[c] * kLog2e, psv = d[C + c] * kLog2e, pev = d[2 * C + c] * kLog2e;
+__device__ __forceinline__ double2 oq_of(const SweepCtx& x, const SweepGeo& g, int C, const double* stg, int p, int c) {
+  const double* d = stg + (size_t)(p & (kStage - 1)) * stg_rows(g) * C;
+  const double s = d[c] * kLog2e;
+  const double psv = g.PsRow ? d[g.PsRow * C + c] * kLog2e : 0.0;
+  const double pev = g.PeRow ? d[g.PeRow * C + c] * kLog2e : 0.0;
   return x.dir == 0 ? make_double2(s + pev, -s + psv) : make_double2(-s + psv, s + pev);
 }
 
 // raw rows S[t], Ps[t], Pe[t-1] of label c at sweep position p into its staging slot
 template <bool ASYNC>
-__device__ __forceinline__ void stage_label(const SweepCtx& x, int T, int C, double* stg, int p, int c) {
+__device__ __forceinline__ void stage_label(const SweepCtx& x, const SweepGeo& g, int T, int C, double* stg, int p,
+                                            int c) {
   const int t = x.tpos(p);
-  double* d = stg + (size_t)(p & (kStage - 1)) * 3 * C + c;
+  double* d = stg + (size_t)(p & (kStage - 1)) * stg_rows(g) * C + c;
   const double* s0 = x.S + (size_t)t * C + c;
   if (ASYNC) cp_async8(d, s0); else d[0] = __ldg(s0);
-  if (x.ps && t < T) {
-    if (ASYNC) cp_async8(d + C, x.ps + (size_t)t * C + c); else d[C] = __ldg(x.ps + (size_t)t * C + c);
-  } else {
-    d[C] = 0.0;
+  if (g.PsRow) {
+    double* dd = d + g.PsRow * C;
+    if (t < T) {
+      if (ASYNC) cp_async8(dd, x.ps + (size_t)t * C + c); else *dd = __ldg(x.ps + (size_t)t * C + c);
+    } else {
+      *dd = 0.0;
+    }
   }
-  if (x.pe && t >= 1) {
-    if (ASYNC) cp_async8(d + 2 * C, x.pe + (size_t)(t - 1) * C + c); else d[2 * C] = __ldg(x.pe + (size_t)(t - 1) * C + c);
-  } else {
-    d[2 * C] = 0.0;
+  if (g.PeRow) {
+    double* dd = d + g.PeRow * C;
+    if (t >= 1) {
+      if (ASYNC) cp_async8(dd, x.pe + (size_t)(t - 1) * C + c); else *dd = __ldg(x.pe + (size_t)(t - 1) * C + c);
+    } else {
+      *dd = 0.0;
+    }
   }
 }
 
@@ -584,7 +636,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   const R2* hhc = h.hh + cs;
   const R* h3c = h.h3 + cs;
   for (int p = 1; p <= L; ++p) {
-    long long* tr = (a.trace && blockIdx.x == 0 && tid == 0 && p >= 64 && p < 64 + 256) ? a.trace + (p - 64) * 16 : nullptr;
+    long long* tr = (a.trace && blockIdx.x == 0 && tid == 0 && p >= a.trace_from && p < a.trace_from + 256) ? a.trace + (p - a.trace_from) * 16 : nullptr;
     if (tr) tr[0] = clock64();
     nbar_sync(BAR_B + (p & 3), NB);
     R y = Mth<R>::ninf();
@@ -608,7 +660,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     }
     if (tid == 0) {
       h.pubA[p & 7] = am;
-      h.nring[p & (kSlots - 1)] = n_p;
+      h.nring[p & (kNring - 1)] = n_p;
     }
     nbar_arrive(BAR_A + (p & 3), NA);
     if (tr) tr[3] = clock64();
@@ -666,13 +718,13 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   auto source = [&](int q) -> R2 {  // r[q] = n_q + X^[q] + Q[q] as an fp32 (hi, lo) pair
     const R X = pubXc[(q & 7) * C];
     const double r = (X == Mth<R>::ninf()) ? -CUDART_INF
-                                            : h.nring[q & (kSlots - 1)] + ((double)X + oqc[(size_t)(q & (kStage - 1)) * C].y);
+                                            : h.nring[q & (kNring - 1)] + ((double)X + oqc[(size_t)(q & (kStage - 1)) * C].y);
     R2 v;
     split2(r, v.x, v.y);
     return v;
   };
   for (int p = gi == 0 ? 2 : 1; p <= L + 4; p += 2) {
-    long long* tr = (a.trace && blockIdx.x == 0 && ntid == 0 && p >= 64 && p < 64 + 256) ? a.trace + (p - 64) * 16 + 8 : nullptr;
+    long long* tr = (a.trace && blockIdx.x == 0 && ntid == 0 && p >= a.trace_from && p < a.trace_from + 256) ? a.trace + (p - a.trace_from) * 16 + 8 : nullptr;
     if (tr) tr[0] = clock64();
     if (p >= 4) nbar_sync(BAR_A + ((p - 4) & 3), NA);
     if (tr) tr[1] = clock64();
@@ -682,7 +734,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     R m = Mth<R>::ninf(), s = 0;
     double n_q = 0.0;
     if (q >= 0) {
-      n_q = h.nring[q & (kSlots - 1)];
+      n_q = h.nring[q & (kNring - 1)];
       R2 r4;
       r4.x = Mth<R>::ninf();
       r4.y = 0;
@@ -714,10 +766,10 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       const int pi = p - kc - 1;
       const int sl = pi & (kSlots - 1);
       if (tr) tr[5] = clock64();
-      mbar_wait(smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1));
+      sweep_wait(a, smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1), 1, p);
       if (tr) tr[6] = clock64();
       if (act && j == 0) {
-        const double d = n_q - h.nring[pi & (kSlots - 1)];  // tail frame n_{p-kc-1} -> n_{p-4}
+        const double d = n_q - h.nring[pi & (kNring - 1)];  // tail frame n_{p-kc-1} -> n_{p-4}
         R d_hi, d_lo;
         split2(d, d_hi, d_lo);
         const R2* tp = tpartc + (size_t)sl * g.WPL * C;
@@ -760,13 +812,13 @@ __device__ void head_aux(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h
   for (int q = 0; q <= L; ++q, t += tstep) {
     cp_async_wait<6>();  // own rows of position q+5 (issued at iteration q-7)
     nbar_sync(BAR_A + (q & 3), NA);
-    const double n_q = h.nring[q & (kSlots - 1)];
+    const double n_q = h.nring[q & (kNring - 1)];
     if (act) {
       Yo[(size_t)t * C] = pYc[(q & 7) * C];
       Xo[(size_t)t * C] = pXc[(q & 7) * C];
-      if (q + 5 <= L) h.oq[(size_t)((q + 5) & (kStage - 1)) * C + c] = oq_of(x, C, h.stg, q + 5, c);
+      if (q + 5 <= L) h.oq[(size_t)((q + 5) & (kStage - 1)) * C + c] = oq_of(x, g, C, h.stg, q + 5, c);
       if (q + 4 <= L) head_edge<R>(C, K, h.oq, h.B2, g.kc, q + 4, c, h.hh, h.h3);
-      if (q + kAhead <= L) stage_label<true>(x, T, C, h.stg, q + kAhead, c);
+      if (q + kAhead <= L) stage_label<true>(x, g, T, C, h.stg, q + kAhead, c);
     }
     cp_async_commit();
     if (c == 0) no[t] = n_q;
@@ -845,7 +897,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     if (TAILS && tid < kSlots) mbar_init(smem_u32(&h.tbar[tid]), 1);
     for (int i = tid; i < kAhead * C; i += NH) {
       const int q = i / C, cc = i % C;
-      if (q <= L) stage_label<false>(x, T, C, h.stg, q, cc);
+      if (q <= L) stage_label<false>(x, g, T, C, h.stg, q, cc);
     }
   }
   __syncthreads();
@@ -858,7 +910,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       }
     for (int i = tid; i < 5 * C; i += NH) {  // (O, Q) of positions 0..4
       const int q = i / C, cc = i % C;
-      if (q <= L) h.oq[(size_t)q * C + cc] = oq_of(x, C, h.stg, q, cc);
+      if (q <= L) h.oq[(size_t)q * C + cc] = oq_of(x, g, C, h.stg, q, cc);
     }
     for (int cc = tid; cc < C; cc += NH) {  // tail owning label cc and its index there
       int rt = 0, cl = 0;
@@ -908,9 +960,12 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
   double* stg = (double*)(smem + TL.stg);
   // own rows of target u (S[t] and Pe[t-1] (alpha) / Ps[t] (beta)) for label cl
+  // each warp stages its own copy (warps sharing a label run at different paces)
+  const int NWs = tail_stage_slots(g), LPW = tail_lpw(g);
+  const int WPL_ = g.WPL, lstep_ = g.NWt / WPL_, cl0_ = warp / WPL_;
   auto stage = [&](int u, int cl) {
     const int t = x.tpos(u), c = lo + cl;
-    double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
+    double* d = stg + ((size_t)(u & (kStage - 1)) * NWs + warp * LPW + (cl - cl0_) / lstep_) * 2;
     cp_async8(d, x.S + (size_t)t * C + c);
     if (x.dir == 0 && x.pe && t >= 1)
       cp_async8(d + 1, x.pe + (size_t)(t - 1) * C + c);
@@ -934,12 +989,12 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   int sn = 0;  // ring slot of the newest source s_new = u - kc - 1
   for (int u = u0; u <= L; ++u) {
     const int s_new = u - kc - 1;
-    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= 64 && u < 64 + 256) ? a.trace + 256 * 16 + (u - 64) * 16 : nullptr;
+    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= a.trace_from && u < a.trace_from + 256) ? a.trace + 256 * 16 + (u - a.trace_from) * 16 : nullptr;
     if (tr) tr[0] = clock64();
     cp_async_wait<kAhead - 1>();
     __syncwarp();
     if (tr) tr[1] = clock64();
-    mbar_wait(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1));
+    sweep_wait(a, smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1), 2, u);
     if (tr) tr[2] = clock64();
     if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
       mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
@@ -948,7 +1003,7 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     for (int cl = cl0; cl < Cg; cl += lstep) {
       const R2* rg = ring + (size_t)cl * (KTm + 1);
       const R* b2 = B2 + (size_t)cl * K;
-      const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
+      const double* d = stg + ((size_t)(u & (kStage - 1)) * NWs + warp * LPW + (cl - cl0) / lstep) * 2;
       const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
       const double O = x.dir == 0 ? s2 + o2 : -s2 + o2;
       R e_hi, e_lo;
@@ -973,28 +1028,28 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
 }
 
 
-// Blocked tail (TBlk): for target u the durations kc+1..K are the sources
-// s in [u-K, u-kc-1]. Sources are grouped in blocks of 32 (block j = [32j, 32j+31]).
-// When block j completes, its values become z[i] = 2^(r[32j+i] - G_j) (G_j = block max)
-// held in 32 registers of lane j % 32, and the block's contribution to target u is
-//   2^(G_j + e[u] + Bmax) * sum_i z[i] * w[u - 32j - i],   w[k] = 2^(B[k-1] - Bmax) (0 outside kc+1..K)
-// a 32-term FMA dot product against a sliding window of w (two shifted copies in SMEM
-// so every window is an aligned 8-byte load). The newest, incomplete block is summed
-// term by term. Requires kc + 32 <= K and K <= 1024 + kc (one block per lane).
+// Blocked tail (TBlk). For target u the tail's durations kc+1..K are the sources
+// s in [u-K, u-kc-1]. Sources form blocks of 32 (block j = [32j, 32j+31]); a complete
+// block is kept as z[i] = 2^(r[32j+i] - G_j) (G_j = its largest source) in the registers of
+// lane j % 32, and contributes 2^(G_j + e[u] + Bmax) * sum_i z[i] * w[u - 32j - i] to target
+// u, with w[k] = 2^(B[k-1] - Bmax) (0 outside kc+1..K). Targets are processed in groups of
+// four (one window load of 35 w values feeds 4 x 32 FMAs); the newest, incomplete block is
+// summed term by term. Each target's partial is in the frame n_{u-kc-1} of its newest
+// source. Needs kc + 32 <= K <= 1024 + kc.
 template <typename R>
 __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                                   const TailLayout& TL, int lo, int Cg) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
-  const int K = a.K, C = a.C, T = a.T, L = x.L, kc = g.kc, KTm = g.KTm;
+  const int C = a.C, T = a.T, L = x.L, kc = g.kc, KTm = g.KTm, K = a.K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = warp;  // one label per warp
   const R2* rg = (const R2*)(smem + TL.ring) + (size_t)cl * (KTm + 1);
   const double* nslot = (const double*)(smem + TL.nslot);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
   double* stg = (double*)(smem + TL.stg);
-  const int WLEN = blk_wlen(kc);
-  const R* wt = (const R*)(smem + TL.wtab) + (size_t)cl * 2 * WLEN;
+  const int WSZ = blk_wsize(kc);
+  const R* wt = (const R*)(smem + TL.wtab) + (size_t)cl * 2 * WSZ;
   const R* bx = (const R*)(smem + TL.bx) + (size_t)cl * (kBlk + 1);
   const R bmax = bx[kBlk];
   auto stage = [&](int u) {
@@ -1009,8 +1064,11 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
       d[1] = 0.0;
   };
   const int u0 = kc + 1;
-  for (int i = 0; i < kAhead; ++i) {
-    if (lane == 0 && u0 + i <= L) stage(u0 + i);
+  // staging runs 3 groups (12 targets) ahead; one commit group per 4 targets
+  for (int gq = 0; gq < 3; ++gq) {
+    if (lane == 0)
+      for (int i = 0; i < 4; ++i)
+        if (u0 + 4 * gq + i <= L) stage(u0 + 4 * gq + i);
     cp_async_commit();
   }
   const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
@@ -1020,28 +1078,120 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   for (int i = 0; i < kBlk; ++i) zr[i] = 0;
   R Gh = Mth<R>::ninf(), Gl = 0;
   int jown = -1;
-  for (int u = u0; u <= L; ++u) {
-    const int s_new = u - kc - 1;
-    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= 64 && u < 64 + 256) ? a.trace + 256 * 16 + (u - 64) * 16 : nullptr;
+  for (int ub = u0; ub <= L; ub += 4) {
+    const int sb = ub - kc - 1;          // newest source of target ub (multiple of 4)
+    const int nt = min(4, L - ub + 1);   // targets in this group
+    long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && ub >= a.trace_from && ub < a.trace_from + 4 * 256)
+                        ? a.trace + 256 * 16 + ((ub - a.trace_from) / 4) * 16
+                        : nullptr;
     if (tr) tr[0] = clock64();
-    cp_async_wait<kAhead - 1>();
+    cp_async_wait<2>();
     __syncwarp();
-    if (tr) tr[1] = clock64();
-    mbar_wait(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1));
-    if (tr) tr[2] = clock64();
-    if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
-      mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
-    const double F = nslot[s_new & (kSlots - 1)];
-    R e_hi, e_lo;
-    {
-      const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
-      const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
-      split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - F, e_hi, e_lo);
+    // the group's sources sb .. sb+nt-1 (and their normalisers)
+    for (int i = 0; i < nt; ++i) {
+      const int s = sb + i;
+      sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
     }
-    const int inb = s_new & (kBlk - 1);
-    if (inb == kBlk - 1) {
-      // block jb = s_new / 32 completes: frame = its largest source, z into the owner lane
-      const int jb = s_new >> 5;
+    if (tr) tr[1] = clock64();
+    R eh[4], el[4];
+    double Fi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      eh[i] = 0;
+      el[i] = 0;
+      Fi[i] = 0.0;
+      if (i < nt) {
+        const int u = ub + i;
+        Fi[i] = nslot[(sb + i) & (kSlots - 1)];
+        const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
+        const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
+        split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - Fi[i], eh[i], el[i]);
+      }
+    }
+    __syncwarp();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < nt; ++i) {
+        const int s = sb + i;
+        if (s + kSlots <= L - kc - 1)
+          mbar_expect(smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
+      }
+    // newest incomplete block: sources [base, sb+i] for target i, term by term
+    const int base = sb & ~(kBlk - 1);
+    R xe[4];
+    {
+      const int s = base + lane;
+      const R2 r = rg[s & KTm];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xe[i] = Mth<R>::ninf();
+        if (i < nt && s <= sb + i) xe[i] = (r.x + eh[i]) + (r.y + el[i]) + bx[ub + i - s - kc - 1];
+      }
+    }
+    // complete block owned by this lane: 4 x 32 FMAs against one window of w
+    R pb[4] = {0, 0, 0, 0};
+    bool have = false;
+    int d0 = 0;
+    if (jown >= 0 && Gh != Mth<R>::ninf()) {
+      d0 = ub - jown * kBlk;     // duration of the block's source 0 for target ub
+      const int wb = d0 - (kBlk - 1);  // window start: durations wb .. wb+34
+      if (wb <= K) {
+        have = true;
+        const int m = wb & 1;
+        const R* wc = wt + (size_t)m * WSZ;  // copy m holds w[y - m] at y (skewed rows)
+        const int e0 = wb + m;               // even
+        const int r0 = e0 >> 5, c0 = e0 & 31;
+        R wv[kBlk + 4];
+#pragma unroll
+        for (int t2 = 0; t2 < (kBlk + 4) / 2; ++t2) {
+          const int cc = c0 + 2 * t2;  // column within row r0 (may run into rows r0+1, r0+2)
+          const int ph = r0 * 34 + cc + (cc >= 32 ? 2 : 0) + (cc >= 64 ? 2 : 0);
+          const auto w2 = *(const typename Vec2<R>::T*)(wc + ph);
+          wv[2 * t2] = w2.x;
+          wv[2 * t2 + 1] = w2.y;
+        }
+        // target i, source j: duration d0 + i - j = wb + (31 - j) + i  ->  wv[31 - j + i]
+#pragma unroll
+        for (int jj = 0; jj < kBlk; ++jj) {
+          const R z = zr[jj];
+          pb[0] += z * wv[31 - jj];
+          pb[1] += z * wv[32 - jj];
+          pb[2] += z * wv[33 - jj];
+          pb[3] += z * wv[34 - jj];
+        }
+      }
+    }
+    if (tr) tr[2] = clock64();
+    R Mv[4], Sv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const R xb = (have && pb[i] > (R)0) ? ((Gh + eh[i]) + (Gl + el[i])) + bmax : Mth<R>::ninf();
+      const R M = warp_max(fmax(xb, xe[i]));
+      R sm = 0;
+      if (M != Mth<R>::ninf()) {
+        if (xb != Mth<R>::ninf()) sm += pb[i] * Mth<R>::ex2(xb - M);
+        if (xe[i] != Mth<R>::ninf()) sm += Mth<R>::ex2(xe[i] - M);
+      }
+      Mv[i] = M;
+      Sv[i] = sm;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Sv[i] += __shfl_xor_sync(0xffffffffu, Sv[i], off);
+    }
+    if (lane == 0) {
+      for (int i = 0; i < nt; ++i) {
+        const int sl = (sb + i) & (kSlots - 1);
+        const uint32_t off = (uint32_t)(((size_t)sl * C + lo + cl) * 2 * sizeof(R));
+        st_async_pair<R>(hpart + off, Mv[i], Sv[i], hbar + (uint32_t)(sl * sizeof(uint64_t)));
+      }
+      for (int i = 0; i < 4; ++i)
+        if (ub + 12 + i <= L) stage(ub + 12 + i);
+    }
+    cp_async_commit();
+    // block (sb+3)/32 completes after this group: frame = its largest source, z to its owner lane
+    if (nt == 4 && ((sb + 3) & (kBlk - 1)) == kBlk - 1) {
+      const int jb = (sb + 3) >> 5;
       const R2 r = rg[(jb * kBlk + lane) & KTm];
       const R gh = warp_max(r.x);
       const unsigned bal = __ballot_sync(0xffffffffu, r.x == gh);
@@ -1059,50 +1209,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
         jown = jb;
       }
     }
-    // contribution of the lane's complete block
-    R xb = Mth<R>::ninf(), pb = 0;
-    if (jown >= 0 && Gh != Mth<R>::ninf()) {
-      const int dd = u - jown * kBlk;  // duration of the block's source 0
-      const int base = dd - (kBlk - 1);
-      if (base <= K) {
-        const int m = base & 1;
-        const typename Vec2<R>::T* wp = (const typename Vec2<R>::T*)(wt + (size_t)m * WLEN + base + m);
-        R p0 = 0, p1 = 0, p2 = 0, p3 = 0;
-#pragma unroll
-        for (int i2 = 0; i2 < kBlk / 2; i2 += 2) {
-          const auto w01 = wp[i2];      // w[base + 2*i2], w[base + 2*i2 + 1]
-          const auto w23 = wp[i2 + 1];  // w[base + 2*i2 + 2], w[base + 2*i2 + 3]
-          // source i has duration dd - i = base + (31 - i)
-          p0 += zr[31 - 2 * i2] * w01.x;
-          p1 += zr[30 - 2 * i2] * w01.y;
-          p2 += zr[29 - 2 * i2] * w23.x;
-          p3 += zr[28 - 2 * i2] * w23.y;
-        }
-        pb = (p0 + p1) + (p2 + p3);
-        if (pb > (R)0) xb = (Gh + e_hi) + (Gl + e_lo) + bmax;
-      }
-    }
-    // the newest incomplete block, term by term (durations kc+1 .. kc+32)
-    R xe = Mth<R>::ninf();
-    if (inb != kBlk - 1 && lane <= inb) {
-      const int sidx = s_new - inb + lane;
-      const R2 r = rg[sidx & KTm];
-      xe = (r.x + e_hi) + (r.y + e_lo) + bx[u - sidx - kc - 1];
-    }
     if (tr) tr[3] = clock64();
-    const R M = warp_max(fmax(xb, xe));
-    R sum = 0;
-    if (M != Mth<R>::ninf()) {
-      if (xb != Mth<R>::ninf()) sum += pb * Mth<R>::ex2(xb - M);
-      if (xe != Mth<R>::ninf()) sum += Mth<R>::ex2(xe - M);
-    }
-    sum = gsum(sum, 32);
-    if (lane == 0) {
-      const uint32_t off = (uint32_t)(((size_t)(s_new & (kSlots - 1)) * C + lo + cl) * 2 * sizeof(R));
-      st_async_pair<R>(hpart + off, M, sum, hbar + (uint32_t)((s_new & (kSlots - 1)) * sizeof(uint64_t)));
-      if (u + kAhead <= L) stage(u + kAhead);
-    }
-    cp_async_commit();
   }
   cp_async_wait<0>();
 }
@@ -1130,6 +1237,7 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       }
     }
     __syncthreads();
+    const int WSZ = blk_wsize(g.kc);
     for (int i = tid; i < Cg * 2 * WLEN; i += blockDim.x) {
       const int cl = i / (2 * WLEN), r = i % (2 * WLEN), m = r / WLEN, y = r % WLEN;
       const int k = y - m;  // copy m holds w[y - m]
@@ -1138,7 +1246,7 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
         const R bm = bx[(size_t)cl * (kBlk + 1) + kBlk];
         v = Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + lo + cl] * kLog2e) - bm);
       }
-      wt[i] = v;
+      wt[((size_t)cl * 2 + m) * WSZ + blk_wphys(y)] = v;
     }
   } else {
     for (int i = tid; i < Cg * K; i += blockDim.x) {

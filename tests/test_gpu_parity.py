@@ -161,3 +161,46 @@ class TestKnownAnswers:
         _, g1, m1 = scrf.posterior(cum, params, upstream=up)
         np.testing.assert_allclose(g1.grad_S, g0.grad_S * up[:, None, None], atol=1e-12)
         np.testing.assert_array_equal(m1.position_marginals, m0.position_marginals)
+
+
+# ---------------------------------------------------------------------------
+# north-star size (config 4, B=8 T=100000 K=1000 C=24): size-independent properties
+
+
+@pytest.mark.parametrize("mode", [CenteringMode.MEAN])
+def test_config4_full_size_invariants(mode):
+    S.set_precision("fp32")
+    _, params, cum = scrf.equivalence_instance(0, T=100_000, K=1000, C=24, B=8, mode=mode)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    fwd, bw = S.device_posterior(prob)
+    logZ = fwd.logZ.cpu().numpy()
+    zb = S.device_beta_logz(prob, fwd, bw).cpu().numpy()
+    # the two independent sweeps agree on log Z (virtual source: LSE_c beta[0, c])
+    np.testing.assert_allclose(zb, logZ, rtol=1e-6)
+    pos = bw.position_marginals.cpu().numpy()
+    # every position is covered by exactly one segment
+    np.testing.assert_allclose(pos.sum(-1), 1.0, atol=1e-4)
+    gS = bw.grad_S.cpu().numpy()
+    # sum over positions and labels of grad_S is zero per sequence (end mass = start mass)
+    assert np.abs(gS.sum(axis=(1, 2))).max() < 1e-2
+    cnt = bw.expected_segment_count.cpu().numpy()
+    # duration and transition gradients both total the expected number of segments
+    # (the first segment's transition comes from the virtual source)
+    np.testing.assert_allclose(bw.grad_B.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
+    np.testing.assert_allclose(bw.grad_T.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
+    bnd = bw.boundary_posterior.cpu().numpy()
+    np.testing.assert_allclose(bnd[:, 0], 1.0, atol=1e-5)
+    assert np.all(np.isfinite(logZ)) and np.all(fwd.dead_at.cpu().numpy() < 0)
+
+
+def test_alpha_beta_logz_agree_on_goldens():
+    S.set_precision("fp32")
+    for name in ["c1rp", "c2", "c3s", "c4s", "c5s"]:
+        case = golden_io.equiv_case(name)
+        if case is None:
+            continue
+        params, cum, delta, exp = case
+        prob = scrf.DeviceProblem.from_host(cum, params)
+        fwd, bw = S.device_posterior(prob, delta)
+        zb = S.device_beta_logz(prob, fwd, bw).cpu().numpy()
+        np.testing.assert_allclose(zb, exp["logZ"], rtol=1e-6)

@@ -40,8 +40,8 @@ for i, n in enumerate(names):
 print("near start - chain start (median):", np.median(nr[:, 0] - ch[:, 0]))
 
 if tl[:, 0].any():
-    print("tail warp0 (median cycles): step", np.median(np.diff(tl[:, 0])))
-    for i, n in enumerate(["cp.wait", "src wait", "lse"]):
+    print("tail warp0 (median cycles): step/group", np.median(np.diff(tl[:, 0])))
+    for i, n in enumerate(["src wait", "fma", "reduce+send"]):
         print(f"  {n:14s} {np.median(tl[:, i + 1] - tl[:, i]):8.0f}")
     # near group 0 handles even p; near tr[5..6] = tail wait
     ev = nr[::2]
