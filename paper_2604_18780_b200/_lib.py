@@ -15,7 +15,7 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libscrf.so")
+LIB_PATH = os.environ.get("SCRF_LIB") or os.path.join(HERE, "libscrf.so")
 
 SCRF_ERRORS = {
     -1: "dimension out of range",

@@ -9,6 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libscrf.so")
+# debug build with clock64/globaltimer phase tracing compiled in (tools/trace_sweep.py)
+OUT_TRACE = os.path.join(HERE, "libscrf_trace.so")
 SOURCES = ["scrf_capi.cu"]
 DEPS = ["scrf_capi.cu", "scrf_sweep.cuh", "scrf_post.cuh", "scrf_viterbi.cu", "scrf_common.cuh",
         os.path.join("..", "..", "include", "scrf.h")]
@@ -27,19 +29,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(os.path.join(SRC, d)) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    out = OUT_TRACE if trace else OUT
+    if not force and up_to_date() and not trace:
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *[os.path.join(SRC, s) for s in SOURCES]]
+    extra = ["-DSCRF_TRACE"] if trace else []
+    cmd = [NVCC, *FLAGS, *extra, "-o", out + ".tmp", *[os.path.join(SRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libscrf.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

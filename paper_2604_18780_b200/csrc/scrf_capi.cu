@@ -125,10 +125,17 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   g.NCW = (C + 31) / 32;
   if (g.NCW > 4) return SCRF_ECONFIG;  // C <= 128 (head roles fit one 512-thread CTA)
   g.Msm = (size_t)C * C * (prec ? 8 : 4) <= 65536 ? 1 : 0;
-  const int maxg = (16 - 2 * g.NCW) / 2;  // warps per near group (two groups)
+  g.NAS = g.NCW == 1 ? 2 : 1;  // separate source and edge warps when they fit
+  g.NG = g.NCW == 1 ? 4 : 2;   // near groups (each owns every NG-th target)
+  g.PubS = g.NAS == 2 ? 16 : 8; // batched edge warps / per-step edge in the source warps
+  const int maxg = (16 - g.NCW - g.NAS * g.NCW) / g.NG;  // warps per near group
+  // near lane-group width: SIMT runs each label's fp64 bookkeeping for the whole warp, so
+  // use one lane per label unless a label has many ring terms (>= 16 per lane)
   auto near_gw = [&](int terms) {
-    int gw = pow2_ceil((terms + 3) / 4 > 0 ? (terms + 3) / 4 : 1);
-    if (gw > 32) gw = 32;
+    int gw = 1;
+    while (gw < 32 && terms / (gw * 2) >= 16) gw *= 2;
+    int env = env_int("SCRF_NEAR_GW", 0);
+    if (env > 0) gw = env;
     while (gw > 1 && (C * gw + 31) / 32 > maxg) gw >>= 1;
     return gw;
   };
@@ -142,11 +149,11 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
     g.KTm = 0;
     g.WPL = 1;
     g.TBlk = 0;
-    g.GWn = near_gw(K > 4 ? K - 4 : 1);
-    g.NNW = 2 * ((C * g.GWn + 31) / 32);
-    g.NT = (2 * g.NCW + g.NNW) * 32;
+    g.GWn = near_gw(K > 5 ? K - 5 : 1);
+    g.NNW = g.NG * ((C * g.GWn + 31) / 32);
+    g.NT = (g.NCW + g.NAS * g.NCW + g.NNW) * 32;
     size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
-    if (g.NNW <= 2 * maxg && sm <= limit) {
+    if (g.NNW <= g.NG * maxg && sm <= limit) {
       *out = g;
       return SCRF_OK;
     }
@@ -155,8 +162,8 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   g.kc = kNear;
   g.KRm = pow2_ceil(kNear) - 1;
   g.KTm = pow2_ceil(K) - 1;
-  g.GWn = near_gw(kNear - 4);
-  g.NNW = 2 * ((C * g.GWn + 31) / 32);
+  g.GWn = near_gw(kNear - 5);
+  g.NNW = g.NG * ((C * g.GWn + 31) / 32);
   // blocked tails (one warp per label, <= 16 labels per tail) when the duration range allows;
   // clusters of >= 12 CTAs hang with the blocked tails on this part (root cause open), so
   // at most 8 tails (8 x 16 labels covers C <= 128)
@@ -186,7 +193,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
       if (!g.TBlk)
         while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
       g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
-      const int head_nt = (2 * g.NCW + g.NNW) * 32;
+      const int head_nt = (g.NCW + g.NAS * g.NCW + g.NNW) * 32;
       g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
       size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
       if (sm <= limit) {
@@ -202,7 +209,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
 
 // forward state ("checkpoint buffer"): per-position alpha-side messages
 struct FLayout {
-  size_t Y, X, n, total;
+  size_t Y, X, n, amx, total;
 };
 FLayout f_layout(const scrf_problem* p, int prec) {
   FLayout L;
@@ -215,6 +222,8 @@ FLayout f_layout(const scrf_problem* p, int prec) {
   o += al(npos * p->C * rs);
   L.n = o;
   o += al(npos * 8);
+  L.amx = o;
+  o += al(npos * rs);
   L.total = o;
   return L;
 }
@@ -271,8 +280,13 @@ BLayout b_layout(const scrf_problem* p, int prec) {
   return L;
 }
 
+// Cluster launch with one CTA per SM: the recurrence CTAs are latency bound, and a second
+// resident CTA (another cluster's tail) would share their issue slots, so the dynamic shared
+// memory request is padded past half of the SM's capacity.
 template <typename Kern, typename ArgT>
 cudaError_t launch_cl(Kern kern, int G, int nclusters, int NT, size_t smem, cudaStream_t st, ArgT arg, bool record) {
+  const size_t half = (size_t)smem_optin() / 2 + 1024;
+  if (smem < half) smem = half;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (G > 8) {
@@ -326,6 +340,7 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   a.Y[0] = (R*)(fb + F.Y);
   a.X[0] = (R*)(fb + F.X);
   a.n[0] = (double*)(fb + F.n);
+  a.amx = (R*)(fb + F.amx);
   if (work) {
     const BLayout W = b_layout(p, sizeof(R) == 8);
     unsigned char* wb = (unsigned char*)work;
@@ -350,10 +365,24 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   }
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
-  if (tails && cw1) return (int)launch_cl(sweep_kernel<R, true, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
-  if (tails) return (int)launch_cl(sweep_kernel<R, true, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
-  if (cw1) return (int)launch_cl(sweep_kernel<R, false, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
-  return (int)launch_cl(sweep_kernel<R, false, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  cudaError_t e;
+  if (tails && cw1)
+    e = launch_cl(sweep_kernel<R, true, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  else if (tails)
+    e = launch_cl(sweep_kernel<R, true, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  else if (cw1)
+    e = launch_cl(sweep_kernel<R, false, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  else
+    e = launch_cl(sweep_kernel<R, false, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+  if (e != cudaSuccess) return (int)e;
+  if (dirs & 1) {
+    // reference bookkeeping (N, dead_at, logZ) from the stored per-position normalisers
+    ++g_launches;
+    book_kernel<R><<<a.B, 256, a.n_ckpt * sizeof(double), st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
+                                                               a.n_ckpt, N, dead_at, logZ);
+    e = cudaGetLastError();
+  }
+  return (int)e;
 }
 
 template <typename R>

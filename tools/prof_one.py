@@ -16,8 +16,12 @@ cfg = CONFIGS[sys.argv[1]]
 T = int(sys.argv[2])
 _, params, cum = scrf.equivalence_instance(0, T=T, K=cfg["K"], C=cfg["C"], B=cfg["B"], mode=scrf.CenteringMode.MEAN)
 prob = scrf.DeviceProblem.from_host(cum, params)
-f = S.device_forward(prob)
-if len(sys.argv) > 3:
+if len(sys.argv) > 3 and sys.argv[3] == "post":
+    S.device_posterior(prob)
+    f = None
+else:
+    f = S.device_forward(prob)
+if len(sys.argv) > 3 and sys.argv[3] == "bwd":
     S.device_backward(prob, f)
 if len(sys.argv) > 4:
     S.device_viterbi(prob)
