@@ -120,6 +120,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   const size_t limit = (size_t)smem_optin();
   SweepGeo g;
   memset(&g, 0, sizeof(g));
+  g.TWb = 1;
   g.PsRow = has_ps ? 1 : 0;
   g.PeRow = has_pe ? (has_ps ? 2 : 1) : 0;
   g.NCW = (C + 31) / 32;
@@ -189,10 +190,12 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
       g.CgMax = (C + tails - 1) / tails;
       g.WPL = 1;
       g.TBlk = (blk && g.CgMax <= 16) ? 1 : 0;
+      g.TWb = (g.TBlk && g.CgMax * 2 <= 16) ? 2 : 1;  // two warps per label when they fit
       g.KTm = g.TBlk ? 63 : pow2_ceil(K) - 1;
       if (!g.TBlk)
         while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
       g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
+      if (g.TBlk) g.NWt = g.CgMax * g.TWb;
       const int head_nt = (g.NCW + g.NAS * g.NCW + g.NNW) * 32;
       g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
       size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);

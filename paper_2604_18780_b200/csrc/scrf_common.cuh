@@ -153,20 +153,8 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity);
 // st.async from peer CTAs). A spin loop written inside one asm block deadlocked for
 // clusters of >= 12 CTAs on B200; this form does not.
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-#if defined(SCRF_EXP_WAIT) && SCRF_EXP_WAIT == 1
-  while (!mbar_try(a, parity)) __nanosleep(32);
-#elif defined(SCRF_EXP_WAIT) && SCRF_EXP_WAIT == 2
-  const unsigned act = __activemask();
-  if ((threadIdx.x & 31) == (__ffs(act) - 1))
-    while (!mbar_try(a, parity)) {
-    }
-  __syncwarp(act);
   while (!mbar_try(a, parity)) {
   }
-#else
-  while (!mbar_try(a, parity)) {
-  }
-#endif
 }
 
 // bounded wait (debug builds of the sweep): returns false after ~2^spin polls
@@ -174,7 +162,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P1;\n}"
       : "=r"(ok)
       : "r"(a), "r"(parity)

@@ -77,24 +77,6 @@ __device__ __forceinline__ void st_async_pair<double>(uint32_t dst, double x, do
                "d"(y), "r"(bar)
                : "memory");
 }
-// remote store + release arrive on a peer CTA's mbarrier (arrival-counted hand-off)
-template <typename R>
-__device__ __forceinline__ void st_cl_pair(uint32_t dst, R x, R y);
-template <>
-__device__ __forceinline__ void st_cl_pair<float>(uint32_t dst, float x, float y) {
-  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(dst), "f"(x), "f"(y) : "memory");
-}
-template <>
-__device__ __forceinline__ void st_cl_pair<double>(uint32_t dst, double x, double y) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(dst), "d"(x), "d"(y) : "memory");
-}
-__device__ __forceinline__ void st_cl_f64(uint32_t dst, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(v) : "memory");
-}
-__device__ __forceinline__ void arrive_cl(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
 __device__ __forceinline__ void st_async_f64(uint32_t dst, double v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v), "r"(bar)
                : "memory");
@@ -136,6 +118,7 @@ struct SweepGeo {
   int NNW;    // near warps
   int NG;     // near groups (2 or 4): group g owns the targets p with p % NG == g
   int PubS;   // slots of the position-indexed head rings (16: edge batches of 4, 8: per-step edge)
+  int TWb;    // blocked tails: warps per label (1, or 2 taking alternate groups of 4 targets)
   int GWn;    // near threads per label (power of two <= 32)
   int NWt;    // tail warps
   int WPL;    // tail warps per label (each pushes its own partial)
@@ -200,6 +183,12 @@ __device__ __forceinline__ long long gtimer() {
 template <typename A>
 __device__ __forceinline__ void sweep_wait(const A& a, uint32_t bar, uint32_t parity, int site, int idx) {
   if (!a.hang) {
+#ifdef SCRF_EXP_BACKOFF
+    if (site == 2) {
+      while (!mbar_try(bar, parity)) __nanosleep(SCRF_EXP_BACKOFF);
+      return;
+    }
+#endif
     mbar_wait(bar, parity);
     return;
   }
@@ -613,7 +602,7 @@ __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx&
   const SweepGeo& g = a.geo;
   const int C = a.C, K = a.K, T = a.T, L = x.L;
   const int pm = g.PubS - 1;
-  const int u = q + 5;
+  const int u = q + edge_lead(g);
   if (act && u <= L) {
     const double2 v = oq_rows(x, g, e.rw[0]);
 #pragma unroll
@@ -683,9 +672,6 @@ __device__ __forceinline__ void edge_batch(const SweepArgs<R>& a, const SweepCtx
 #pragma unroll
     for (int i = 0; i < 4; ++i) e.qh[i] = qa[4 + i];
   }
-#ifdef SCRF_EXP_NOOUT
-  outputs = false;
-#endif
   if (outputs) {
     const size_t rowbase = (size_t)x.b * (T + 1);
     const int cs = act ? c : 0;
@@ -1048,15 +1034,8 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
       split2(r, v.x, v.y);
       ringc[q & KRm] = v;
       if (TAILS && q <= nsend_max)
-#ifdef SCRF_SRC_ARRIVE
-      {
-        st_cl_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), v.x, v.y);
-        arrive_cl(t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-      }
-#else
         st_async_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), v.x, v.y,
                          t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-#endif
     }
     if (blockIdx.x == 0 && c == 0) SCRF_GT(0, q);
 #ifdef SCRF_TRACE
@@ -1064,15 +1043,8 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
       a.trace[576 * 16 + (q - a.trace_from) * 16] = clock64();  // source q sent (head clock)
 #endif
     if (TAILS && nsender && q <= nsend_max)
-#ifdef SCRF_SRC_ARRIVE
-    {
-      st_cl_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q);
-      arrive_cl(t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-    }
-#else
       st_async_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q,
                    t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-#endif
     if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
     if (!do_edge && q > Lq) {  // outputs of the positions after the last edge batch
       const size_t rowbase = (size_t)x.b * (T + 1);
@@ -1253,10 +1225,8 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     if (tr) tr[1] = clock64();
     sweep_wait(a, smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1), 2, u);
     if (tr) tr[2] = clock64();
-#ifndef SCRF_SRC_ARRIVE
     if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
       mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
-#endif
     const double F = nslot[s_new & (kSlots - 1)];
     const int kmax = min(K, u);
     for (int cl = cl0; cl < Cg; cl += lstep) {
@@ -1302,7 +1272,8 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   const SweepGeo& g = a.geo;
   const int C = a.C, T = a.T, L = x.L, kc = g.kc, KTm = g.KTm, K = a.K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cl = warp;  // one label per warp
+  const int TWb = g.TWb;
+  const int cl = warp / TWb, par = warp % TWb;  // label; which of the label's warps
   const R2* rg = (const R2*)(smem + TL.ring) + (size_t)cl * (KTm + 1);
   const double* nslot = (const double*)(smem + TL.nslot);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
@@ -1324,10 +1295,11 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   };
   // one lane per target (lanes 0..3) stages / computes / sends; results are broadcast
   const int li = lane & 3;
-  const int u0 = kc + 1;
-  // staging runs 3 groups (12 targets) ahead; one commit group per 4 targets
-  for (int gq = 0; gq < 3; ++gq) {
-    if (lane < 4 && u0 + 4 * gq + li <= L) stage(u0 + 4 * gq + li);
+  const int gstep = 4 * TWb;          // this warp's groups: ub = u0 + 4 par + gstep i
+  const int u0 = kc + 1 + 4 * par;
+  const int nahead = TWb == 1 ? 3 : 2;  // staging distance in own groups (12 / 16 targets)
+  for (int gq = 0; gq < nahead; ++gq) {
+    if (lane < 4 && u0 + gstep * gq + li <= L) stage(u0 + gstep * gq + li);
     cp_async_commit();
   }
   const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
@@ -1336,12 +1308,14 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
 #pragma unroll
   for (int i = 0; i < kBlk; ++i) zr[i] = 0;
   R Gh = Mth<R>::ninf(), Gl = 0;
-  int jown = -1;
+  int jown = -1;   // block whose z this lane holds
+  int jlast = -1;  // newest block loaded by this warp
+  int snext = 0;   // first source this warp has not waited for
 #ifdef SCRF_TRACE
   long long st_wait = 0, st_loop = 0, st_slow = 0;
   const long long st_t0 = clock64();
 #endif
-  for (int ub = u0; ub <= L; ub += 4) {
+  for (int ub = u0; ub <= L; ub += gstep) {
     const int sb = ub - kc - 1;          // newest source of target ub (multiple of 4)
     const int nt = min(4, L - ub + 1);   // targets in this group
 #ifdef SCRF_TRACE
@@ -1352,18 +1326,29 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
     constexpr long long* tr = nullptr;
 #endif
     if (tr) tr[0] = clock64();
-    cp_async_wait<2>();
+    if (TWb == 1)
+      cp_async_wait<2>();
+    else
+      cp_async_wait<1>();
     __syncwarp();
     if (tr) tr[9] = clock64();
     // the group's sources sb .. sb+nt-1 (and their normalisers)
 #ifdef SCRF_TRACE
     const long long w0 = clock64();
+    if (a.trace && blockIdx.x == 1 && threadIdx.x == 0 && sb + 3 >= a.trace_from && sb + 3 < a.trace_from + 256) {
+      a.trace[1312 * 16 + (sb + 3 - a.trace_from) * 2] = gtimer();  // tail starts waiting for sb..sb+3
+      a.trace[1312 * 16 + (sb + 3 - a.trace_from) * 2 + 1] =
+          mbar_try(smem_u32(&tbar[(sb + 3) & (kSlots - 1)]), (uint32_t)(((sb + 3) / kSlots) & 1)) ? 1 : 2;
+    }
 #endif
-    for (int i = 0; i < nt; ++i) {
-      const int s = sb + i;
+    // every source up to this group's newest (the other warp's group too: block loads need
+    // them); warp 0 re-arms each slot for its next use
+    const int s0 = snext;
+    for (int s = s0; s < sb + nt; ++s) {
       sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
       if (threadIdx.x == 0 && blockIdx.x == 1) SCRF_GT(1, s);
     }
+    snext = sb + nt;
 #ifdef SCRF_TRACE
     if (ub >= 1000) st_wait += clock64() - w0;
 #endif
@@ -1386,13 +1371,32 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
     }
     __syncwarp();
     if (tr) tr[4] = clock64();
-#ifndef SCRF_SRC_ARRIVE
-    if (warp == 0 && lane < nt) {
-      const int s = sb + lane;
+    if (warp == 0 && lane < snext - s0) {
+      const int s = s0 + lane;
       if (s + kSlots <= L - kc - 1)
         mbar_expect(smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
     }
-#endif
+    // newest complete block: z = 2^(r - G) into the registers of its owner lane
+    if (sb >= kBlk && (sb >> 5) - 1 > jlast) {
+      const int jb = (sb >> 5) - 1;
+      const R2 r = rg[(jb * kBlk + lane) & KTm];
+      const R gh = warp_max(r.x);
+      const unsigned bal = __ballot_sync(0xffffffffu, r.x == gh);
+      const R gl = __shfl_sync(0xffffffffu, r.y, __ffs(bal) - 1);
+      const R z = (gh == Mth<R>::ninf() || r.x == Mth<R>::ninf()) ? (R)0 : Mth<R>::ex2((r.x - gh) + (r.y - gl));
+      const bool own = lane == (jb & 31);
+#pragma unroll
+      for (int i = 0; i < kBlk; ++i) {
+        const R v = __shfl_sync(0xffffffffu, z, i);
+        if (own) zr[i] = v;
+      }
+      if (own) {
+        Gh = gh;
+        Gl = gl;
+        jown = jb;
+      }
+      jlast = jb;
+    }
     // newest incomplete block: sources [base, sb+i] for target i, term by term
     const int base = sb & ~(kBlk - 1);
     R xe[4];
@@ -1493,30 +1497,10 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
         st_async_pair<R>(hpart + off, mi, si, hbar + (uint32_t)(sl * sizeof(uint64_t)));
         if (warp == 0 && blockIdx.x == 1) SCRF_GT(2, ub + lane);
       }
-      if (lane < 4 && ub + 12 + lane <= L) stage(ub + 12 + lane);
+      if (lane < 4 && ub + gstep * nahead + lane <= L) stage(ub + gstep * nahead + lane);
     }
     cp_async_commit();
     if (tr) tr[8] = clock64();
-    // block (sb+3)/32 completes after this group: frame = its largest source, z to its owner lane
-    if (nt == 4 && ((sb + 3) & (kBlk - 1)) == kBlk - 1) {
-      const int jb = (sb + 3) >> 5;
-      const R2 r = rg[(jb * kBlk + lane) & KTm];
-      const R gh = warp_max(r.x);
-      const unsigned bal = __ballot_sync(0xffffffffu, r.x == gh);
-      const R gl = __shfl_sync(0xffffffffu, r.y, __ffs(bal) - 1);
-      const R z = (gh == Mth<R>::ninf() || r.x == Mth<R>::ninf()) ? (R)0 : Mth<R>::ex2((r.x - gh) + (r.y - gl));
-      const bool own = lane == (jb & 31);
-#pragma unroll
-      for (int i = 0; i < kBlk; ++i) {
-        const R v = __shfl_sync(0xffffffffu, z, i);
-        if (own) zr[i] = v;
-      }
-      if (own) {
-        Gh = gh;
-        Gl = gl;
-        jown = jb;
-      }
-    }
     if (tr) tr[3] = clock64();
 #ifdef SCRF_TRACE
     if (ub < 1000) st_loop = clock64();
@@ -1575,18 +1559,12 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       B2[i] = (R)(a.dur[(size_t)k * C + lo + cl] * kLog2e);
     }
   }
-#ifdef SCRF_SRC_ARRIVE
-  if (tid < kSlots) mbar_init(smem_u32(&tbar[tid]), Cg + 1);  // Cg source lanes + the n lane
-  __syncthreads();
-  if (tid == 0) mbar_fence_init();
-#else
   if (tid < kSlots) mbar_init(smem_u32(&tbar[tid]), 1);
   __syncthreads();
   if (tid == 0) {
     mbar_fence_init();
     for (int q = 0; q < kSlots; ++q) mbar_expect(smem_u32(&tbar[q]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
   }
-#endif
   __syncthreads();
   cluster_sync_all();
   if ((tid >> 5) < g.NWt) {

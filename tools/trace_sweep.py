@@ -24,7 +24,7 @@ prob = scrf.DeviceProblem.from_host(cum, params)
 post = len(sys.argv) > 3 and sys.argv[3] == "post"
 run = (lambda: S.device_posterior(prob)) if post else (lambda: S.device_forward(prob))
 run()
-buf = torch.zeros((1280 + 16, 16), dtype=torch.int64, device="cuda")
+buf = torch.zeros((1312 + 32, 16), dtype=torch.int64, device="cuda")
 lib = _lib.load()
 lib.scrf_debug_trace(buf.data_ptr())
 run()
@@ -189,3 +189,15 @@ if (snd > 0).all() and (rcv > 0).all():
     rtt = rcv - snd
     off = ech - (snd + rcv) / 2  # tail clock - head clock
     print(f"gt calibration: head<->tail1 global-flag rtt mean {rtt.mean():.0f} ns; offset (tail - head) mean {off.mean():.0f} ns")
+
+tw = buf.cpu().numpy()[1312:].reshape(-1)[:512].reshape(256, 2).astype(np.float64)
+off_th = off.mean() if (snd > 0).all() and (rcv > 0).all() else 0.0
+d_start, d_saw, ready = [], [], []
+for r in range(256):
+    if tw[r, 0] > 0 and G[r, 0] > 0 and G[r, 1] > 0:
+        d_start.append(tw[r, 0] - off_th - G[r, 0])  # tail wait start - head sent (head clock)
+        d_saw.append(G[r, 1] - off_th - G[r, 0])
+        ready.append(tw[r, 1] == 1)
+if d_start:
+    print(f"tail group wait for source q=sb+3: start - sent {np.mean(d_start):.0f} ns, saw - sent {np.mean(d_saw):.0f} ns, "
+          f"already complete at start {100.0 * np.mean(ready):.0f}%")
