@@ -165,6 +165,17 @@ def measured_peaks() -> dict:
         return {}
 
 
+def hbm_peak_gbs():
+    """HBM copy peak: MEASURED_PEAKS.json (driver-written) or the profiling guide's fallback."""
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        with open(f) as fh:
+            d = json.load(fh)
+        if "hbm_gbs" in d:
+            return float(d["hbm_gbs"]), "of measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "of fallback (6.65 TB/s, B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
 def mufu_peak_per_s(sm_mhz: float | None) -> tuple[float, str]:
     """MUFU ex2 peak = 148 SMs x 16 / clk x f_SM (16/clk/SM measured: profiles/r01_microbench.jsonl)."""
     peaks = measured_peaks()
@@ -260,13 +271,22 @@ def run_ours(args, rank, world, local):
 
     out = None
     if rank == 0:
-        # roofline of the dominant kernel (the backward cluster kernel: replay + beta + marginals)
-        # dominant kernel: the fused alpha+beta sweep (one launch): (K*C + C^2) ex2 per position per direction
+        # dominant kernel: the fused alpha+beta sweep (one launch): (K*C + C^2) ex2 per position per
+        # direction (SFU-bound roofline); HBM figures beside it from ncu
         E_sweep = 2 * (K * C + C * C)
         sweep_avg = float(np.mean(fwd_ms))
         post_avg = float(np.mean(bwd_ms)) - sweep_avg
         peak, peak_note = mufu_peak_per_s(clocks["sm_mhz"])
         achieved = B * T * E_sweep / (sweep_avg / 1e3)
+        # algorithmic HBM bytes of the sweep launch: S read by both sweeps, Y^/X^ fp32 messages and
+        # fp64 normaliser / max-shift rows written
+        alg_bytes = 2 * B * (T + 1) * C * 8 + 2 * 2 * B * (T + 1) * C * 4 + B * (T + 1) * (2 * 8 + 4)
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "r01_sweep_traffic.json")
+        if os.path.exists(tfile) and (B, T, K, C) == (8, 100000, 1000, 24):
+            with open(tfile) as fh:
+                traffic = int(json.load(fh)["bytes_per_launch"])
+        hbm_peak, hbm_src = hbm_peak_gbs()
         out = {
             "metric": METRIC,
             "value": value,
@@ -293,7 +313,12 @@ def run_ours(args, rank, world, local):
                 "peak": peak / 1e9,
                 "unit": "Gexp2/s",
                 "frac": achieved / peak,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_source": "profiles/r01_sweep_traffic.json (dram__bytes_read+write of one ncu --set full capture)",
+                "hbm": {"algorithmic_bytes": alg_bytes, "achieved": alg_bytes / (sweep_avg / 1e3) / 1e9,
+                        "peak": hbm_peak, "unit": "GB/s", "frac": alg_bytes / (sweep_avg / 1e3) / 1e9 / hbm_peak,
+                        "peak_source": hbm_src,
+                        "note": "latency bound: one dependent recurrence step per position, so HBM is far from binding"},
                 "algorithm": "factored: (K*C + C^2) ex2 per position per direction",
                 "per_launch_exps": B * T * E_sweep,
                 "kernel_ms": sweep_avg,
