@@ -245,6 +245,7 @@ PostGeo post_geo(const scrf_problem* p, int prec) {
   if (cg > C) cg = C;
   const size_t limit = (size_t)smem_optin();
   while (cg > 1 && (prec ? post_gradB_smem<double>(K, cg) : post_gradB_smem<float>(K, cg)) > limit) --cg;
+  while (cg > 1 && (long long)cg * ((K + kGBJ - 1) / kGBJ) > (long long)kGBW * 512) --cg;
   q.CGB = cg;
   const int ngc = (C + cg - 1) / cg;
   long long want = 4LL * num_sms();
@@ -443,6 +444,8 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
   }
   {
+    // one CTA holds every duration window of its label group (K <= kGBW * 512 * kGBJ = 4096)
+    if ((long long)q.CGB * ((K + kGBJ - 1) / kGBJ) > (long long)kGBW * 512) return SCRF_ECONFIG;
     const size_t sm = post_gradB_smem<R>(K, q.CGB);
     e = cudaFuncSetAttribute(post_gradB_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;

@@ -165,10 +165,18 @@ __global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, i
   }
 }
 
-// grad_B partial: CTA (b, source range, label group); thread owns (label, duration) pairs.
-// ra[s] / rb[u] are staged per sub-chunk of 128 sources as (hi, lo) pairs in the
-// working type; terms are (ra_hi + rb_hi) + (ra_lo + rb_lo) + B2[k-1].
+// grad_B partial: CTA (b, source range, label group). A thread owns a window of kGBJ
+// consecutive durations k0..k0+kGBJ-1 of one label and slides it along the sources: per
+// source it loads ra[s] (a warp broadcast) and the one new rb[s+k0+kGBJ-1]; the other
+// kGBJ-1 values are the previous source's, shifted in registers. ra[s] / rb[u] are staged
+// per sub-chunk of kGBSub sources as (hi, lo) pairs in the working type (rb rows skewed by
+// one pair per 16 so lanes kGBJ pairs apart hit distinct banks); terms are
+// (ra_hi + rb_hi) + (ra_lo + rb_lo) + B2[k-1], one ex2 each.
 constexpr int kGBSub = 128;
+constexpr int kGBJ = 4;
+constexpr int kGBW = 2;  // windows per thread (host keeps CG * ceil(K / kGBJ) <= kGBW * 512)
+__host__ __device__ inline int gb_skew(int ui) { return ui + (ui >> 4); }
+__host__ __device__ inline int gb_row(int K) { return gb_skew(kGBSub + K + kGBJ) + 1; }
 
 template <typename R>
 __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
@@ -179,24 +187,27 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
   const int L = (int)a.lengths[b];
   const int c0 = cg * CG;
   const int Cn = min(CG, C - c0);
-  const int nU = kGBSub + K;
+  const int nU = kGBSub + K + kGBJ;  // rb for u = s0+1 .. s0+nU (window over-read is -inf)
+  const int rowU = gb_row(K);
   R2* sa = (R2*)sm;                      // [CG][kGBSub]
-  R2* sbv = sa + (size_t)CG * kGBSub;    // [CG][nU]  rb for u = s0+1 .. s0+kGBSub+K
-  R* B2 = (R*)(sbv + (size_t)CG * nU);   // [CG][K]
+  R2* sbv = sa + (size_t)CG * kGBSub;    // [CG][rowU] (skewed)
+  R* B2 = (R*)(sbv + (size_t)CG * rowU); // [CG][K]
   const double Z2 = a.logZ[b] * kLog2e;
   const size_t rb0 = (size_t)b * (T + 1);
   for (int i = threadIdx.x; i < Cn * K; i += blockDim.x) {
     const int cl = i / K, k = i % K;
     B2[i] = (R)(a.dur[(size_t)k * C + c0 + cl] * kLog2e);
   }
-  // accumulators: thread owns pairs (cl, k) = idx, idx + blockDim, ...
-  constexpr int MAXP = 8;
-  double acc[MAXP];
+  const int nkb = (K + kGBJ - 1) / kGBJ;
+  const int nwin = Cn * nkb;
+  double acc[kGBW][kGBJ];
 #pragma unroll
-  for (int q = 0; q < MAXP; ++q) acc[q] = 0.0;
-  const int npairs = Cn * K;
+  for (int w = 0; w < kGBW; ++w)
+#pragma unroll
+    for (int j = 0; j < kGBJ; ++j) acc[w][j] = 0.0;
   const int sbeg = sb * a.SCB;
   const int send = min(sbeg + a.SCB, L);  // sources s < L
+  __syncthreads();
   for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
     __syncthreads();
     const int ns = min(kGBSub, send - s0);
@@ -218,51 +229,62 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       R2 v;
       v.x = Mth<R>::ninf();
       v.y = 0;
-      if (u <= L) {
+      if (u <= L && ui < kGBSub + K) {
         const size_t o = (rb0 + u) * C + c;
         const double rv = a.nb[rb0 + u] + (double)a.Xb[o] + a.S[o] * kLog2e +
                           (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
         split2(rv, v.x, v.y);
       }
-      sbv[(size_t)cl * nU + ui] = v;
+      sbv[(size_t)cl * rowU + gb_skew(ui)] = v;
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < MAXP; ++q) {
-      const int idx = threadIdx.x + q * blockDim.x;
-      if (idx < npairs) {
-        const int cl = idx / K, k = idx % K + 1;
+    for (int w = 0; w < kGBW; ++w) {
+      const int idx = threadIdx.x + w * blockDim.x;
+      if (idx < nwin) {
+        const int cl = idx / nkb, k0 = (idx % nkb) * kGBJ + 1;
         const R2* A = sa + (size_t)cl * kGBSub;
-        const R2* Bv = sbv + (size_t)cl * nU + (k - 1);  // u = s + k -> ui = si + k - 1
-        const R bk = B2[(size_t)cl * K + k - 1];
-        R s0a = 0, s1a = 0;
-        int si = 0;
-        for (; si + 1 < ns; si += 2) {
-          const R2 x0 = A[si], y0 = Bv[si], x1 = A[si + 1], y1 = Bv[si + 1];
-          s0a += Mth<R>::ex2(((x0.x + y0.x) + (x0.y + y0.y)) + bk);
-          s1a += Mth<R>::ex2(((x1.x + y1.x) + (x1.y + y1.y)) + bk);
+        const R2* Bv = sbv + (size_t)cl * rowU;
+        const int ub = k0 - 1;  // u = s + k -> ui = si + k - 1
+        R bk[kGBJ];
+        R2 wv[kGBJ];
+#pragma unroll
+        for (int j = 0; j < kGBJ; ++j) {
+          bk[j] = (k0 + j <= K) ? B2[(size_t)cl * K + k0 - 1 + j] : Mth<R>::ninf();
+          if (j < kGBJ - 1) wv[j] = Bv[gb_skew(ub + j)];
         }
-        if (si < ns) {
-          const R2 x0 = A[si], y0 = Bv[si];
-          s0a += Mth<R>::ex2(((x0.x + y0.x) + (x0.y + y0.y)) + bk);
+        R sj[kGBJ];
+#pragma unroll
+        for (int j = 0; j < kGBJ; ++j) sj[j] = 0;
+#pragma unroll 4
+        for (int si = 0; si < ns; ++si) {
+          wv[kGBJ - 1] = Bv[gb_skew(si + ub + kGBJ - 1)];
+          const R2 x = A[si];
+#pragma unroll
+          for (int j = 0; j < kGBJ; ++j) sj[j] += Mth<R>::ex2(((x.x + wv[j].x) + (x.y + wv[j].y)) + bk[j]);
+#pragma unroll
+          for (int j = 0; j < kGBJ - 1; ++j) wv[j] = wv[j + 1];
         }
-        acc[q] += (double)(s0a + s1a);
+#pragma unroll
+        for (int j = 0; j < kGBJ; ++j) acc[w][j] += (double)sj[j];
       }
     }
   }
 #pragma unroll
-  for (int q = 0; q < MAXP; ++q) {
-    const int idx = threadIdx.x + q * blockDim.x;
-    if (idx < npairs) {
-      const int cl = idx / K, k = idx % K;
-      a.gBp[(((size_t)b * a.nchB + sb) * K + k) * C + c0 + cl] = acc[q];
+  for (int w = 0; w < kGBW; ++w) {
+    const int idx = threadIdx.x + w * blockDim.x;
+    if (idx < nwin) {
+      const int cl = idx / nkb, k0 = (idx % nkb) * kGBJ;
+#pragma unroll
+      for (int j = 0; j < kGBJ; ++j)
+        if (k0 + j < K) a.gBp[(((size_t)b * a.nchB + sb) * K + k0 + j) * C + c0 + cl] = acc[w][j];
     }
   }
 }
 
 template <typename R>
 __host__ __device__ inline size_t post_gradB_smem(int K, int CG) {
-  return (size_t)CG * kGBSub * 2 * sizeof(R) + (size_t)CG * (kGBSub + K) * 2 * sizeof(R) + (size_t)CG * K * sizeof(R) + 16;
+  return (size_t)CG * kGBSub * 2 * sizeof(R) + (size_t)CG * gb_row(K) * 2 * sizeof(R) + (size_t)CG * K * sizeof(R) + 16;
 }
 
 // fixed-order reductions: per-sequence partials (unscaled) and batch totals (upstream-weighted)
