@@ -117,16 +117,21 @@ class DeviceProblem:
         return self.duration_bias.shape[0]
 
     @classmethod
-    def from_host(cls, cum: CumulativeScores, params: SemiCRFParams, device=None, non_blocking=False):
+    def from_host(cls, cum: CumulativeScores, params: SemiCRFParams, device=None, non_blocking=True):
+        """Copy the host problem to the device. Large arrays are staged through pinned memory
+        (torch's caching host allocator keeps each staging block alive until its copy has run),
+        which is ~2.5x faster than a pageable copy."""
         dev = device or _dev()
 
         def put(a, dt=torch.float64):
             if a is None:
                 return None
             t = torch.from_numpy(np.ascontiguousarray(a))
-            if non_blocking:
-                t = t.pin_memory()
-            return t.to(device=dev, dtype=dt, non_blocking=non_blocking)
+            if t.dtype != dt:
+                t = t.to(dt)
+            if non_blocking and t.numel() * t.element_size() >= (1 << 16):
+                return t.pin_memory().to(device=dev, non_blocking=True)
+            return t.to(device=dev)
 
         return cls(put(cum.S), put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
                    put(params.duration_bias), put(cum.proj_start), put(cum.proj_end))
@@ -417,17 +422,30 @@ def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts
     return _grads_to_host(bw), _marg_to_host(bw, cum)
 
 
+def _to_host(*tensors):
+    """Device tensors -> numpy arrays backed by pinned host memory (torch's caching host
+    allocator): all copies are queued non-blocking on the current stream, then one sync.
+    A pageable .cpu() copy of a 154 MB array takes ~70 ms on this platform, a pinned one ~3 ms."""
+    outs = []
+    for t in tensors:
+        if t is None:
+            outs.append(None)
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [None if h is None else h.numpy() for h in outs]
+
+
 def _grads_to_host(bw: DeviceBackward) -> GradientSet:
-    return GradientSet(
-        grad_S=bw.grad_S.cpu().numpy(), grad_T=bw.grad_T.cpu().numpy(), grad_B=bw.grad_B.cpu().numpy(),
-        grad_P_start=None if bw.grad_P_start is None else bw.grad_P_start.cpu().numpy(),
-        grad_P_end=None if bw.grad_P_end is None else bw.grad_P_end.cpu().numpy(),
-    )
+    gS, gT, gB, gPs, gPe = _to_host(bw.grad_S, bw.grad_T, bw.grad_B, bw.grad_P_start, bw.grad_P_end)
+    return GradientSet(grad_S=gS, grad_T=gT, grad_B=gB, grad_P_start=gPs, grad_P_end=gPe)
 
 
 def _marg_to_host(bw: DeviceBackward, cum: CumulativeScores) -> MarginalSet:
-    return MarginalSet(bw.position_marginals.cpu().numpy(), bw.boundary_posterior.cpu().numpy(),
-                       bw.expected_segment_count.cpu().numpy(), np.asarray(cum.lengths))
+    pm, bp, ec = _to_host(bw.position_marginals, bw.boundary_posterior, bw.expected_segment_count)
+    return MarginalSet(pm, bp, ec, np.asarray(cum.lengths))
 
 
 def _segments_to_host(v: DeviceViterbi) -> list[Segmentation]:
