@@ -11,6 +11,7 @@
 #include "scrf_sweep.cuh"
 #include "scrf_post.cuh"
 #include "scrf_viterbi.cu"
+#include "scrf_vit2.cuh"
 
 using namespace scrf;
 
@@ -608,9 +609,60 @@ int scrf_beta_logz(const scrf_problem* p, int precision, const void* work, doubl
 
 static size_t vit_dvr_bytes(const scrf_problem* p, const Geometry& g) { return al((size_t)p->B * g.G * p->K * p->C * 8); }
 
+// head + tails Viterbi (scrf_vit2.cuh): head-only when K <= 16, otherwise the head keeps
+// durations 1..R/2 (R = 32, 16 or 8, the largest whose rings fit next to the C x C transition
+// table) and ceil(C (K - kn) / 4000) tails (<= 16 labels each, two warps per label when they fit)
+int choose_vit2_geo(int B, int K, int C, bool has_ps, V2Geo* out) {
+  if (env_int("SCRF_VIT_OLD", 0)) return SCRF_ECONFIG;
+  const size_t limit = (size_t)smem_optin();
+  V2Geo g;
+  memset(&g, 0, sizeof(g));
+  g.NCW = (C + 31) / 32;
+  if (g.NCW > 16) return SCRF_ECONFIG;
+  g.TW = 1;
+  g.KR = 8;
+  if (K <= 16) {
+    g.G = 1;
+    g.R = 32;
+    g.kn = K;
+    g.NT = g.NCW * 32;
+    if (v2_smem_bytes(K, C, g, has_ps) > limit) return SCRF_ECONFIG;
+    *out = g;
+    return SCRF_OK;
+  }
+  for (int R = 32; R >= 8; R >>= 1) {
+    g.R = R;
+    g.kn = R / 2;
+    int nt = (int)(((long long)C * (K - g.kn) + 3999) / 4000);
+    const int ntmin = (C + 15) / 16;
+    if (nt < ntmin) nt = ntmin;
+    if (nt > 15) nt = 15;
+    if (nt > C) nt = C;
+    while (nt > ntmin && (long long)B * (1 + nt) > num_sms()) --nt;
+    g.G = 1 + nt;
+    g.CgMax = (C + nt - 1) / nt;
+    if (g.CgMax > 16) continue;
+    g.TW = g.CgMax * 2 <= 16 ? 2 : 1;
+    g.KR = K + 8;
+    const int nth = g.NCW * 32, ntt = g.CgMax * g.TW * 32;
+    g.NT = nth > ntt ? nth : ntt;
+    if (g.NT > 512) continue;
+    if (v2_smem_bytes(K, C, g, has_ps) <= limit) {
+      *out = g;
+      return SCRF_OK;
+    }
+  }
+  return SCRF_ECONFIG;
+}
+
 int scrf_viterbi_work_bytes(const scrf_problem* p, size_t* bytes) {
   int rc = check_problem(p);
   if (rc) return rc;
+  V2Geo g2;
+  if (choose_vit2_geo((int)p->B, (int)p->K, (int)p->C, p->proj_start != nullptr, &g2) == SCRF_OK) {
+    *bytes = al((size_t)p->B * (p->T + 1) * p->C * 8) + al((size_t)p->B * (p->T + 1) * p->C * 4);
+    return SCRF_OK;
+  }
   Geometry g;
   rc = choose_vit_geo((int)p->B, (int)p->K, (int)p->C, p->proj_start != nullptr, &g);
   if (rc) return rc;
@@ -627,6 +679,45 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
   size_t need = 0;
   scrf_viterbi_work_bytes(p, &need);
   if (work_bytes < need) return SCRF_EWORK;
+  V2Geo g2;
+  if (choose_vit2_geo((int)p->B, (int)p->K, (int)p->C, p->proj_start != nullptr, &g2) == SCRF_OK) {
+    V2Args a;
+    memset(&a, 0, sizeof(a));
+    a.S = p->S;
+    a.lengths = p->lengths;
+    a.trans = p->transition;
+    a.dur = p->duration_bias;
+    a.ps = p->proj_start;
+    a.pe = p->proj_end;
+    a.B = (int)p->B;
+    a.T = (int)p->T;
+    a.K = (int)p->K;
+    a.C = (int)p->C;
+    a.geo = g2;
+    unsigned char* w = (unsigned char*)work;
+    a.hist = (double*)w;
+    a.bp = (int32_t*)(w + al((size_t)p->B * (p->T + 1) * p->C * 8));
+    a.score = score;
+    a.seg_start = seg_start;
+    a.seg_end = seg_end;
+    a.seg_label = seg_label;
+    a.seg_count = seg_count;
+    const size_t smem = v2_smem_bytes(a.K, a.C, g2, a.ps != nullptr);
+    cudaError_t e;
+    if (g2.G > 1) {
+      e = launch_cl(vit2_kernel, g2.G, a.B, g2.NT, smem, (cudaStream_t)stream, a, true);
+    } else {
+      e = cudaFuncSetAttribute(vit2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) {
+        ++g_launches;
+        if (g_ev_start) cudaEventRecord(g_ev_start, (cudaStream_t)stream);
+        vit2_kernel<<<a.B, g2.NT, smem, (cudaStream_t)stream>>>(a);
+        e = cudaGetLastError();
+        if (g_ev_stop) cudaEventRecord(g_ev_stop, (cudaStream_t)stream);
+      }
+    }
+    return (int)e;
+  }
   Geometry g;
   rc = choose_vit_geo((int)p->B, (int)p->K, (int)p->C, p->proj_start != nullptr, &g);
   if (rc) return rc;

@@ -208,3 +208,19 @@ def test_alpha_beta_logz_agree_on_goldens():
         fwd, bw = S.device_posterior(prob, delta)
         zb = S.device_beta_logz(prob, fwd, bw).cpu().numpy()
         np.testing.assert_allclose(zb, exp["logZ"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,T,B", [("c3", 1500, 3), ("c4", 3000, 2), ("c5", 800, 2)])
+def test_viterbi_head_tails_matches_single_cluster_kernel(monkeypatch, cfg, T, B):
+    """The head + tails Viterbi (scrf_vit2.cuh) against the label-sliced cluster kernel
+    (scrf_viterbi.cu, SCRF_VIT_OLD=1): both restate streaming.py:411-470 exactly, so scores
+    and segmentations must be bit-identical at the BASELINE configs' K and C."""
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    c = CONFIGS[cfg]
+    _, params, cum = scrf.equivalence_instance(3, T=T, K=c["K"], C=c["C"], B=B, mode=scrf.CenteringMode.MEAN)
+    segs_new, sc_new = scrf.decode(cum, params)
+    monkeypatch.setenv("SCRF_VIT_OLD", "1")
+    segs_old, sc_old = scrf.decode(cum, params)
+    assert np.array_equal(sc_new, sc_old)
+    assert [tuple(s) for s in segs_new] == [tuple(s) for s in segs_old]
