@@ -704,14 +704,15 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
     a.seg_count = seg_count;
     const size_t smem = v2_smem_bytes(a.K, a.C, g2, a.ps != nullptr);
     cudaError_t e;
+    auto kern = g2.NT <= 256 ? vit2_kernel<256> : vit2_kernel<512>;
     if (g2.G > 1) {
-      e = launch_cl(vit2_kernel, g2.G, a.B, g2.NT, smem, (cudaStream_t)stream, a, true);
+      e = launch_cl(kern, g2.G, a.B, g2.NT, smem, (cudaStream_t)stream, a, true);
     } else {
-      e = cudaFuncSetAttribute(vit2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e == cudaSuccess) {
         ++g_launches;
         if (g_ev_start) cudaEventRecord(g_ev_start, (cudaStream_t)stream);
-        vit2_kernel<<<a.B, g2.NT, smem, (cudaStream_t)stream>>>(a);
+        kern<<<a.B, g2.NT, smem, (cudaStream_t)stream>>>(a);
         e = cudaGetLastError();
         if (g_ev_stop) cudaEventRecord(g_ev_stop, (cudaStream_t)stream);
       }

@@ -18,6 +18,8 @@
 //    directions (no cluster barriers in the loop).
 #pragma once
 
+#include <cstdio>
+
 #include "scrf_common.cuh"
 
 namespace scrf {
@@ -191,13 +193,20 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     const double* v = vsm + (t & 1) * C;
     double best = -CUDART_INF, sec = -CUDART_INF;
     int arg = 0;
-    for (int cp = 0; cp < C; ++cp) {
-      const double x = __dadd_rn(v[cp], Tm[(size_t)cp * C + cs]);
-      if (x > best) {
-        sec = best;
-        best = x;
-        arg = cp;
+    for (int c0 = 0; c0 < C; c0 += 8) {  // 8 independent loads + adds, then the ordered scan
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int cp = min(c0 + j, C - 1);
+        x[j] = __dadd_rn(v[cp], Tm[(size_t)cp * C + cs]);
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c0 + j < C && x[j] > best) {
+          sec = best;
+          best = x[j];
+          arg = c0 + j;
+        }
     }
     if (act) {
       const int r = t & Rm;
@@ -232,7 +241,16 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     fPe[i] = (act && hpe && t <= L) ? __ldg(pe + (size_t)(t - 1) * C + cs) : 0.0;
     fPs[i] = (act && hps && t <= L && t < T) ? __ldg(ps + (size_t)t * C + cs) : 0.0;
   }
+#ifdef SCRF_VIT_PROF
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, c0 = 0, c1 = 0;
+#define VPH(i) do { c1 = clock64(); ph[i] += c1 - c0; c0 = c1; } while (0)
+#else
+#define VPH(i) do {} while (0)
+#endif
   for (int t = 1; t <= L; ++t) {
+#ifdef SCRF_VIT_PROF
+    c0 = clock64();
+#endif
     const double St = fS[0], Pet = fPe[0], Pst = fPs[0];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -251,20 +269,24 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     double best = -CUDART_INF, hb = 0.0;
     int bk = 0;
     const int kmax = min(kn, t);
+    // all ring reads and adds first (slots of absent durations hold stale but readable values)
+    double cv[16], hv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = (t - i - 1) & Rm;
+      hv[i] = v2_h(St, hS[r * C + cs], bkr[i], hP ? hP[r * C + cs] : 0.0, Pet, hps, hpe);
+      cv[i] = __dadd_rn(hg[r * C + cs], hv[i]);
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int k = i + 1;
-      if (k <= kmax) {
-        const int r = (t - k) & Rm;
-        const double h = v2_h(St, hS[r * C + cs], bkr[i], hP ? hP[r * C + cs] : 0.0, Pet, hps, hpe);
-        const double cand = __dadd_rn(hg[r * C + cs], h);
-        if (cand > best || (cand == best && k > bk)) {
-          best = cand;
-          bk = k;
-          hb = h;
-        }
+      if (k <= kmax && (cv[i] > best || (cv[i] == best && k > bk))) {
+        best = cv[i];
+        bk = k;
+        hb = hv[i];
       }
     }
+    VPH(0);
     int src = 0;
     bool flag = false;
     if (bk > 0) {
@@ -273,6 +295,7 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
       const double sec = hs[r * C + cs];
       flag = src > 0 && sec != -CUDART_INF && __dadd_rn(sec, hb) == best;
     }
+    VPH(1);
     // durations kn+1..K from the tails
     if (tails && t > kn && K > kn) {
       const int pi = t - kn - 1;
@@ -289,6 +312,7 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
       }
       if (tid == 0 && t + g.R <= L) mbar_expect(smem_u32(&tbar[sl]), (uint32_t)(C * 16));
     }
+    VPH(2);
     if (act && flag) {
       // rare: an earlier source label ties after rounding; re-scan in the reference's order
       const int s = t - bk;
@@ -308,8 +332,15 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
       vsm[(t & 1) * C + c] = best;
     }
     sync_head();
+    VPH(3);
     gamma(t, St, Pst);
+    VPH(4);
   }
+#ifdef SCRF_VIT_PROF
+  if (b == 0 && tid == 0)
+    printf("vit2 head cycles/step: near %.0f, flag %.0f, tail wait+merge %.0f, fix+store+sync %.0f, gamma+send %.0f\n",
+           (double)ph[0] / L, (double)ph[1] / L, (double)ph[2] / L, (double)ph[3] / L, (double)ph[4] / L);
+#endif
   sync_head();
   if (tid == 0) {
     const double* fin = vsm + (L & 1) * C;
@@ -450,7 +481,10 @@ __device__ void v2_tail(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
   }
 }
 
-__global__ void __launch_bounds__(512) vit2_kernel(V2Args a) {
+// NTMAX: thread bound of the instantiation (256 leaves the head 255 registers for its
+// candidate arrays; 512 when the tails need 16 warps)
+template <int NTMAX>
+__global__ void __launch_bounds__(NTMAX) vit2_kernel(V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const V2Geo& g = a.geo;
   const int b = blockIdx.x / g.G, rank = blockIdx.x % g.G;
