@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also time forward-only and Viterbi")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the forward-only and Viterbi throughputs (reported beside the headline, SURVEY 8(d))")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -401,7 +402,7 @@ def main():
             out["e2e"] = e2e_measure(ctx, args)
         elif not args.no_e2e:
             out["e2e"] = None
-        if args.extras:
+        if not args.no_extras and world == 1:
             out["extras"] = extras_measure(ctx, args)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
