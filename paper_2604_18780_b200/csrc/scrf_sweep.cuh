@@ -784,13 +784,29 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       nbar_sync(BAR_CH2, nch);
       if (act) {
         int y = 0;
-        for (; y + 4 <= C; y += 4) {
-          s0 += h.ew[y] * Mval(y);
-          s1 += h.ew[y + 1] * Mval(y + 1);
-          s2 += h.ew[y + 2] * Mval(y + 2);
-          s3 += h.ew[y + 3] * Mval(y + 3);
+        if (g.Msm) {  // M column of this label in shared memory: loads pipelined 8 deep
+          const R* Mc = h.M + c;
+#pragma unroll 2
+          for (; y + 8 <= C; y += 8) {
+            s0 += h.ew[y] * Mc[(size_t)y * C];
+            s1 += h.ew[y + 1] * Mc[(size_t)(y + 1) * C];
+            s2 += h.ew[y + 2] * Mc[(size_t)(y + 2) * C];
+            s3 += h.ew[y + 3] * Mc[(size_t)(y + 3) * C];
+            s0 += h.ew[y + 4] * Mc[(size_t)(y + 4) * C];
+            s1 += h.ew[y + 5] * Mc[(size_t)(y + 5) * C];
+            s2 += h.ew[y + 6] * Mc[(size_t)(y + 6) * C];
+            s3 += h.ew[y + 7] * Mc[(size_t)(y + 7) * C];
+          }
+          for (; y < C; ++y) s0 += h.ew[y] * Mc[(size_t)y * C];
+        } else {
+          for (; y + 4 <= C; y += 4) {
+            s0 += h.ew[y] * Mval(y);
+            s1 += h.ew[y + 1] * Mval(y + 1);
+            s2 += h.ew[y + 2] * Mval(y + 2);
+            s3 += h.ew[y + 3] * Mval(y + 3);
+          }
+          for (; y < C; ++y) s0 += h.ew[y] * Mval(y);
         }
-        for (; y < C; ++y) s0 += h.ew[y] * Mval(y);
       }
       nbar_sync(BAR_CH, nch);
     }
