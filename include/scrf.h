@@ -129,6 +129,13 @@ int scrf_last_launch_count(void);
  * dominant kernel live (no profiler). */
 void scrf_profile_events(void* start, void* stop);
 
+/* Record the given cudaEvent_t (or NULL to disable) on the call's stream as soon as the
+ * per-position outputs of every subsequent scrf_backward / scrf_posterior call on this thread
+ * are final (grad_S, grad_P*, position marginals, boundary posterior), before the duration-
+ * gradient pass. Lets a caller start their device-to-host copies on another stream while the
+ * remaining pass runs. */
+void scrf_position_outputs_event(void* event);
+
 /* Debug: if non-NULL, the next sweep writes clock64() phase stamps of cluster 0 for
  * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);

@@ -67,6 +67,7 @@ _SIGS = {
     "scrf_export_checkpoints": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
+    "scrf_position_outputs_event": (None, [_vp]),
     "scrf_debug_trace": (None, [_vp]),
     "scrf_debug_hang": (_int, [_vp]),
 }

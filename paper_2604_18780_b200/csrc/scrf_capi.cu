@@ -21,6 +21,7 @@ thread_local int g_launches = 0;
 // optional events recorded around the next main kernel launch (forward / backward / Viterbi)
 thread_local cudaEvent_t g_ev_start = nullptr;
 thread_local cudaEvent_t g_ev_stop = nullptr;
+thread_local cudaEvent_t g_ev_pos = nullptr;  // recorded once the per-position outputs are final
 thread_local long long* g_trace = nullptr;  // debug: clock64 phase stamps of the next sweep
 int* g_hang = nullptr;                        // debug: watchdog record (SCRF_WATCHDOG=1)
 
@@ -443,6 +444,7 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     post_pos_kernel<R><<<dim3(q.nch, B), 256, sm, st>>>(a);
     ++g_launches;
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
+    if (g_ev_pos) cudaEventRecord(g_ev_pos, st);
   }
   {
     // one CTA holds every duration window of its label group (K <= kGBW * 512 * kGBJ = 4096)
@@ -784,5 +786,7 @@ void scrf_profile_events(void* start, void* stop) {
   g_ev_start = (cudaEvent_t)start;
   g_ev_stop = (cudaEvent_t)stop;
 }
+
+void scrf_position_outputs_event(void* event) { g_ev_pos = (cudaEvent_t)event; }
 
 }  // extern "C"

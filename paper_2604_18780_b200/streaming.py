@@ -18,6 +18,7 @@ Two layers:
 
 from __future__ import annotations
 
+import ctypes
 import enum
 from dataclasses import dataclass, field
 from math import sqrt
@@ -438,6 +439,30 @@ def _to_host(*tensors):
     return [None if h is None else h.numpy() for h in outs]
 
 
+_SIDE = {}
+
+
+def _side_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream()
+    return _SIDE[dev]
+
+
+def _to_host_async(*tensors):
+    """Queue device->pinned-host copies on the current stream (no sync); returns the host
+    tensors (None passes through)."""
+    outs = []
+    for t in tensors:
+        if t is None:
+            outs.append(None)
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    return outs
+
+
 def _grads_to_host(bw: DeviceBackward) -> GradientSet:
     gS, gT, gB, gPs, gPe = _to_host(bw.grad_S, bw.grad_T, bw.grad_B, bw.grad_P_start, bw.grad_P_end)
     return GradientSet(grad_S=gS, grad_T=gT, grad_B=gB, grad_P_start=gPs, grad_P_end=gPe)
@@ -489,12 +514,30 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
             raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
         up_t = torch.as_tensor(up)
     prob = DeviceProblem.from_host(cum, params)
-    fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device))
+    # the per-position outputs (the bulk of the device->host bytes) are copied on a side stream
+    # while the duration-gradient pass still runs
+    lib = _lib.load()
+    ready = torch.cuda.Event()
+    ready.record()  # torch creates the CUDA event lazily: make the handle real before passing it
+    lib.scrf_position_outputs_event(ctypes.c_void_p(ready.cuda_event))
+    try:
+        fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device))
+    finally:
+        lib.scrf_position_outputs_event(None)
+    side = _side_stream()
+    side.wait_event(ready)
+    with torch.cuda.stream(side):
+        early = _to_host_async(bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals,
+                               bw.boundary_posterior)
     _raise_if_dead(fwd)
     if ledger is not None:
         ledger.record("checkpoints", fwd.ckpt)
         ledger.record("workspace", bw.work)
-    return fwd.logZ.cpu().numpy(), _grads_to_host(bw), _marg_to_host(bw, cum)
+    logZ, gT, gB, cnt = _to_host(fwd.logZ, bw.grad_T, bw.grad_B, bw.expected_segment_count)
+    side.synchronize()
+    gS, gPs, gPe, pm, bp = (None if h is None else h.numpy() for h in early)
+    return (logZ, GradientSet(grad_S=gS, grad_T=gT, grad_B=gB, grad_P_start=gPs, grad_P_end=gPe),
+            MarginalSet(pm, bp, cnt, np.asarray(cum.lengths)))
 
 
 def decode(cum, params, backend=None, *, ledger=None):
