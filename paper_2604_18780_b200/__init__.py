@@ -58,9 +58,15 @@ from .streaming import (
     streaming_viterbi,
 )
 
+from .layer import SemiCRF, build_scores_t, gold_scores_t, training_loss_and_grads_device
+
 __version__ = "0.1.0"
 
 __all__ = [
+    "SemiCRF",
+    "build_scores_t",
+    "gold_scores_t",
+    "training_loss_and_grads_device",
     "BackendKind", "CenteredEmissions", "CenteringMode", "CheckpointSet", "ContractViolation",
     "CumulativeScores", "DeviceProblem", "EmissionBatch", "GradientSet", "MarginalSet", "MemoryLedger",
     "NEG_INF", "RingAudit", "RunStats", "Segmentation", "SemiCRFParams", "CONFIGS", "boundary_entropy",
