@@ -224,3 +224,35 @@ def test_viterbi_head_tails_matches_single_cluster_kernel(monkeypatch, cfg, T, B
     segs_old, sc_old = scrf.decode(cum, params)
     assert np.array_equal(sc_new, sc_old)
     assert [tuple(s) for s in segs_new] == [tuple(s) for s in segs_old]
+
+
+@pytest.mark.parametrize("which", ["start", "end"])
+def test_single_projection_equals_zero_partner(which):
+    """proj_start and proj_end are independent inputs (the reference assumes
+    both or neither, streaming.py:325): one projection alone must give the results of the
+    pair with an all-zero partner, including its own gradient."""
+    from dataclasses import replace
+
+    _, params, cum = scrf.equivalence_instance(4, T=300, K=20, C=6, B=3, mode=scrf.CenteringMode.MEAN)
+    rng = np.random.default_rng(11)
+    B, T, C = cum.batch_size, cum.max_length, cum.num_labels
+    P = rng.uniform(-0.5, 0.5, (B, T, C))
+    Z = np.zeros((B, T, C))
+    one = replace(cum, proj_start=P if which == "start" else None, proj_end=P if which == "end" else None)
+    pair = replace(cum, proj_start=P if which == "start" else Z, proj_end=P if which == "end" else Z)
+    for prec, tol in (("fp64", 1e-12), ("fp32", 1e-6)):
+        S.set_precision(prec)
+        try:
+            z1, g1, m1 = scrf.posterior(one, params)
+            z2, g2, m2 = scrf.posterior(pair, params)
+        finally:
+            S.set_precision("fp32")
+        np.testing.assert_allclose(z1, z2, rtol=tol)
+        for a, b in ((g1.grad_S, g2.grad_S), (g1.grad_T, g2.grad_T), (g1.grad_B, g2.grad_B),
+                     (m1.position_marginals, m2.position_marginals), (m1.boundary_posterior, m2.boundary_posterior)):
+            np.testing.assert_allclose(a, b, atol=tol * 10)
+        mine = g1.grad_P_start if which == "start" else g1.grad_P_end
+        ref = g2.grad_P_start if which == "start" else g2.grad_P_end
+        assert mine is not None
+        np.testing.assert_allclose(mine, ref, atol=tol * 10)
+        assert (g1.grad_P_end if which == "start" else g1.grad_P_start) is None
