@@ -103,3 +103,41 @@ def test_training_loss_and_grads_match_reference_formula():
     np.testing.assert_allclose(ge, (ge_model - g_e) / B, atol=1e-10)
     np.testing.assert_allclose(gT, (grads.grad_T - g_T) / B, atol=1e-10)
     np.testing.assert_allclose(gB, (grads.grad_B - g_B) / B, atol=1e-10)
+
+
+def test_cli_parser_and_dense_rejection(capsys):
+    from paper_2604_18780_b200 import cli
+
+    args = cli.build_parser().parse_args(["decode", "--params", "p.json", "--emissions", "e.csv", "--backend", "dense"])
+    assert args.command == "decode" and args.centering == "none"
+    assert cli.main(["bench", "--backend", "dense"]) == 2
+    assert '"status": "fail"' in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_cli_decode_with_marginals(tmp_path):
+    """decode --marginals (cli.py:390-440): segmentations and scores equal decode(); the
+    marginal document equals posterior()'s per-position marginals trimmed to each length."""
+    import json
+
+    from paper_2604_18780_b200 import cli, streaming as S
+    from paper_2604_18780_b200.potentials import save_emissions_csv, save_params_json
+
+    em, lengths, params = _instance(9, B=2, T=30, K=5, C=3)
+    params = SemiCRFParams(params.transition, params.duration_bias)
+    save_params_json(params, str(tmp_path / "p.json"))
+    save_emissions_csv(EmissionBatch(em, lengths), str(tmp_path / "e.csv"))
+    rc = cli.main(["decode", "--params", str(tmp_path / "p.json"), "--emissions", str(tmp_path / "e.csv"),
+                   "--marginals", str(tmp_path / "m.json"), "--out", str(tmp_path / "d.json")])
+    assert rc == 0
+    doc = json.load(open(tmp_path / "d.json"))
+    cum = build_scores(EmissionBatch(em, lengths), params, CenteringMode.NONE)
+    segs, scores = S.decode(cum, params)
+    assert doc["scores"] == [float(v) for v in scores]
+    from paper_2604_18780_b200.potentials import segmentations_from_json
+
+    assert [tuple(s) for s in segmentations_from_json(doc["segmentations"])] == [tuple(s) for s in segs]
+    m = json.load(open(tmp_path / "m.json"))
+    _, _, marg = S.posterior(cum, params)
+    for b, L in enumerate(lengths):
+        np.testing.assert_allclose(np.array(m["position_marginals"][b]), marg.position_marginals[b, :L], atol=1e-12)
