@@ -458,9 +458,9 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
   {
     const int nT = C * C, nB = K * C;
     ++g_launches;
-    post_reduce_kernel<<<(nT + 255) / 256, 256, 0, st>>>(B, nT, q.nch, a.gTp, upstream, (double*)(wb + W.gTs), grad_T);
+    post_reduce2_kernel<<<(nT + 31) / 32, 256, 0, st>>>(B, nT, q.nch, a.gTp, upstream, (double*)(wb + W.gTs), grad_T);
     ++g_launches;
-    post_reduce_kernel<<<(nB + 255) / 256, 256, 0, st>>>(B, nB, q.nchB, a.gBp, upstream, (double*)(wb + W.gBs), grad_B);
+    post_reduce2_kernel<<<(nB + 31) / 32, 256, 0, st>>>(B, nB, q.nchB, a.gBp, upstream, (double*)(wb + W.gBs), grad_B);
     ++g_launches;
     post_count_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, q.nch, a.cntp, cnt);
   }

@@ -302,6 +302,41 @@ __global__ void post_reduce_kernel(int B, int n, int nparts, const double* parts
   if (total) total[i] = tot;
 }
 
+// Same sums, parallel over the parts: block (32 outputs x 8 warps); warp w sums parts
+// w, w+8, ... in order and the 8 warp sums are added in warp order (a fixed order, so the
+// result is deterministic and independent of scheduling).
+__global__ void __launch_bounds__(256) post_reduce2_kernel(int B, int n, int nparts, const double* parts,
+                                                           const double* upstream, double* per_seq, double* total) {
+  __shared__ double ws[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  const bool ok = i < n;
+  double tot = 0.0;
+  for (int b = 0; b < B; ++b) {
+    double s0 = 0.0, s1 = 0.0;
+    const double* pb = parts + (size_t)b * nparts * n + i;
+    int q = w;
+    for (; q + 8 < nparts; q += 16) {
+      if (ok) {
+        s0 += pb[(size_t)q * n];
+        s1 += pb[(size_t)(q + 8) * n];
+      }
+    }
+    if (q < nparts && ok) s0 += pb[(size_t)q * n];
+    ws[w][lane] = s0 + s1;
+    __syncthreads();
+    if (w == 0) {
+      double sb = 0.0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) sb += ws[v][lane];
+      if (ok && per_seq) per_seq[(size_t)b * n + i] = sb;
+      tot += (upstream ? upstream[b] : 1.0) * sb;
+    }
+    __syncthreads();
+  }
+  if (w == 0 && ok && total) total[i] = tot;
+}
+
 __global__ void post_count_kernel(int B, int nch, const double* cntp, double* count) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
