@@ -384,7 +384,7 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   if (dirs & 1) {
     // reference bookkeeping (N, dead_at, logZ) from the stored per-position normalisers
     ++g_launches;
-    book_kernel<R><<<a.B, 256, a.n_ckpt * sizeof(double), st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
+    book_kernel<R><<<a.B, 1024, a.n_ckpt * sizeof(double), st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
                                                                a.n_ckpt, N, dead_at, logZ);
     e = cudaGetLastError();
   }
@@ -443,6 +443,8 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     ++g_launches;
     post_pos_kernel<R><<<dim3(q.nch, B), 256, sm, st>>>(a);
     ++g_launches;
+    ++g_launches;
+    post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
     if (g_ev_pos) cudaEventRecord(g_ev_pos, st);
   }

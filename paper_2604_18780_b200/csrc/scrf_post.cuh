@@ -148,19 +148,54 @@ __host__ __device__ inline size_t post_pos_smem(int C, int CH) {
 }
 
 // pass 2: add the carry of the preceding chunks to the local coverage, clip, zero padding
+// chunk totals -> exclusive prefix over chunks, in place: one warp per (b, c); each lane
+// sums a run of consecutive chunks, a warp scan of the run totals gives every run's start
+// (fixed order, deterministic)
+__global__ void __launch_bounds__(256) post_prefix_kernel(int B, int C, int nch, double* tot) {
+  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (wid >= B * C) return;
+  const int b = wid / C, c = wid % C;
+  double* base = tot + (size_t)b * nch * C + c;
+  const int per = (nch + 31) / 32, q0 = lane * per;
+  double loc = 0.0;
+  for (int i = 0; i < per; ++i)
+    if (q0 + i < nch) loc += base[(size_t)(q0 + i) * C];
+  double incl = loc;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  double run = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) run = 0.0;
+  for (int i = 0; i < per; ++i)
+    if (q0 + i < nch) {
+      const double v = base[(size_t)(q0 + i) * C];
+      base[(size_t)(q0 + i) * C] = run;
+      run += v;
+    }
+}
+
+// pass 2: add the carry of the preceding chunks (tot holds exclusive prefixes after
+// post_prefix_kernel) to the local coverage, clip, zero padding
 __global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, int CH, int nch, const double* tot,
-                                  double* pos) {
+                                  double* __restrict__ pos) {
   const int b = blockIdx.y, ch = blockIdx.x;
   const int L = (int)lengths[b];
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    double carry = 0.0;
-    for (int q = 0; q < ch; ++q) carry += tot[((size_t)b * nch + q) * C + c];
+    const double carry = tot[((size_t)b * nch + ch) * C + c];
     const int t0 = ch * CH;
-    for (int i = 0; i < CH; ++i) {
-      const int t = t0 + i;
-      if (t >= T) break;
-      double* p = pos + ((size_t)b * T + t) * C + c;
-      *p = (t < L) ? fmin(fmax(*p + carry, 0.0), 1.0) : 0.0;
+    for (int i = 0; i < CH; i += 4) {
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = t0 + i + j;
+        v[j] = (i + j < CH && t < T) ? pos[((size_t)b * T + t) * C + c] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = t0 + i + j;
+        if (i + j < CH && t < T) pos[((size_t)b * T + t) * C + c] = (t < L) ? fmin(fmax(v[j] + carry, 0.0), 1.0) : 0.0;
+      }
     }
   }
 }

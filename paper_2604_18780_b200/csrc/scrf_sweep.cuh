@@ -1648,7 +1648,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
 // message at or below the guard relative to the running N), and logZ = LSE_c alpha[L,c].
 // One block per sequence; N_i is a short sequential recurrence, the dead scan is parallel.
 template <typename R>
-__global__ void __launch_bounds__(256) book_kernel(const R* Ya, const double* na, const R* amx, const int64_t* lengths,
+__global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* na, const R* amx, const int64_t* lengths,
                                                    int T, int C, int delta, int n_ckpt, double* N, int32_t* dead_at,
                                                    double* logZ) {
   const int b = blockIdx.x;
