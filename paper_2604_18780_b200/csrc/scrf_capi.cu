@@ -634,7 +634,7 @@ int choose_vit2_geo(int B, int K, int C, bool has_ps, V2Geo* out) {
     *out = g;
     return SCRF_OK;
   }
-  for (int R = 32; R >= 8; R >>= 1) {
+  for (int R = 8; R >= 8; R >>= 1) {  // near durations 1..4: the head's fp64 compares are its bottleneck
     g.R = R;
     g.kn = R / 2;
     int nt = (int)(((long long)C * (K - g.kn) + 3999) / 4000);
@@ -708,7 +708,8 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
     a.seg_count = seg_count;
     const size_t smem = v2_smem_bytes(a.K, a.C, g2, a.ps != nullptr);
     cudaError_t e;
-    auto kern = g2.NT <= 256 ? vit2_kernel<256> : vit2_kernel<512>;
+    auto kern = g2.NT <= 256 ? (g2.kn <= 4 ? vit2_kernel<256, 4> : g2.kn <= 8 ? vit2_kernel<256, 8> : vit2_kernel<256, 16>)
+                             : (g2.kn <= 4 ? vit2_kernel<512, 4> : g2.kn <= 8 ? vit2_kernel<512, 8> : vit2_kernel<512, 16>);
     if (g2.G > 1) {
       e = launch_cl(kern, g2.G, a.B, g2.NT, smem, (cudaStream_t)stream, a, true);
     } else {

@@ -125,6 +125,7 @@ __device__ __forceinline__ double v2_h(double St, double Ss, double Bk, double P
 }
 
 // ---------------------------------------------------------------------------- head
+template <int NK>  // near candidates per step (>= kn)
 __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, int b) {
   const V2Geo& g = a.geo;
   const int C = a.C, K = a.K, T = a.T;
@@ -164,9 +165,9 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
   const int c = tid;
   const bool act = c < C;
   const int cs = act ? c : 0;
-  double bkr[16];  // duration biases 1..kn of this label
+  double bkr[NK];  // duration biases 1..kn of this label
 #pragma unroll
-  for (int i = 0; i < 16; ++i) bkr[i] = (i < kn) ? a.dur[(size_t)i * C + cs] : 0.0;
+  for (int i = 0; i < NK; ++i) bkr[i] = (i < kn) ? a.dur[(size_t)i * C + cs] : 0.0;
   // destination of this label's sources in its tail
   uint32_t t_gs = 0, t_sp = 0, t_ga = 0, t_bar = 0;
   if (tails) {
@@ -270,15 +271,15 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     int bk = 0;
     const int kmax = min(kn, t);
     // all ring reads and adds first (slots of absent durations hold stale but readable values)
-    double cv[16], hv[16];
+    double cv[NK], hv[NK];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < NK; ++i) {
       const int r = (t - i - 1) & Rm;
       hv[i] = v2_h(St, hS[r * C + cs], bkr[i], hP ? hP[r * C + cs] : 0.0, Pet, hps, hpe);
       cv[i] = __dadd_rn(hg[r * C + cs], hv[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < NK; ++i) {
       const int k = i + 1;
       if (k <= kmax && (cv[i] > best || (cv[i] == best && k > bk))) {
         best = cv[i];
@@ -483,14 +484,14 @@ __device__ void v2_tail(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
 
 // NTMAX: thread bound of the instantiation (256 leaves the head 255 registers for its
 // candidate arrays; 512 when the tails need 16 warps)
-template <int NTMAX>
+template <int NTMAX, int NK>
 __global__ void __launch_bounds__(NTMAX) vit2_kernel(V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const V2Geo& g = a.geo;
   const int b = blockIdx.x / g.G, rank = blockIdx.x % g.G;
   const V2Tail TL = v2_tail_layout(a.K, g);
   if (rank == 0)
-    v2_head(a, smem, TL, b);
+    v2_head<NK>(a, smem, TL, b);
   else
     v2_tail(a, smem, TL, b, rank);
   if (g.G > 1) cluster_sync_all();
