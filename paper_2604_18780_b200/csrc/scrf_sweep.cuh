@@ -869,16 +869,15 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     const bool dead = (am == Mth<R>::ninf());
     const R yh = dead ? Mth<R>::ninf() : y - am;
     const double n_p = dead ? n_prev : n_prev + (double)am;
-    const R xh = gemv(yh);
-    if (tr) tr[2] = clock64();
-    if (act) {
-      h.pubY[(p & pubm) * C + c] = yh;
-      h.pubX[(p & pubm) * C + c] = xh;
-    }
+    // everything but X^[p] is published before the GEMV so those stores overlap it
+    if (act) h.pubY[(p & pubm) * C + c] = yh;
     if (tid == 0) {
       h.pubA[p & pubm] = am;
       h.nring[p & (kNring - 1)] = n_p;
     }
+    const R xh = gemv(yh);
+    if (tr) tr[2] = clock64();
+    if (act) h.pubX[(p & pubm) * C + c] = xh;
     nbar_arrive(BAR_A + (p & 3), NA + ((p & 3) == 0 ? NAE : 0));
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(5, p);
     if (tr) tr[3] = clock64();
