@@ -130,7 +130,18 @@ class DeviceProblem:
             t = torch.from_numpy(np.ascontiguousarray(a))
             if t.dtype != dt:
                 t = t.to(dt)
-            if non_blocking and t.numel() * t.element_size() >= (1 << 16):
+            nbytes = t.numel() * t.element_size()
+            if non_blocking and nbytes >= (16 << 20):
+                # chunked: the host copy of chunk i into pinned memory overlaps the DMA of chunk i-1
+                flat = t.reshape(-1)
+                pin = torch.empty(flat.shape, dtype=dt, pin_memory=True)
+                out = torch.empty(flat.shape, dtype=dt, device=dev)
+                step = -(-flat.numel() // 8)
+                for i0 in range(0, flat.numel(), step):
+                    pin[i0:i0 + step].copy_(flat[i0:i0 + step])
+                    out[i0:i0 + step].copy_(pin[i0:i0 + step], non_blocking=True)
+                return out.view(t.shape)
+            if non_blocking and nbytes >= (1 << 16):
                 return t.pin_memory().to(device=dev, non_blocking=True)
             return t.to(device=dev)
 
