@@ -1289,6 +1289,9 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TWb = g.TWb;
   const int cl = warp / TWb, par = warp % TWb;  // label; which of the label's warps
+  // tails of an uneven label split own fewer than CgMax labels: their spare warps must not run
+  // (they would send partials into another tail's label slots and break the head's byte count)
+  if (cl >= Cg) return;
   const R2* rg = (const R2*)(smem + TL.ring) + (size_t)cl * (KTm + 1);
   const double* nslot = (const double*)(smem + TL.nslot);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);

@@ -256,3 +256,21 @@ def test_single_projection_equals_zero_partner(which):
         assert mine is not None
         np.testing.assert_allclose(mine, ref, atol=tol * 10)
         assert (g1.grad_P_end if which == "start" else g1.grad_P_start) is None
+
+
+@pytest.mark.parametrize("shape", ["36,1000,2,1500", "24,1000,2,1500,SCRF_SWEEP_G=6", "20,300,3,900,SCRF_SWEEP_G=13"])
+def test_uneven_tail_label_split_completes(shape):
+    """Tails of an uneven label split (C not a multiple of the tail count) once ran spare
+    warps that wrote into another tail's partial slots and hung the head; run each geometry
+    in a subprocess with a timeout so a regression fails instead of hanging the suite, and
+    check alpha- and beta-side log Z agree."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "hang_probe.py"), shape], capture_output=True,
+                       text=True, timeout=300)
+    line = (r.stdout.strip().splitlines() or [""])[-1]
+    assert " ok " in line, line + r.stderr[-500:]
+    assert float(line.split()[-1]) < 1e-4
