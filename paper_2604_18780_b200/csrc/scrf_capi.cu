@@ -167,9 +167,9 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   g.KTm = pow2_ceil(K) - 1;
   g.GWn = near_gw(kNear - 5);
   g.NNW = g.NG * ((C * g.GWn + 31) / 32);
-  // blocked tails (one warp per label, <= 16 labels per tail) when the duration range allows;
-  // clusters of >= 12 CTAs hang with the blocked tails on this part (root cause open), so
-  // at most 8 tails (8 x 16 labels covers C <= 128)
+  // blocked tails (one or two warps per label, <= 16 labels per tail) when the duration range
+  // allows; at most 8 tails (8 x 16 labels covers C <= 128). (Larger clusters used to hang
+  // because of spare warps in tails of an uneven label split; fixed in tail_loop_blocked.)
   bool blk = env_int("SCRF_TAIL_EXACT", 0) == 0 && K >= kNear + 33 && K <= 1024 + kNear;
   const int maxt = C < 8 ? C : 8;
   auto start_tails = [&](bool blocked) {
