@@ -274,3 +274,20 @@ def test_uneven_tail_label_split_completes(shape):
     line = (r.stdout.strip().splitlines() or [""])[-1]
     assert " ok " in line, line + r.stderr[-500:]
     assert float(line.split()[-1]) < 1e-4
+
+
+def test_viterbi_full_config4_matches_single_cluster_kernel(monkeypatch):
+    """Config 4 at its full size (B=8, T=1e5, K=1000, C=24): the head + tails Viterbi and the
+    label-sliced kernel agree bit for bit on every score and segment (size-independent check
+    of the exact max-plus restatement, streaming.py:411-470)."""
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    c = CONFIGS["c4"]
+    _, params, cum = scrf.equivalence_instance(0, T=c["T"], K=c["K"], C=c["C"], B=c["B"], mode=scrf.CenteringMode.MEAN)
+    segs_new, sc_new = scrf.decode(cum, params)
+    monkeypatch.setenv("SCRF_VIT_OLD", "1")
+    segs_old, sc_old = scrf.decode(cum, params)
+    assert np.array_equal(sc_new, sc_old)
+    assert [tuple(s) for s in segs_new] == [tuple(s) for s in segs_old]
+    for b, s in enumerate(segs_new):
+        s.validate(int(cum.lengths[b]), params.max_duration, params.num_labels)
