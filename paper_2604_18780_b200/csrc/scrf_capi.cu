@@ -131,7 +131,8 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   g.NAS = g.NCW == 1 ? 2 : 1;  // separate source and edge warps when they fit
   g.NG = g.NCW == 1 ? 4 : 2;   // near groups (each owns every NG-th target)
   g.PubS = g.NAS == 2 ? 16 : 8; // batched edge warps / per-step edge in the source warps
-  const int maxg = (16 - g.NCW - g.NAS * g.NCW) / g.NG;  // warps per near group
+  g.NOW = g.NAS == 2 ? 1 : 0;   // output warp beside the edge warps
+  const int maxg = (16 - g.NCW - g.NAS * g.NCW - g.NOW) / g.NG;  // warps per near group
   // near lane-group width: SIMT runs each label's fp64 bookkeeping for the whole warp, so
   // use one lane per label unless a label has many ring terms (>= 16 per lane)
   auto near_gw = [&](int terms) {
@@ -154,7 +155,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
     g.TBlk = 0;
     g.GWn = near_gw(K > 5 ? K - 5 : 1);
     g.NNW = g.NG * ((C * g.GWn + 31) / 32);
-    g.NT = (g.NCW + g.NAS * g.NCW + g.NNW) * 32;
+    g.NT = (g.NCW + g.NAS * g.NCW + g.NNW + g.NOW) * 32;
     size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
     if (g.NNW <= g.NG * maxg && sm <= limit) {
       *out = g;
@@ -198,7 +199,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
         while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
       g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
       if (g.TBlk) g.NWt = g.CgMax * g.TWb;
-      const int head_nt = (g.NCW + g.NAS * g.NCW + g.NNW) * 32;
+      const int head_nt = (g.NCW + g.NAS * g.NCW + g.NNW + g.NOW) * 32;
       g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
       size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
       if (sm <= limit) {

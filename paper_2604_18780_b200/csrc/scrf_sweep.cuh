@@ -119,6 +119,7 @@ struct SweepGeo {
   int NG;     // near groups (2 or 4): group g owns the targets p with p % NG == g
   int PubS;   // slots of the position-indexed head rings (16: edge batches of 4, 8: per-step edge)
   int TWb;    // blocked tails: warps per label (1, or 2 taking alternate groups of 4 targets)
+  int NOW;    // output warps (1 with separate edge warps: they write Y^, X^, n, max shift)
   int GWn;    // near threads per label (power of two <= 32)
   int NWt;    // tail warps
   int WPL;    // tail warps per label (each pushes its own partial)
@@ -633,6 +634,35 @@ __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx&
   }
 }
 
+// per-position outputs (Y^, X^, n, max shift) of positions q-3 .. q from the published rings
+template <typename R>
+__device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
+                                             bool act) {
+  const int C = a.C, T = a.T;
+  {
+    const size_t rowbase = (size_t)x.b * (T + 1);
+    const int cs = act ? c : 0;
+    R* Yo = a.Y[x.dir] + rowbase * C + cs;
+    R* Xo = a.X[x.dir] + rowbase * C + cs;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int pos = q - 3 + i;
+      if (pos >= 0) {
+        const int t = x.tpos(pos);
+        const int sl = pos & 15;
+        if (act) {
+          Yo[(size_t)t * C] = h.pubY[sl * C + c];
+          Xo[(size_t)t * C] = h.pubX[sl * C + c];
+        }
+        if (c == 0) {
+          a.n[x.dir][rowbase + t] = h.nring[pos & (kNring - 1)];
+          if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
+        }
+      }
+    }
+  }
+}
+
 // One edge batch at A(q) (q % 4 == 0) for label c: (O, Q) and edge terms hk = O[u] + Q[u-k] +
 // B[k-1] (k = 1..4) of targets u = q+kLead .. q+kLead+3, the outputs Y^, X^, n, max shift of
 // positions q-3 .. q, and the register prefetch of the next batch's rows.
@@ -672,28 +702,7 @@ __device__ __forceinline__ void edge_batch(const SweepArgs<R>& a, const SweepCtx
 #pragma unroll
     for (int i = 0; i < 4; ++i) e.qh[i] = qa[4 + i];
   }
-  if (outputs) {
-    const size_t rowbase = (size_t)x.b * (T + 1);
-    const int cs = act ? c : 0;
-    R* Yo = a.Y[x.dir] + rowbase * C + cs;
-    R* Xo = a.X[x.dir] + rowbase * C + cs;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int pos = q - 3 + i;
-      if (pos >= 0) {
-        const int t = x.tpos(pos);
-        const int sl = pos & 15;
-        if (act) {
-          Yo[(size_t)t * C] = h.pubY[sl * C + c];
-          Xo[(size_t)t * C] = h.pubX[sl * C + c];
-        }
-        if (c == 0) {
-          a.n[x.dir][rowbase + t] = h.nring[pos & (kNring - 1)];
-          if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
-        }
-      }
-    }
-  }
+  if (outputs) edge_outputs<R>(a, x, h, q, c, act);
 }
 
 // log2(2^m s + sum_k 2^xk), k = 1..4
@@ -1099,8 +1108,22 @@ __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr
   edge_init(x, g, h.oq, T, C, L, cs, es);
   for (int q = 0; q <= L; q += 4) {
     nbar_sync(BAR_A + 0, NA + NAE);
-    edge_batch<R>(a, x, h, q, c, act, b2c, es, true);
+    edge_batch<R>(a, x, h, q, c, act, b2c, es, g.NOW == 0);
     if (blockIdx.x == 0 && c == 0) SCRF_GT(7, q);
+  }
+}
+
+// ======================= output warp (lane = label), NOW == 1 =======================
+// Joins A(q) for q % 4 == 0 like the edge warps and writes the outputs of positions q-3 .. q,
+// so the edge batch (on the critical path through that barrier) carries no HBM stores.
+template <typename R>
+__device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
+  const int C = a.C, L = x.L;
+  const int c = threadIdx.x - wbase * 32;
+  const bool act = c < C;
+  for (int q = 0; q <= L; q += 4) {
+    nbar_sync(BAR_A + 0, NA + NAE);
+    edge_outputs<R>(a, x, h, q, c, act);
   }
 }
 
@@ -1114,8 +1137,8 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   const int NAUX = g.NAS * g.NCW;                            // source (+ edge) warps
   const int NA = (2 * g.NCW + g.NNW / g.NG) * 32;            // chain + source + one near group
   const int NB = (g.NCW + g.NNW / g.NG) * 32;                // chain + one near group
-  const int NAE = g.NAS == 2 ? g.NCW * 32 : 0;               // edge warps (A(q), q % 4 == 0 only)
-  const int NH = (g.NCW + g.NNW + NAUX) * 32;                // all head threads
+  const int NAE = g.NAS == 2 ? (g.NCW + g.NOW) * 32 : 0;     // edge + output warps (A(q), q % 4 == 0 only)
+  const int NH = (g.NCW + g.NNW + NAUX + g.NOW) * 32;        // all head threads
   HeadPtr<R> h = head_ptrs<R>(smem, HL);
   const int kc = g.kc;
 
@@ -1180,8 +1203,10 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     head_near<R, TAILS>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
     head_src<R, TAILS>(a, x, smem, h, TL, NA, NAE, g.NCW + g.NNW, g.NAS == 1);
-  else if (warp < NH / 32)
+  else if (g.NAS == 2 && warp < 3 * g.NCW + g.NNW)
     head_edge_role<R>(a, x, h, NA, NAE, 2 * g.NCW + g.NNW);
+  else if (g.NOW && warp < NH / 32)
+    head_out_role<R>(a, x, h, NA, NAE, 3 * g.NCW + g.NNW);
 }
 
 // ----------------------------------------------------------------------------
