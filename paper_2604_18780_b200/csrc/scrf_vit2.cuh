@@ -64,7 +64,7 @@ struct V2Head {
 __host__ __device__ inline V2Head v2_head_layout(int C, const V2Geo& g, bool has_ps) {
   V2Head L;
   size_t o = 0;
-  const size_t RC = (size_t)g.R * C;
+  const size_t RC = (size_t)g.R * g.NCW * 32;  // ring columns padded to the head's lanes
   L.hg = o;   o += v2_a16(RC * 8);
   L.hs = o;   o += v2_a16(RC * 8);
   L.hS = o;   o += v2_a16(RC * 8);
@@ -209,13 +209,17 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
           arg = c0 + j;
         }
     }
-    if (act) {
+    {
+      // every lane owns a ring column (padded to NH), so inactive lanes never read another
+      // lane's slot
       const int r = t & Rm;
-      hg[r * C + c] = best;
-      hs[r * C + c] = sec;
-      ha[r * C + c] = arg;
-      hS[r * C + c] = St;
-      if (hP) hP[r * C + c] = Pst;
+      hg[r * NH + c] = best;
+      hs[r * NH + c] = sec;
+      ha[r * NH + c] = arg;
+      hS[r * NH + c] = St;
+      if (hP) hP[r * NH + c] = Pst;
+    }
+    if (act) {
       if (tails && t <= nsrc_max) {
         const uint32_t sl = (uint32_t)(t % g.KR);
         const uint32_t bar = t_bar + (uint32_t)((t & (kVSrc - 1)) * 8);
@@ -275,8 +279,8 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
 #pragma unroll
     for (int i = 0; i < NK; ++i) {
       const int r = (t - i - 1) & Rm;
-      hv[i] = v2_h(St, hS[r * C + cs], bkr[i], hP ? hP[r * C + cs] : 0.0, Pet, hps, hpe);
-      cv[i] = __dadd_rn(hg[r * C + cs], hv[i]);
+      hv[i] = v2_h(St, hS[r * NH + c], bkr[i], hP ? hP[r * NH + c] : 0.0, Pet, hps, hpe);
+      cv[i] = __dadd_rn(hg[r * NH + c], hv[i]);
     }
 #pragma unroll
     for (int i = 0; i < NK; ++i) {
@@ -292,8 +296,8 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     bool flag = false;
     if (bk > 0) {
       const int r = (t - bk) & Rm;
-      src = ha[r * C + cs];
-      const double sec = hs[r * C + cs];
+      src = ha[r * NH + c];
+      const double sec = hs[r * NH + c];
       flag = src > 0 && sec != -CUDART_INF && __dadd_rn(sec, hb) == best;
     }
     VPH(1);
