@@ -1048,7 +1048,17 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
   if (do_edge) edge_init(x, g, h.oq, T, C, L, cs, es);
   const int Lq = L & ~3;  // last position written by an edge batch
   for (int q = 0; q <= L; ++q) {
+#ifdef SCRF_TRACE
+    // source-warp phases (cluster 0, lane 0): [0] loop top, [1] after A(q), [2] ring written, [3] sends issued
+    long long* trs = (a.trace && blockIdx.x == 0 && c == 0 && q >= a.trace_from && q < a.trace_from + 256)
+                         ? a.trace + 1344 * 16 + (q - a.trace_from) * 4
+                         : nullptr;
+    if (trs) trs[0] = clock64();
+#endif
     nbar_sync(BAR_A + (q & 3), NA + ((q & 3) == 0 ? NAE : 0));
+#ifdef SCRF_TRACE
+    if (trs) trs[1] = clock64();
+#endif
     const double n_q = h.nring[q & (kNring - 1)];
     const int sl = q & (g.PubS - 1);
     if (act) {
@@ -1057,11 +1067,17 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
       R2 v;
       split2(r, v.x, v.y);
       ringc[q & KRm] = v;
+#ifdef SCRF_TRACE
+      if (trs) trs[2] = clock64();
+#endif
       if (TAILS && q <= nsend_max)
         st_async_pair<R>(t_ring + (uint32_t)((q & KTm) * 2 * sizeof(R)), v.x, v.y,
                          t_bar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
     }
     if (blockIdx.x == 0 && c == 0) SCRF_GT(0, q);
+#ifdef SCRF_TRACE
+    if (trs) trs[3] = clock64();
+#endif
 #ifdef SCRF_TRACE
     if (a.trace && blockIdx.x == 0 && c == 0 && q >= a.trace_from && q < a.trace_from + 256)
       a.trace[576 * 16 + (q - a.trace_from) * 16] = clock64();  // source q sent (head clock)

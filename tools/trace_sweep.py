@@ -24,7 +24,7 @@ prob = scrf.DeviceProblem.from_host(cum, params)
 post = len(sys.argv) > 3 and sys.argv[3] == "post"
 run = (lambda: S.device_posterior(prob)) if post else (lambda: S.device_forward(prob))
 run()
-buf = torch.zeros((1312 + 32, 16), dtype=torch.int64, device="cuda")
+buf = torch.zeros((1344 + 64, 16), dtype=torch.int64, device="cuda")
 lib = _lib.load()
 lib.scrf_debug_trace(buf.data_ptr())
 run()
@@ -201,3 +201,11 @@ for r in range(256):
 if d_start:
     print(f"tail group wait for source q=sb+3: start - sent {np.mean(d_start):.0f} ns, saw - sent {np.mean(d_saw):.0f} ns, "
           f"already complete at start {100.0 * np.mean(ready):.0f}%")
+
+ss = buf.cpu().numpy()[1344:].reshape(-1)[: 256 * 4].reshape(256, 4).astype(np.float64)
+ok = ss[:, 0] > 0
+if ok.sum() > 4:
+    it = np.diff(ss[ok, 0])
+    print("source warp (median cycles): iteration", np.median(it), "| wait at A", np.median(ss[ok, 1] - ss[ok, 0]),
+          "| A -> ring written", np.median(ss[ok, 2] - ss[ok, 1]), "| ring -> sends issued", np.median(ss[ok, 3] - ss[ok, 2]),
+          "| sends -> next loop top", np.median(ss[1:, 0][ok[1:]] - ss[:-1, 3][ok[1:]]))
