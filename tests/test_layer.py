@@ -141,3 +141,23 @@ def test_cli_decode_with_marginals(tmp_path):
     _, _, marg = S.posterior(cum, params)
     for b, L in enumerate(lengths):
         np.testing.assert_allclose(np.array(m["position_marginals"][b]), marg.position_marginals[b, :L], atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_cli_bench_csv(tmp_path):
+    """bench --format csv (cli.py:42-53, 131-200): the reference's columns first, then the
+    fwd+bwd throughput and device peak; one row per T."""
+    from paper_2604_18780_b200 import cli
+
+    out = tmp_path / "b.csv"
+    rc = cli.main(["bench", "--T", "200", "400", "--K", "20", "--C", "4", "--B", "2", "--repeats", "1",
+                   "--format", "csv", "--out", str(out)])
+    assert rc == 0
+    lines = out.read_text().strip().splitlines()
+    assert lines[0].startswith("#")
+    header = lines[1].split(",")
+    assert header[: len(cli.BENCH_COLUMNS)] == list(cli.BENCH_COLUMNS)
+    assert len(lines) == 4
+    for row in lines[2:]:
+        cells = dict(zip(header, row.split(",")))
+        assert cells["status"] == "ok" and float(cells["positions_per_sec_fwd_bwd"]) > 0
