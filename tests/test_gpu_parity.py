@@ -291,3 +291,29 @@ def test_viterbi_full_config4_matches_single_cluster_kernel(monkeypatch):
     assert [tuple(s) for s in segs_new] == [tuple(s) for s in segs_old]
     for b, s in enumerate(segs_new):
         s.validate(int(cum.lengths[b]), params.max_duration, params.num_labels)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_full_size_invariants_other_configs(cfg):
+    """Configs 3 and 5 at their full BASELINE sizes (c5: C = 128, the C^2 contraction stress):
+    alpha- and beta-side log Z agree, every valid position is covered once, gradient totals
+    equal the expected segment count, and the device Viterbi tiling is valid."""
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    c = CONFIGS[cfg]
+    S.set_precision("fp32")
+    _, params, cum = scrf.equivalence_instance(0, T=c["T"], K=c["K"], C=c["C"], B=c["B"], mode=scrf.CenteringMode.MEAN)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    fwd, bw = S.device_posterior(prob)
+    logZ = fwd.logZ.cpu().numpy()
+    zb = S.device_beta_logz(prob, fwd, bw).cpu().numpy()
+    np.testing.assert_allclose(zb, logZ, rtol=1e-6)
+    pos = bw.position_marginals.cpu().numpy()
+    assert float(np.abs(pos.sum(-1) - 1.0).max()) < 5e-5
+    cnt = bw.expected_segment_count.cpu().numpy()
+    np.testing.assert_allclose(bw.grad_B.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
+    np.testing.assert_allclose(bw.grad_T.cpu().numpy().sum(), cnt.sum(), rtol=1e-5)
+    segs, scores = scrf.decode(cum, params)
+    for b, s in enumerate(segs):
+        s.validate(int(cum.lengths[b]), params.max_duration, params.num_labels)
+    assert np.all(np.isfinite(scores))
