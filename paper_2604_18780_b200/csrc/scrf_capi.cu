@@ -172,10 +172,12 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   // allows; at most 8 tails (8 x 16 labels covers C <= 128). (Larger clusters used to hang
   // because of spare warps in tails of an uneven label split; fixed in tail_loop_blocked.)
   bool blk = env_int("SCRF_TAIL_EXACT", 0) == 0 && K >= kNear + 33 && K <= 1024 + kNear;
-  const int maxt = C < 8 ? C : 8;
+  // blocked tails: <= 8 (8 x 16 labels covers C <= 128); exact tails may need up to 15 when their
+  // K-long rings crowd shared memory (cluster of 16, non-portable size)
+  auto max_tails = [&](bool blocked) { const int m = blocked ? 8 : 15; return C < m ? C : m; };
   auto start_tails = [&](bool blocked) {
     int t = forced > 1 ? forced - 1 : (blocked ? (C + 7) / 8 : (int)(((long long)K * C + 3499) / 3500));
-    if (t > maxt) t = maxt;
+    if (t > max_tails(blocked)) t = max_tails(blocked);
     if (t < 1) t = 1;
     if (!forced)
       while (t > 1 && (long long)B * ndirs * (1 + t) > num_sms()) --t;
@@ -188,7 +190,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
       if (!blk) break;
       blk = false;
     }
-    for (int tails = start_tails(blk); tails <= maxt; ++tails) {
+    for (int tails = start_tails(blk); tails <= max_tails(blk); ++tails) {
       g.G = 1 + tails;
       g.CgMax = (C + tails - 1) / tails;
       g.WPL = 1;
