@@ -12,7 +12,7 @@ OUT = os.path.join(HERE, "libscrf.so")
 # debug build with clock64/globaltimer phase tracing compiled in (tools/trace_sweep.py)
 OUT_TRACE = os.path.join(HERE, "libscrf_trace.so")
 SOURCES = ["scrf_capi.cu"]
-DEPS = ["scrf_capi.cu", "scrf_sweep.cuh", "scrf_post.cuh", "scrf_viterbi.cu", "scrf_common.cuh",
+DEPS = ["scrf_capi.cu", "scrf_sweep.cuh", "scrf_post.cuh", "scrf_viterbi.cu", "scrf_vit2.cuh", "scrf_cut.cuh", "scrf_common.cuh",
         os.path.join("..", "..", "include", "scrf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

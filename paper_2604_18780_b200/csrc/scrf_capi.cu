@@ -10,6 +10,7 @@
 #include "../../include/scrf.h"
 #include "scrf_sweep.cuh"
 #include "scrf_post.cuh"
+#include "scrf_cut.cuh"
 #include "scrf_viterbi.cu"
 #include "scrf_vit2.cuh"
 
@@ -266,8 +267,12 @@ PostGeo post_geo(const scrf_problem* p, int prec) {
 
 // backward work buffer: beta-side messages + partials
 struct BLayout {
-  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, total;
+  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, cutU, corr, total;
 };
+
+// cut-normaliser spacing (scrf_cut.cuh): 0 disables the correction (SCRF_CUT_D=0, debugging)
+int cut_spacing() { return env_int("SCRF_CUT_D", 512); }
+int cut_slots(int64_t T, int d) { return d > 0 ? (int)((T - 1) / d) + 2 : 0; }
 BLayout b_layout(const scrf_problem* p, int prec) {
   BLayout L;
   const size_t rs = prec ? 8 : 4;
@@ -285,6 +290,9 @@ BLayout b_layout(const scrf_problem* p, int prec) {
   L.gBp = o;   o += al(B * q.nchB * K * C * 8);
   L.gTs = o;   o += al(B * C * C * 8);
   L.gBs = o;   o += al(B * K * C * 8);
+  const int d = cut_spacing();
+  L.cutU = o;  o += d > 0 ? al(B * (size_t)cut_slots(p->T, d) * C * 8) : 0;
+  L.corr = o;  o += d > 0 ? al(B * (p->T + 1) * 8) : 0;
   L.total = o;
   return L;
 }
@@ -387,7 +395,7 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   if (dirs & 1) {
     // reference bookkeeping (N, dead_at, logZ) from the stored per-position normalisers
     ++g_launches;
-    book_kernel<R><<<a.B, 1024, a.n_ckpt * sizeof(double), st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
+    book_kernel<R><<<a.B, 1024, 0, st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
                                                                a.n_ckpt, N, dead_at, logZ);
     e = cudaGetLastError();
   }
@@ -439,6 +447,40 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
   a.gBp = (double*)(wb + W.gBp);
   const int B = a.B, C = a.C, K = a.K, T = a.T;
   cudaError_t e;
+  const int cd = cut_spacing();
+  if (cd > 0) {
+    // cut normalisers, then the per-position frame correction the passes below apply
+    CutArgs<R> ca;
+    memset(&ca, 0, sizeof(ca));
+    ca.S = p->S;
+    ca.lengths = p->lengths;
+    ca.dur = p->duration_bias;
+    ca.ps = p->proj_start;
+    ca.pe = p->proj_end;
+    ca.logZ = logZ;
+    ca.B = B;
+    ca.T = T;
+    ca.K = K;
+    ca.C = C;
+    ca.Ya = a.Ya;
+    ca.Xa = a.Xa;
+    ca.Yb = a.Yb;
+    ca.Xb = a.Xb;
+    ca.na = a.na;
+    ca.nb = a.nb;
+    ca.d = cd;
+    ca.ncut = cut_slots(T, cd);
+    ca.U = (double*)(wb + W.cutU);
+    const size_t sm = cut_smem<R>(K);
+    e = cudaFuncSetAttribute(cut_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
+    ++g_launches;
+    cut_kernel<R><<<dim3(ca.ncut, (C + kCutCG - 1) / kCutCG, B), 256, sm, st>>>(ca);
+    ++g_launches;
+    cut_corr_kernel<<<dim3((T + 1 + 255) / 256, B), 256, 0, st>>>(p->lengths, T, C, cd, ca.ncut, ca.U,
+                                                                   (double*)(wb + W.corr));
+    a.corr = (const double*)(wb + W.corr);
+  }
   {
     const size_t sm = post_pos_smem<R>(C, q.CH);
     e = cudaFuncSetAttribute(post_pos_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -447,7 +489,11 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     post_pos_kernel<R><<<dim3(q.nch, B), 256, sm, st>>>(a);
     ++g_launches;
     ++g_launches;
-    post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
+    if (cd > 0 && cd % q.CH == 0)
+      cut_prefix_kernel<<<(B * C + 127) / 128, 128, 0, st>>>(p->lengths, B, C, q.nch, q.CH, cd, cut_slots(T, cd),
+                                                           (const double*)(wb + W.cutU), a.tot);
+    else
+      post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
     if (g_ev_pos) cudaEventRecord(g_ev_pos, st);
   }

@@ -21,6 +21,7 @@ constexpr double kLog2e = 1.4426950408889634;
 constexpr double kLn2 = 0.6931471805599453;
 constexpr double kNegInfRef = -1.0e9;          // reference sentinel (_numerics.py:18)
 constexpr double kGuard = kNegInfRef + 1.0;    // reference guard (_numerics.py:59-75)
+constexpr double kGuardL2 = kGuard * kLog2e;   // the guard in log2 units
 
 template <typename R>
 struct Mth;

@@ -1,0 +1,289 @@
+// Cut normalisers: exact-identity drift correction of the fp32 message sweeps (sm_100a).
+//
+// Every segmentation of [0, L) either has a boundary at t or one segment [s, e) with
+// s < t < e, so for every boundary t (Appendix A identities; the reference's
+// coverage bookkeeping, streaming.py:357-380, relies on the same fact):
+//
+//   U_t = sum_c E[t,c] + sum_c sum_{s < t < e <= s+K} mu(s, e-s, c) = 1,
+//   E[t,c] = 2^(alpha[t,c] + beta[t,c] - Z),  mu = 2^(ra[s,c] + rb[e,c] + B[e-s-1,c])   (log2 units)
+//
+// with ra = gamma - S + Ps (alpha side) and rb = beta + S + Pe - Z (beta side), as in the
+// grad_B pass (scrf_post.cuh). At t = 0 the identity is sum_c A[0,c] = 1, at t = L it is
+// sum_c E[L,c] = 1.
+//
+// The fp32 sweeps carry a slowly varying frame error eps_t (a random walk plus a small
+// per-step bias of the fp32/MUFU arithmetic, up to ~1e-4 relative at T = 1e5): every mass
+// computed at boundary t is off by the factor (1 + eps_t), and U_t measures exactly that
+// factor. The posterior passes divide the masses by U interpolated (in log space) between
+// cut points every `d` positions; the residual is the walk's excursion between two cuts.
+//
+// Cost per interior cut and label: K(K-1)/2 terms, evaluated in exp space on the FMA pipe
+// (a_s = 2^(ra[s] - Ra), b_e = 2^(rb[e] - Rb), w_k = 2^(B[k] - Bmax): 2K + K ex2, K^2/2 FMA)
+// with per-block fp64 accumulation. Terms that underflow fp32 in a factor are below
+// 2^-126 of a term bound that is itself <= 1 up to the duration-bias range: negligible.
+#pragma once
+
+#include "scrf_common.cuh"
+
+namespace scrf {
+
+constexpr int kCutSG = 8;   // sources per thread (register window over w)
+constexpr int kCutEC = 64;  // targets per work item
+constexpr int kCutCG = 4;   // labels per CTA
+
+template <typename R>
+struct CutArgs {
+  const double* S;
+  const int64_t* lengths;
+  const double* dur;
+  const double* ps;
+  const double* pe;
+  const double* logZ;  // (B,) nats
+  int B, T, K, C;
+  const R *Ya, *Xa, *Yb, *Xb;  // [B][T+1][C]
+  const double *na, *nb;       // [B][T+1]
+  int d;                       // cut spacing
+  int ncut;                    // cut slots per sequence: 0, d, 2d, ..., and L (last used slot)
+  double* U;                   // [B][ncut][C] per-label contributions to U_t
+};
+
+// cut slot j of sequence with length L: t_j = j * d for j <= J = (L - 1) / d, t_{J+1} = L
+__host__ __device__ inline int cut_count(int L, int d) { return (L - 1) / d + 2; }
+__host__ __device__ inline int cut_pos(int j, int L, int d) {
+  const int J = (L - 1) / d;
+  return j <= J ? j * d : L;
+}
+
+template <typename R>
+__host__ __device__ inline size_t cut_smem(int K) {
+  // per label: a[K + kCutSG] (sources t-K+1 .. t-1, padded), b[K + kCutEC] (targets), w[2K + 2 kCutEC]
+  return (size_t)kCutCG * ((K + kCutSG) + (K + kCutEC) + (2 * K + 2 * kCutEC)) * sizeof(float) + 64;
+}
+
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];  // fixed order
+  return s;
+}
+
+__device__ __forceinline__ double block_max_d(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = -CUDART_INF;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = fmax(s, red[i]);
+  return s;
+}
+
+// grid (cut slot j, label group, b), 256 threads
+template <typename R>
+__global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ double red[8];
+  const int j = blockIdx.x, cg = blockIdx.y, b = blockIdx.z;
+  const int C = a.C, T = a.T, K = a.K;
+  const int L = (int)a.lengths[b];
+  if (j >= cut_count(L, a.d)) return;
+  const int t = cut_pos(j, L, a.d);
+  const int c0 = cg * kCutCG;
+  const int Cn = min(kCutCG, C - c0);
+  const size_t rb0 = (size_t)b * (T + 1);
+  const double Z2 = a.logZ[b] * kLog2e;
+  const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC;
+  float* sa = (float*)sm;                  // [CG][NA]   a[s], s = t-K+1+i
+  float* sb = sa + (size_t)kCutCG * NA;    // [CG][NBv]  b[e], e = t+1+i
+  float* sw = sb + (size_t)kCutCG * NBv;   // [CG][NW]   w[k], k = i - kCutEC (k in 1..K nonzero)
+  const int s_lo = t - K + 1;
+  for (int cl = 0; cl < Cn; ++cl) {
+    const int c = c0 + cl;
+    // point term: E[t,c] (interior, t = L) or A[0,c] (t = 0), fp64
+    double pt = 0.0;
+    if (threadIdx.x == 0) {
+      const size_t o = (rb0 + t) * C + c;
+      const double f = a.na[rb0 + t] + a.nb[rb0 + t] - Z2;
+      const R y = t == 0 ? a.Xa[o] : a.Ya[o];
+      const R x = t == 0 ? a.Yb[o] : a.Xb[o];
+      if (y > Mth<R>::ninf() && x > Mth<R>::ninf()) pt = exp2(f + (double)y + (double)x);
+    }
+    double cross = 0.0;
+    if (t > 0 && t < L && K >= 2) {
+      // log2 source / target values (fp64), their maxima as references
+      double ra_max = -CUDART_INF, rb_max = -CUDART_INF, bm = -CUDART_INF;
+      for (int i = threadIdx.x; i < K - 1; i += blockDim.x) {
+        const int s = s_lo + i;
+        if (s >= 0) {
+          const size_t o = (rb0 + s) * C + c;
+          const R xa = a.Xa[o];
+          if (xa > Mth<R>::ninf()) {
+            const double ra = a.na[rb0 + s] + (double)xa - a.S[o] * kLog2e +
+                              ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
+            ra_max = fmax(ra_max, ra);
+          }
+        }
+        const int e = t + 1 + i;
+        if (e <= L) {
+          const size_t o = (rb0 + e) * C + c;
+          const R xb = a.Xb[o];
+          if (xb > Mth<R>::ninf()) {
+            const double rv = a.nb[rb0 + e] + (double)xb + a.S[o] * kLog2e +
+                              (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
+            rb_max = fmax(rb_max, rv);
+          }
+        }
+      }
+      for (int k = threadIdx.x; k < K; k += blockDim.x) bm = fmax(bm, a.dur[(size_t)k * C + c] * kLog2e);
+      ra_max = block_max_d(ra_max, red);
+      rb_max = block_max_d(rb_max, red);
+      bm = block_max_d(bm, red);
+      float* A = sa + (size_t)cl * NA;
+      float* Bv = sb + (size_t)cl * NBv;
+      float* W = sw + (size_t)cl * NW;
+      const bool live = ra_max > -CUDART_INF && rb_max > -CUDART_INF && bm > -CUDART_INF;
+      for (int i = threadIdx.x; i < NA; i += blockDim.x) {
+        const int s = s_lo + i;
+        float v = 0.f;
+        if (live && i < K - 1 && s >= 0) {
+          const size_t o = (rb0 + s) * C + c;
+          const R xa = a.Xa[o];
+          if (xa > Mth<R>::ninf()) {
+            const double ra = a.na[rb0 + s] + (double)xa - a.S[o] * kLog2e +
+                              ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
+            v = exp2f((float)(ra - ra_max));
+          }
+        }
+        A[i] = v;
+      }
+      for (int i = threadIdx.x; i < NBv; i += blockDim.x) {
+        const int e = t + 1 + i;
+        float v = 0.f;
+        if (live && i < K - 1 && e <= L) {
+          const size_t o = (rb0 + e) * C + c;
+          const R xb = a.Xb[o];
+          if (xb > Mth<R>::ninf()) {
+            const double rv = a.nb[rb0 + e] + (double)xb + a.S[o] * kLog2e +
+                              (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
+            v = exp2f((float)(rv - rb_max));
+          }
+        }
+        Bv[i] = v;
+      }
+      for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+        const int k = i - kCutEC;
+        W[i] = (live && k >= 1 && k <= K) ? exp2f((float)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : 0.f;
+      }
+      __syncthreads();
+      // sum_{s,e} a_s b_e w_{e-s}: item = (source group of kCutSG, target chunk of kCutEC)
+      const int nsg = (K - 1 + kCutSG - 1) / kCutSG;
+      const int nec = (K - 1 + kCutEC - 1) / kCutEC;
+      double acc = 0.0;
+      for (int it = threadIdx.x; it < nsg * nec; it += blockDim.x) {
+        const int g = it / nec, q = it % nec;
+        const int i0 = g * kCutSG;   // sources s = s_lo + i0 + r, r < kCutSG
+        const int e0 = q * kCutEC;   // targets e = t + 1 + e0 + u
+        // k = e - s = (t + 1 + e0 + u) - (s_lo + i0 + r) = K + e0 + u - i0 - r
+        const int kb = K + e0 - i0;  // k of (u = 0, r = 0)
+        float wv[kCutSG];
+#pragma unroll
+        for (int r = 0; r < kCutSG; ++r) wv[r] = W[kb - r + kCutEC];
+        float sr[kCutSG];
+#pragma unroll
+        for (int r = 0; r < kCutSG; ++r) sr[r] = 0.f;
+#pragma unroll 8
+        for (int u = 0; u < kCutEC; ++u) {
+          const float bv = Bv[e0 + u];
+#pragma unroll
+          for (int r = 0; r < kCutSG; ++r) sr[r] = fmaf(bv, wv[r], sr[r]);
+#pragma unroll
+          for (int r = kCutSG - 1; r > 0; --r) wv[r] = wv[r - 1];
+          wv[0] = W[kb + u + 1 + kCutEC];
+        }
+        double tot = 0.0;
+#pragma unroll
+        for (int r = 0; r < kCutSG; ++r) tot += (double)A[i0 + r] * (double)sr[r];
+        acc += tot;
+      }
+      acc = block_sum_d(acc, red);
+      if (live && acc > 0.0) cross = acc * exp2(ra_max + rb_max + bm);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.U[((size_t)b * a.ncut + j) * C + c] = pt + cross;
+  }
+}
+
+// log2 correction of boundary t: -lerp_j(log2 U_j) with U summed over labels in fixed order;
+// 0 when the cut totals are not sane (|log2 U| > 1e-2: nothing to correct reliably)
+__device__ __forceinline__ double cut_log2U(const double* U, int C) {
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s += U[c];
+  const double l = s > 0.0 ? log2(s) : 0.0;
+  return fabs(l) <= 1e-2 ? l : 0.0;
+}
+
+}  // namespace scrf
+
+namespace scrf {
+
+// per-position log2 correction corr[b][t] = -lerp(log2 U) between the enclosing cut slots
+// (0 past L); grid (chunks of 256 positions, B)
+__global__ void __launch_bounds__(256) cut_corr_kernel(const int64_t* lengths, int T, int C, int d, int ncut,
+                                                       const double* U, double* corr) {
+  const int b = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  const int L = (int)lengths[b];
+  double v = 0.0;
+  if (t <= L) {
+    const int J = (L - 1) / d;
+    const int j = t >= J * d ? J : t / d;
+    const int t0 = cut_pos(j, L, d), t1 = cut_pos(j + 1, L, d);
+    const double* Ub = U + (size_t)b * ncut * C;
+    const double l0 = cut_log2U(Ub + (size_t)j * C, C);
+    const double l1 = cut_log2U(Ub + (size_t)(j + 1) * C, C);
+    const double f = t1 > t0 ? (double)(t - t0) / (double)(t1 - t0) : 0.0;
+    v = -(l0 + (l1 - l0) * f);
+  }
+  corr[(size_t)b * (T + 1) + t] = v;
+}
+
+}  // namespace scrf
+
+namespace scrf {
+
+// Exclusive prefix of the coverage chunk totals, re-anchored at every interior cut point:
+// the coverage of cell t_j - 1 is exactly E[t_j,c] + (segments of label c crossing t_j), the
+// per-label cut contribution U[b][j][c] (divided by the cut total, the frame correction at
+// t_j), so the running sum restarts there and fp32 rounding accumulates over <= d positions
+// only. Chunk starts coincide with cut points (CH divides d). One thread per (b, c).
+__global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch, int CH, int d, int ncut,
+                                  const double* U, double* tot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * C) return;
+  const int b = i / C, c = i % C;
+  const int L = (int)lengths[b];
+  const int J = (L - 1) / d;
+  const double* Ub = U + (size_t)b * ncut * C;
+  double* base = tot + (size_t)b * nch * C + c;
+  double run = 0.0;
+  for (int q = 0; q < nch; ++q) {
+    const int t0 = q * CH;
+    if (t0 > 0 && t0 % d == 0 && t0 / d <= J) {
+      const int j = t0 / d;
+      double s = 0.0;
+      for (int cc = 0; cc < C; ++cc) s += Ub[(size_t)j * C + cc];
+      const double l = s > 0.0 ? log2(s) : 1.0;
+      if (fabs(l) <= 1e-2) run = Ub[(size_t)j * C + c] / s;
+    }
+    const double v = base[(size_t)q * C];
+    base[(size_t)q * C] = run;
+    run += v;
+  }
+}
+
+}  // namespace scrf

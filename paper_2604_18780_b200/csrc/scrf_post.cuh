@@ -29,6 +29,7 @@ struct PostArgs {
   int B, T, K, C;
   const R *Ya, *Xa, *Yb, *Xb;  // [B][T+1][C]
   const double *na, *nb;       // [B][T+1]
+  const double* corr;          // [B][T+1] log2 frame correction from the cut normalisers (scrf_cut.cuh) or null
   // outputs
   double* grad_S;  // (B, T+1, C)
   double* grad_Ps; // (B, T, C) or null
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
   const size_t rb = (size_t)b * (T + 1);
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
     const int t = t0 + i;
-    sf[i] = (t <= L) ? a.na[rb + t] + a.nb[rb + t] - Z2 : 0.0;
+    sf[i] = (t <= L) ? a.na[rb + t] + a.nb[rb + t] - Z2 + (a.corr ? a.corr[rb + t] : 0.0) : 0.0;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < nt * C; e += blockDim.x) {
@@ -267,7 +268,8 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       if (u <= L && ui < kGBSub + K) {
         const size_t o = (rb0 + u) * C + c;
         const double rv = a.nb[rb0 + u] + (double)a.Xb[o] + a.S[o] * kLog2e +
-                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
+                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2 +
+                          (a.corr ? a.corr[rb0 + u] : 0.0);
         split2(rv, v.x, v.y);
       }
       sbv[(size_t)cl * rowU + gb_skew(ui)] = v;

@@ -853,6 +853,8 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   nbar_arrive(BAR_A + 0, NA + NAE);
   R a1 = 0, a2 = 0, a3 = 0;  // frame shifts amax_{p-1}, amax_{p-2}, amax_{p-3}
   double n_prev = 0.0;
+  double n_ref = 0.0;  // alpha: checkpoint normaliser in effect (log2); beta: 0 (absolute frame)
+  int ck_cnt = 0;
   const int cs = act ? c : 0;
   const R2* partc = h.part + cs;
   const typename Vec4<R>::T* hhc = h.hh + cs;
@@ -875,14 +877,21 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     }
     if (tr) tr[1] = clock64();
     const R am = chain_max(y);
-    const bool dead = (am == Mth<R>::ninf());
+    // the reference's guard (_numerics.py:59-75): a position whose every message is at or below
+    // NEG_INF + 1 in the reference frame (alpha: relative to the checkpoint normaliser in effect,
+    // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
+    const bool dead = (am == Mth<R>::ninf()) || (n_prev + (double)am) - n_ref <= kGuardL2;
     const R yh = dead ? Mth<R>::ninf() : y - am;
     const double n_p = dead ? n_prev : n_prev + (double)am;
     // everything but X^[p] is published before the GEMV so those stores overlap it
     if (act) h.pubY[(p & pubm) * C + c] = yh;
     if (tid == 0) {
-      h.pubA[p & pubm] = am;
+      h.pubA[p & pubm] = dead ? Mth<R>::ninf() : am;
       h.nring[p & (kNring - 1)] = n_p;
+    }
+    if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
+      ck_cnt = 0;
+      if (!dead) n_ref = n_p;
     }
     const R xh = gemv(yh);
     if (tr) tr[2] = clock64();
@@ -1697,12 +1706,11 @@ __global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* n
   const int b = blockIdx.x;
   const int L = (int)lengths[b];
   const size_t rb = (size_t)b * (T + 1);
-  extern __shared__ double Ns[];  // [n_ckpt] running N in effect from checkpoint i on
+  double* Nb = N + (size_t)b * n_ckpt;  // running N in effect from checkpoint i on (global: any n_ckpt)
   __shared__ int dmin;
   if (threadIdx.x == 0) {
     double N_cur = 0.0;
-    Ns[0] = 0.0;
-    N[(size_t)b * n_ckpt] = 0.0;
+    Nb[0] = 0.0;
     for (int i = 1; i < n_ckpt; ++i) {
       const long long q = (long long)i * delta;
       if (q <= L) {
@@ -1710,21 +1718,16 @@ __global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* n
         const double amax_abs = (am == Mth<R>::ninf()) ? -CUDART_INF : na[rb + q] * kLn2;
         if (amax_abs - N_cur > kGuard) N_cur = amax_abs;
       }
-      Ns[i] = N_cur;
-      N[(size_t)b * n_ckpt + i] = N_cur;
+      Nb[i] = N_cur;
     }
     dmin = 0x7fffffff;
   }
   __syncthreads();
-  // dead check at q uses the N in effect before the shift at q: checkpoint floor((q-1)/delta)
+  // first dead position (streaming.py:198-200): every message at or below the guard; the chain
+  // marks those positions with a max shift of -inf
   int best = 0x7fffffff;
-  for (int q = 1 + threadIdx.x; q <= L; q += blockDim.x) {
-    const R am = amx[rb + q];
-    const double amax_abs = (am == Mth<R>::ninf()) ? -CUDART_INF : na[rb + q] * kLn2;
-    int i = (q - 1) / delta;
-    if (i >= n_ckpt) i = n_ckpt - 1;
-    if (!(amax_abs - Ns[i] > kGuard)) best = min(best, q);
-  }
+  for (int q = 1 + threadIdx.x; q <= L; q += blockDim.x)
+    if (amx[rb + q] == Mth<R>::ninf()) best = min(best, q);
   atomicMin(&dmin, best);
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -1743,9 +1746,11 @@ __global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* n
       const bool deadL = (amL == Mth<R>::ninf()) || !any;
       const double lz = deadL ? -CUDART_INF : (na[rb + L] + (double)Mth<R>::lg2(s)) * kLn2;
       logZ[b] = lz;
-      int da = dmin == 0x7fffffff ? -1 : dmin;
-      const double Nfin = Ns[n_ckpt - 1 < (L / delta) ? n_ckpt - 1 : (L / delta)];
-      if (da < 0 && !(lz - Nfin > kGuard)) da = L;
+      // the reference raises only when the final log-partition is at or below the guard
+      // (streaming.py:216-225), naming the first dead position, else L
+      const double Nfin = Nb[n_ckpt - 1 < (L / delta) ? n_ckpt - 1 : (L / delta)];
+      int da = -1;
+      if (!(lz - Nfin > kGuard)) da = dmin == 0x7fffffff ? L : dmin;
       dead_at[b] = da;
     }
   }

@@ -148,11 +148,37 @@ class DeviceProblem:
         return cls(put(cum.S), put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
                    put(params.duration_bias), put(cum.proj_start), put(cum.proj_end))
 
-    def c_struct(self) -> _lib.ScrfProblem:
-        for name in ("S", "lengths", "transition", "duration_bias", "proj_start", "proj_end"):
+    def validate(self) -> None:
+        """Shape / dtype / device contract of the C ABI (include/scrf.h): fp64 scores and
+        parameters, int64 lengths with 1 <= L_b <= T (potentials.py:79-80; checked on the device
+        without a host sync)."""
+        S = self.S
+        if S.dim() != 3:
+            raise ValueError(f"S must be (B, T+1, C), got shape {tuple(S.shape)}")
+        B, T1, C = S.shape
+        K = self.duration_bias.shape[0] if self.duration_bias.dim() == 2 else -1
+        want = {"S": (B, T1, C), "lengths": (B,), "transition": (C, C), "duration_bias": (K, C),
+                "proj_start": (B, T1 - 1, C), "proj_end": (B, T1 - 1, C)}
+        for name, shape in want.items():
             t = getattr(self, name)
-            if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            if t is None:
+                continue
+            if not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous CUDA tensor")
+            if t.device != S.device:
+                raise ValueError(f"{name} is on {t.device}, S on {S.device}")
+            dt = torch.int64 if name == "lengths" else torch.float64
+            if t.dtype != dt:
+                raise ValueError(f"{name} must be {dt}, got {t.dtype}")
+            if tuple(t.shape) != shape or K < 1:
+                raise ValueError(f"{name} must be shaped {shape}, got {tuple(t.shape)}")
+        if T1 < 2:
+            raise ValueError("S needs at least one position (T >= 1)")
+        L = self.lengths
+        torch._assert_async(((L >= 1) & (L <= T1 - 1)).all(), "lengths must lie in [1, T]")
+
+    def c_struct(self) -> _lib.ScrfProblem:
+        self.validate()
         return _lib.ScrfProblem(
             _lib.ptr(self.S), _lib.ptr(self.lengths), _lib.ptr(self.transition), _lib.ptr(self.duration_bias),
             _lib.ptr(self.proj_start), _lib.ptr(self.proj_end), self.B, self.T, self.K, self.C,
