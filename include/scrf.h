@@ -119,6 +119,14 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
 int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
                             const double* N, double* omega, void* stream);
 
+/* Clamp-event count per sequence (B,) int32 after scrf_forward (ckpt) and optionally
+ * scrf_backward / scrf_posterior (work, or NULL): positions whose max alpha message relative
+ * to the checkpoint normaliser, or max (unnormalised) beta message, leaves +-1e6 -- where the
+ * reference's clamp_log (_numerics.py:41-56) would clip. The kernels do not clip (exact fp64
+ * normalisers); callers reject inputs with a non-zero count (ClampSemanticsError). */
+int scrf_clamp_events(const scrf_problem* p, int precision, const void* ckpt, const void* work,
+                      int32_t* events, void* stream);
+
 /* Number of kernel launches issued by the last call on this thread (for the
  * benchmark's gpu_launches claim). */
 int scrf_last_launch_count(void);

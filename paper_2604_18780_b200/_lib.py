@@ -65,6 +65,7 @@ _SIGS = {
     "scrf_viterbi_work_bytes": (_int, [_P, _psz]),
     "scrf_viterbi": (_int, [_P, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "scrf_export_checkpoints": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
+    "scrf_clamp_events": (_int, [_P, _int, _vp, _vp, _vp, _vp]),
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
     "scrf_position_outputs_event": (None, [_vp]),

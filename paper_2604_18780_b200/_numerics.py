@@ -23,10 +23,18 @@ LN2 = 0.6931471805599453
 
 @dataclass
 class ClampStats:
-    """Counter kept for API compatibility (`_numerics.py:26-38`).
+    """Clamp-event counter (`_numerics.py:26-38`).
 
-    The device kernels never clamp finite intermediates (they carry a per-position
-    fp64 normaliser instead), so this counter stays at zero.
+    The reference clips finite log-domain intermediates to +-CLAMP_LIMIT
+    (`clamp_log`, `_numerics.py:41-56`), which changes its results once a message
+    or a duration score leaves that range (e.g. alpha at T >~ 3e5 with
+    delta = T, or a "soft mask" duration bias of -5e8). The device kernels carry
+    exact fp64 normalisers instead and do NOT reproduce that clipping: they count
+    the positions where the reference would clip (alpha: max message relative to
+    the checkpoint normaliser; beta: the unnormalised max message; edge scores: a
+    device bound on |S[t]-S[t-k] + B + P|) and the API raises `ClampSemanticsError`
+    whenever that count is non-zero, instead of silently returning a different
+    answer. On well-scaled inputs the count is 0, as in the reference.
     """
 
     events: int = 0
@@ -44,3 +52,7 @@ class RunStats:
     @property
     def clamp_events(self) -> int:
         return self.clamp.events
+
+
+class ClampSemanticsError(ValueError):
+    """Raised when the reference would have clipped an intermediate to +-CLAMP_LIMIT."""

@@ -218,7 +218,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
 
 // forward state ("checkpoint buffer"): per-position alpha-side messages
 struct FLayout {
-  size_t Y, X, n, amx, total;
+  size_t Y, X, n, amx, clamp, total;
 };
 FLayout f_layout(const scrf_problem* p, int prec) {
   FLayout L;
@@ -233,6 +233,8 @@ FLayout f_layout(const scrf_problem* p, int prec) {
   o += al(npos * 8);
   L.amx = o;
   o += al(npos * rs);
+  L.clamp = o;
+  o += al(p->B * 4);
   L.total = o;
   return L;
 }
@@ -267,7 +269,7 @@ PostGeo post_geo(const scrf_problem* p, int prec) {
 
 // backward work buffer: beta-side messages + partials
 struct BLayout {
-  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, cutU, corr, total;
+  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, cutU, corr, clamp, total;
 };
 
 // cut-normaliser spacing (scrf_cut.cuh): 0 disables the correction (SCRF_CUT_D=0, debugging)
@@ -293,6 +295,7 @@ BLayout b_layout(const scrf_problem* p, int prec) {
   const int d = cut_spacing();
   L.cutU = o;  o += d > 0 ? al(B * (size_t)cut_slots(p->T, d) * C * 8) : 0;
   L.corr = o;  o += d > 0 ? al(B * (p->T + 1) * 8) : 0;
+  L.clamp = o; o += al(B * 4);
   L.total = o;
   return L;
 }
@@ -358,6 +361,7 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   a.X[0] = (R*)(fb + F.X);
   a.n[0] = (double*)(fb + F.n);
   a.amx = (R*)(fb + F.amx);
+  a.clamp = (dirs & 1) ? (int32_t*)(fb + F.clamp) : nullptr;
   if (work) {
     const BLayout W = b_layout(p, sizeof(R) == 8);
     unsigned char* wb = (unsigned char*)work;
@@ -476,10 +480,16 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
     cut_kernel<R><<<dim3(ca.ncut, (C + kCutCG - 1) / kCutCG, B), 256, sm, st>>>(ca);
-    ++g_launches;
-    cut_corr_kernel<<<dim3((T + 1 + 255) / 256, B), 256, 0, st>>>(p->lengths, T, C, cd, ca.ncut, ca.U,
-                                                                   (double*)(wb + W.corr));
     a.corr = (const double*)(wb + W.corr);
+  }
+  {
+    // per-position frame correction (when enabled) and the beta-side clamp-event count
+    e = cudaMemsetAsync(wb + W.clamp, 0, (size_t)B * 4, st);
+    if (e != cudaSuccess) return (int)e;
+    ++g_launches;
+    cut_corr_kernel<R><<<dim3((T + 1 + 255) / 256, B), 256, 0, st>>>(
+        p->lengths, T, C, cd, cd > 0 ? cut_slots(T, cd) : 0, cd > 0 ? (const double*)(wb + W.cutU) : nullptr,
+        cd > 0 ? (double*)(wb + W.corr) : nullptr, a.Xb, a.nb, (int32_t*)(wb + W.clamp));
   }
   {
     const size_t sm = post_pos_smem<R>(C, q.CH);
@@ -545,6 +555,10 @@ __global__ void export_kernel(const R* Ya, const double* na, const double* N, co
   }
   const double v = (na[o] + (double)y) * kLn2 - N[(size_t)b * nck + ck];
   omega[i] = v <= kGuard ? kNegInfRef : v;
+}
+__global__ void clamp_sum_kernel(int B, const int32_t* a, const int32_t* b, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) out[i] = a[i] + (b ? b[i] : 0);
 }
 }  // namespace
 
@@ -821,6 +835,20 @@ int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision,
     export_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)(base + F.Y), (const double*)(base + F.n), N,
                                                                  p->lengths, (int)p->B, (int)p->T, nck, (int)p->K,
                                                                  (int)p->C, (int)delta, omega);
+  return (int)cudaGetLastError();
+}
+
+int scrf_clamp_events(const scrf_problem* p, int precision, const void* ckpt, const void* work, int32_t* events,
+                      void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (!ckpt || !events) return SCRF_ENULL;
+  const FLayout F = f_layout(p, precision);
+  cudaStream_t st = (cudaStream_t)stream;
+  ++g_launches;
+  clamp_sum_kernel<<<(unsigned)((p->B + 127) / 128), 128, 0, st>>>(
+      (int)p->B, (const int32_t*)((const unsigned char*)ckpt + F.clamp),
+      work ? (const int32_t*)((const unsigned char*)work + b_layout(p, precision).clamp) : nullptr, events);
   return (int)cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ constexpr double kLn2 = 0.6931471805599453;
 constexpr double kNegInfRef = -1.0e9;          // reference sentinel (_numerics.py:18)
 constexpr double kGuard = kNegInfRef + 1.0;    // reference guard (_numerics.py:59-75)
 constexpr double kGuardL2 = kGuard * kLog2e;   // the guard in log2 units
+constexpr double kClampLimit = 1.0e6;          // reference CLAMP_LIMIT (_numerics.py:23)
 
 template <typename R>
 struct Mth;

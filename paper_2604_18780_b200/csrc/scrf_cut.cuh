@@ -232,14 +232,24 @@ namespace scrf {
 
 // per-position log2 correction corr[b][t] = -lerp(log2 U) between the enclosing cut slots
 // (0 past L); grid (chunks of 256 positions, B)
+// Also counts the beta positions whose (absolute, unnormalised in the reference) message
+// max leaves +-CLAMP_LIMIT (the reference would clamp them, _numerics.py:41-56).
+template <typename R>
 __global__ void __launch_bounds__(256) cut_corr_kernel(const int64_t* lengths, int T, int C, int d, int ncut,
-                                                       const double* U, double* corr) {
+                                                       const double* U, double* corr, const R* Xb, const double* nb,
+                                                       int32_t* clampB) {
   const int b = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > T) return;
   const int L = (int)lengths[b];
+  const size_t rt = (size_t)b * (T + 1) + t;
+  if (clampB && t < L) {
+    R m = Mth<R>::ninf();
+    for (int c = 0; c < C; ++c) m = fmax(m, Xb[rt * C + c]);
+    if (m > Mth<R>::ninf() && fabs((nb[rt] + (double)m) * kLn2) > kClampLimit) atomicAdd(&clampB[b], 1);
+  }
   double v = 0.0;
-  if (t <= L) {
+  if (d > 0 && t <= L) {
     const int J = (L - 1) / d;
     const int j = t >= J * d ? J : t / d;
     const int t0 = cut_pos(j, L, d), t1 = cut_pos(j + 1, L, d);
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(256) cut_corr_kernel(const int64_t* lengths, i
     const double f = t1 > t0 ? (double)(t - t0) / (double)(t1 - t0) : 0.0;
     v = -(l0 + (l1 - l0) * f);
   }
-  corr[(size_t)b * (T + 1) + t] = v;
+  if (corr) corr[(size_t)b * (T + 1) + t] = v;
 }
 
 }  // namespace scrf

@@ -150,6 +150,7 @@ struct SweepArgs {
   double* logZ;      // [B] nats (alpha)
   double* logZb;     // [B] nats (beta: LSE_c beta[0,c], consistency value)
   int32_t* dead_at;  // [B]
+  int32_t* clamp;    // [B] alpha positions whose max message leaves the reference's +-CLAMP_LIMIT (or null)
   double* N;         // [B][n_ckpt] reference checkpoint normalisers
   int delta, n_ckpt;
   long long* trace;  // debug: [256][16] clock64 stamps of cluster 0 (chain lane 0: 0..7, near thread 0: 8..15)
@@ -855,6 +856,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   double n_prev = 0.0;
   double n_ref = 0.0;  // alpha: checkpoint normaliser in effect (log2); beta: 0 (absolute frame)
   int ck_cnt = 0;
+  int n_clamp = 0;
   const int cs = act ? c : 0;
   const R2* partc = h.part + cs;
   const typename Vec4<R>::T* hhc = h.hh + cs;
@@ -889,6 +891,9 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       h.pubA[p & pubm] = dead ? Mth<R>::ninf() : am;
       h.nring[p & (kNring - 1)] = n_p;
     }
+    // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
+    // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
+    if (x.dir == 0 && !dead && fabs((n_p - n_ref) * kLn2) > kClampLimit) ++n_clamp;
     if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
       ck_cnt = 0;
       if (!dead) n_ref = n_p;
@@ -908,6 +913,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     a1 = dead ? (R)0 : am;
     n_prev = n_p;
   }
+  if (x.dir == 0 && tid == 0 && a.clamp) a.clamp[x.b] = n_clamp;
 }
 
 // ======================= near warps =======================

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._numerics import LN2, NEG_INF, RunStats
+from ._numerics import CLAMP_LIMIT, LN2, NEG_INF, ClampSemanticsError, RunStats
 from .accounting import MemoryLedger
 from .diagnostics import GradientSet, MarginalSet
 from .potentials import CumulativeScores, Segmentation, SemiCRFParams
@@ -148,6 +148,11 @@ class DeviceProblem:
         return cls(put(cum.S), put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
                    put(params.duration_bias), put(cum.proj_start), put(cum.proj_end))
 
+    def _signature(self):
+        return tuple(None if t is None else (t.data_ptr(), t._version, tuple(t.shape), t.dtype)
+                     for t in (self.S, self.lengths, self.transition, self.duration_bias, self.proj_start,
+                               self.proj_end))
+
     def validate(self) -> None:
         """Shape / dtype / device contract of the C ABI (include/scrf.h): fp64 scores and
         parameters, int64 lengths with 1 <= L_b <= T (potentials.py:79-80; checked on the device
@@ -178,7 +183,9 @@ class DeviceProblem:
         torch._assert_async(((L >= 1) & (L <= T1 - 1)).all(), "lengths must lie in [1, T]")
 
     def c_struct(self) -> _lib.ScrfProblem:
-        self.validate()
+        if getattr(self, "_checked", None) != self._signature():
+            self.validate()
+            self._checked = self._signature()
         return _lib.ScrfProblem(
             _lib.ptr(self.S), _lib.ptr(self.lengths), _lib.ptr(self.transition), _lib.ptr(self.duration_bias),
             _lib.ptr(self.proj_start), _lib.ptr(self.proj_end), self.B, self.T, self.K, self.C,
@@ -400,6 +407,48 @@ def _check_labels(cum: CumulativeScores, params: SemiCRFParams) -> None:
         raise ValueError(f"label count mismatch: scores have {cum.num_labels}, params {params.num_labels}")
 
 
+def device_clamp_events(prob: DeviceProblem, fwd: DeviceForward, bw: "DeviceBackward | None" = None) -> torch.Tensor:
+    """(B,) int32: positions where the reference would clip a message to +-CLAMP_LIMIT
+    (alpha from the forward, plus beta when `bw` is given); no host sync."""
+    lib = _lib.load()
+    out = torch.empty(prob.B, dtype=torch.int32, device=prob.S.device)
+    rc = lib.scrf_clamp_events(prob.c_struct(), PRECISIONS[fwd.precision], _lib.ptr(fwd.ckpt),
+                               None if bw is None else _lib.ptr(bw.work), _lib.ptr(out), _lib.stream_handle())
+    _lib.check(rc, "scrf_clamp_events")
+    return out
+
+
+def edge_score_bound(prob: DeviceProblem) -> torch.Tensor:
+    """Device upper bound of |h| = |S[t]-S[t-k] + B[k-1] (+ Ps + Pe)| over unmasked terms
+    (|S[t]-S[t-k]| <= k max|S[t]-S[t-1]|); the reference clips h beyond CLAMP_LIMIT."""
+    K = prob.K
+    S = prob.S
+    step = (S[:, 1:] - S[:, :-1]).abs().amax() if S.shape[1] > 1 else S.new_zeros(())
+    db = prob.duration_bias
+    live = db > NEG_INF + 1.0
+    bmax = torch.where(live, db.abs(), torch.zeros_like(db)).amax()
+    bound = K * step + bmax
+    for P in (prob.proj_start, prob.proj_end):
+        if P is not None:
+            bound = bound + P.abs().amax()
+    return bound
+
+
+def _check_clamp(prob: DeviceProblem, fwd: DeviceForward, bw=None, stats: RunStats | None = None) -> None:
+    n = int(device_clamp_events(prob, fwd, bw).sum().item())
+    if float(edge_score_bound(prob).item()) > CLAMP_LIMIT:
+        n += 1
+    if stats is not None:
+        stats.clamp.add(n)
+    if n:
+        raise ClampSemanticsError(
+            f"{n} position(s) would be clipped to +-{CLAMP_LIMIT:g} by the reference's clamp_log "
+            "(_numerics.py:41-56); the device kernels carry exact normalisers and do not reproduce "
+            "that clipping, so the results would differ -- use a smaller checkpoint interval or "
+            "rescale the potentials"
+        )
+
+
 def _raise_if_dead(fwd: DeviceForward) -> None:
     dead = fwd.dead_at.cpu().numpy()
     bad = np.nonzero(dead >= 0)[0]
@@ -421,6 +470,7 @@ def streaming_forward(cum: CumulativeScores, params: SemiCRFParams, delta: int |
     prob = DeviceProblem.from_host(cum, params)
     fwd = device_forward(prob, delta)
     _raise_if_dead(fwd)
+    _check_clamp(prob, fwd, None, stats)
     if ledger is not None:
         ledger.record("checkpoints", fwd.ckpt)
     return fwd.logZ.cpu().numpy(), CheckpointSet(prob, fwd)
@@ -455,6 +505,7 @@ def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts
     fwd_used = DeviceForward(logZ_t, fwd.N, fwd.dead_at, fwd.ckpt, fwd.delta, fwd.precision)
     up_t = None if up is None else torch.as_tensor(up, device=prob.S.device)
     bw = device_backward(prob, fwd_used, up_t)
+    _check_clamp(prob, fwd, bw, stats)
     if ledger is not None:
         ledger.record("workspace", bw.work)
     return _grads_to_host(bw), _marg_to_host(bw, cum)
@@ -567,6 +618,7 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         early = _to_host_async(bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals,
                                bw.boundary_posterior)
     _raise_if_dead(fwd)
+    _check_clamp(prob, fwd, bw, stats)
     if ledger is not None:
         ledger.record("checkpoints", fwd.ckpt)
         ledger.record("workspace", bw.work)
