@@ -218,7 +218,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
 
 // forward state ("checkpoint buffer"): per-position alpha-side messages
 struct FLayout {
-  size_t Y, X, n, amx, clamp, total;
+  size_t Y, X, n, clamp, total;
 };
 FLayout f_layout(const scrf_problem* p, int prec) {
   FLayout L;
@@ -231,8 +231,6 @@ FLayout f_layout(const scrf_problem* p, int prec) {
   o += al(npos * p->C * rs);
   L.n = o;
   o += al(npos * 8);
-  L.amx = o;
-  o += al(npos * rs);
   L.clamp = o;
   o += al(p->B * 4);
   L.total = o;
@@ -360,7 +358,6 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   a.Y[0] = (R*)(fb + F.Y);
   a.X[0] = (R*)(fb + F.X);
   a.n[0] = (double*)(fb + F.n);
-  a.amx = (R*)(fb + F.amx);
   a.clamp = (dirs & 1) ? (int32_t*)(fb + F.clamp) : nullptr;
   if (work) {
     const BLayout W = b_layout(p, sizeof(R) == 8);
@@ -395,14 +392,6 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
     e = launch_cl(sweep_kernel<R, false, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
   else
     e = launch_cl(sweep_kernel<R, false, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
-  if (e != cudaSuccess) return (int)e;
-  if (dirs & 1) {
-    // reference bookkeeping (N, dead_at, logZ) from the stored per-position normalisers
-    ++g_launches;
-    book_kernel<R><<<a.B, 1024, 0, st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta,
-                                                               a.n_ckpt, N, dead_at, logZ);
-    e = cudaGetLastError();
-  }
   return (int)e;
 }
 

@@ -131,6 +131,19 @@ struct SweepGeo {
   int Msm;    // exp-space transition matrix staged in shared memory
 };
 
+// One window replay (sublinear-memory mode, streaming.py:232-261 recompute_alpha and its beta
+// twin): a sweep over local positions p = 0 .. steps with absolute position t = t0 + p (alpha)
+// or t0 - p (beta), whose first `nforce` positions are forced to the stored messages
+// (Y^ and n rows fY/fN from frow on) instead of being computed; outputs go to window rows
+// out_row + (t - t_lo).
+struct SweepTask {
+  int b, dir, t0, steps, nforce, t_lo;
+  int fstep;      // forced row of local position p: frow + fstep * p
+  long long frow, out_row;
+  int ck_phase;   // alpha: t0 % delta (checkpoint counter at local position 0)
+  double n_ref;   // alpha: checkpoint normaliser in effect after t0 (log2 units)
+};
+
 template <typename R>
 struct SweepArgs {
   const double* S;
@@ -146,13 +159,22 @@ struct SweepArgs {
   R* Y[2];
   R* X[2];
   double* n[2];
-  R* amx;            // [B][T+1] per-position max shift of the alpha sweep (-inf: dead position)
   double* logZ;      // [B] nats (alpha)
   double* logZb;     // [B] nats (beta: LSE_c beta[0,c], consistency value)
   int32_t* dead_at;  // [B]
   int32_t* clamp;    // [B] alpha positions whose max message leaves the reference's +-CLAMP_LIMIT (or null)
   double* N;         // [B][n_ckpt] reference checkpoint normalisers
   int delta, n_ckpt;
+  // storage mode of the per-position outputs Y^, X^, n:
+  //   0 = every position at row b*(T+1) + t (full mode, linear memory);
+  //   1 = checkpoint rows only (sublinear mode, pass 1): alpha rows of the last mA positions of
+  //       every delta-period (+ t = 0), beta rows of [jW, t_top(j)] for every interior window
+  //       boundary jW (ck_row_* below); Y^ and n only
+  int store;
+  int mA, W, nW;            // store == 1 geometry
+  const SweepTask* tasks;   // replay mode (one task per cluster) or null
+  const R* fY[2];           // forced Y^ rows of the replay tasks
+  const double* fN[2];      // forced n rows
   long long* trace;  // debug: [256][16] clock64 stamps of cluster 0 (chain lane 0: 0..7, near thread 0: 8..15)
   int trace_from;    // first traced position
   int* hang;         // debug: watchdog record {block, thread, site, index} (first writer wins), or null
@@ -435,12 +457,37 @@ __device__ __forceinline__ void ring_lse(const typename Vec2<R>::T* rg, int mask
 // per-sweep context
 
 struct SweepCtx {
-  int b, dir, L, rank;
+  int b, dir, L, rank;  // L: local steps (positions 0 .. L)
+  int t0;               // absolute position of local position 0 (alpha: 0, beta: L_b in full sweeps)
+  int Lb;               // true length of sequence b
   const double* S;   // row base of sequence b: S + b*(T+1)*C
   const double* ps;  // proj_start rows of b or null
   const double* pe;
-  __device__ __forceinline__ int tpos(int p) const { return dir == 0 ? p : L - p; }
+  const SweepTask* task;  // replay task or null
+  __device__ __forceinline__ int tpos(int p) const { return dir == 0 ? t0 + p : t0 - p; }
 };
+
+// checkpoint rows (store == 1). Alpha: t = 0 -> row 0; else period i = ceil(t / delta),
+// e = i*delta - t, stored iff e < mA at row 1 + (i-1)*mA + (mA-1-e). Beta: boundary j =
+// floor(t / W) >= 1 with jW < L, stored iff t <= t_top(j) at row (j-1)*(K+32) + t - jW.
+__host__ __device__ inline int ck_ttop(int j, int W, int K, int L) {
+  const int need = j * W + K - 1;
+  return need >= L ? L : L - 32 * ((L - need) / 32);
+}
+__host__ __device__ inline long long ck_rows_alpha(int T, int delta, int mA) {
+  return 1 + (long long)((T + delta - 1) / delta) * mA;
+}
+__device__ __forceinline__ long long ck_row(int dir, int t, int L, int K, int delta, int mA, int W) {
+  if (dir == 0) {
+    if (t == 0) return 0;
+    const int i = (t + delta - 1) / delta;
+    const int e = i * delta - t;
+    return e < mA ? 1 + (long long)(i - 1) * mA + (mA - 1 - e) : -1;
+  }
+  const int j = t / W;
+  if (j < 1 || j * W >= L || t > ck_ttop(j, W, K, L)) return -1;
+  return (long long)(j - 1) * (K + 32) + (t - j * W);
+}
 
 // ----------------------------------------------------------------------------
 // head CTA
@@ -581,6 +628,29 @@ __device__ __forceinline__ double2 oq_rows(const SweepCtx& x, const SweepGeo& g,
   return x.dir == 0 ? make_double2(s + pev, -s + psv) : make_double2(-s + psv, s + pev);
 }
 
+// row of the per-position outputs of absolute position t, or -1 when it is not stored
+template <typename R>
+__device__ __forceinline__ long long out_row(const SweepArgs<R>& a, const SweepCtx& x, int t) {
+  if (x.task) return x.task->out_row + (t - x.task->t_lo);
+  if (a.store == 0) return (long long)x.b * (a.T + 1) + t;
+  const long long r = ck_row(x.dir, t, x.Lb, a.K, a.delta, a.mA, a.W);
+  if (r < 0) return -1;
+  return (x.dir == 0 ? (long long)x.b * ck_rows_alpha(a.T, a.delta, a.mA) : (long long)x.b * a.nW * (a.K + 32)) + r;
+}
+
+template <typename R>
+__device__ __forceinline__ void put_out(const SweepArgs<R>& a, const SweepCtx& x, int t, int c, bool act, R y, R xv,
+                                        double n) {
+  const long long row = out_row(a, x, t);
+  if (row < 0) return;
+  const int C = a.C;
+  if (act) {
+    a.Y[x.dir][row * C + c] = y;
+    if (a.X[x.dir]) a.X[x.dir][row * C + c] = xv;
+  }
+  if (c == 0) a.n[x.dir][row] = n;
+}
+
 // edge-batch state of one label: Q of the four positions before the next batch's targets and
 // the prefetched rows of those targets
 struct EdgeState {
@@ -622,44 +692,23 @@ __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx&
     for (int i = 0; i < 3; ++i) e.qh[i] = e.qh[i + 1];
     e.qh[3] = v.y;
   }
-  const size_t rowbase = (size_t)x.b * (T + 1);
-  const int t = x.tpos(q);
   const int sl = q & pm;
-  if (act) {
-    a.Y[x.dir][(rowbase + t) * C + c] = h.pubY[sl * C + c];
-    a.X[x.dir][(rowbase + t) * C + c] = h.pubX[sl * C + c];
-  }
-  if (c == 0) {
-    a.n[x.dir][rowbase + t] = h.nring[q & (kNring - 1)];
-    if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
-  }
+  const int cs = act ? c : 0;
+  put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[q & (kNring - 1)]);
 }
 
 // per-position outputs (Y^, X^, n, max shift) of positions q-3 .. q from the published rings
 template <typename R>
 __device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
                                              bool act) {
-  const int C = a.C, T = a.T;
-  {
-    const size_t rowbase = (size_t)x.b * (T + 1);
-    const int cs = act ? c : 0;
-    R* Yo = a.Y[x.dir] + rowbase * C + cs;
-    R* Xo = a.X[x.dir] + rowbase * C + cs;
+  const int C = a.C;
+  const int cs = act ? c : 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int pos = q - 3 + i;
-      if (pos >= 0) {
-        const int t = x.tpos(pos);
-        const int sl = pos & 15;
-        if (act) {
-          Yo[(size_t)t * C] = h.pubY[sl * C + c];
-          Xo[(size_t)t * C] = h.pubX[sl * C + c];
-        }
-        if (c == 0) {
-          a.n[x.dir][rowbase + t] = h.nring[pos & (kNring - 1)];
-          if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
-        }
-      }
+  for (int i = 0; i < 4; ++i) {
+    const int pos = q - 3 + i;
+    if (pos >= 0) {
+      const int sl = pos & 15;
+      put_out<R>(a, x, x.tpos(pos), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[pos & (kNring - 1)]);
     }
   }
 }
@@ -837,9 +886,27 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     return am;
   };
 
-  // position 0: alpha[0] = 0 (virtual source) / beta[L] = 0
-  const R yh0 = x.dir == 0 ? (R)0 : Mth<R>::ninf();
-  R x1h = x.dir == 0 ? gemv((R)0) : (R)0;  // X^[p-1]
+  // replay: the first nforce positions take the stored messages (Y^, n) instead of the
+  // computed ones; X^ (the transition GEMV) and everything downstream are recomputed, so the
+  // replay reproduces the sweep that stored them (same positions mod 32, same arithmetic)
+  const SweepTask* tk = x.task;
+  const int nforce = tk ? tk->nforce : 0;
+  const int cs = act ? c : 0;
+  const R* fY = tk ? a.fY[x.dir] + (long long)tk->frow * C + cs : nullptr;
+  const long long fsC = tk ? (long long)tk->fstep * C : 0;
+  const int fs1 = tk ? tk->fstep : 0;
+  const double* fN = tk ? a.fN[x.dir] + tk->frow : nullptr;
+  R fq[4];
+  double nq[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    fq[i] = (i < nforce && act) ? fY[i * fsC] : Mth<R>::ninf();
+    nq[i] = i < nforce ? fN[i * fs1] : 0.0;
+  }
+  // position 0: alpha[0] = 0 (virtual source) / beta[L] = 0, or the first forced position
+  const R yh0 = nforce > 0 ? fq[0] : (x.dir == 0 ? (R)0 : Mth<R>::ninf());
+  const double n0 = nforce > 0 ? nq[0] : 0.0;
+  R x1h = (nforce > 0 || x.dir == 0) ? gemv(nforce > 0 ? yh0 : (R)0) : (R)0;  // X^[p-1]
   R x2h = Mth<R>::ninf();                    // X^[p-2]
   R x3h = Mth<R>::ninf();                    // X^[p-3]
   R x4h = Mth<R>::ninf();                    // X^[p-4]
@@ -849,15 +916,31 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   }
   if (tid == 0) {
     h.pubA[0] = 0;
-    h.nring[0] = 0.0;
+    h.nring[0] = n0;
   }
   nbar_arrive(BAR_A + 0, NA + NAE);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    fq[i] = fq[i + 1];
+    nq[i] = nq[i + 1];
+  }
+  fq[3] = (4 < nforce && act) ? fY[4 * fsC] : Mth<R>::ninf();
+  nq[3] = 4 < nforce ? fN[4 * fs1] : 0.0;
   R a1 = 0, a2 = 0, a3 = 0;  // frame shifts amax_{p-1}, amax_{p-2}, amax_{p-3}
-  double n_prev = 0.0;
-  double n_ref = 0.0;  // alpha: checkpoint normaliser in effect (log2); beta: 0 (absolute frame)
-  int ck_cnt = 0;
+  double n_prev = n0;
+  // alpha: checkpoint normaliser in effect (log2) and the position counter since the last
+  // checkpoint (streaming.py:205-214); beta: 0 (absolute frame)
+  double n_ref = tk ? tk->n_ref : 0.0;
+  int ck_cnt = tk ? tk->ck_phase : 0;
+  // reference bookkeeping of the forward (alpha, full sweeps): checkpoint normalisers N_i,
+  // the first dead position, clamp events
+  const bool book = x.dir == 0 && !tk && tid == 0;
+  double* Nb = (book && a.N) ? a.N + (size_t)x.b * a.n_ckpt : nullptr;
+  if (Nb) Nb[0] = 0.0;
+  int i_ck = 1;
+  int dmin = -1;
   int n_clamp = 0;
-  const int cs = act ? c : 0;
+  R yh_last = yh0;
   const R2* partc = h.part + cs;
   const typename Vec4<R>::T* hhc = h.hh + cs;
   const int pubm = g.PubS - 1;
@@ -870,33 +953,55 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     if (tr) tr[0] = clock64();
     nbar_sync(BAR_B + (p & 3), NB);
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(4, p);
-    R y = Mth<R>::ninf();
-    if (act) {
-      const R2 pm = partc[(p & 3) * C];  // durations >= 5, frame n_{p-4}
-      const auto hv = hhc[(p & pubm) * C];  // edge terms of durations 1..4
-      const R s12 = a2 + a1, s123 = a3 + s12;
-      y = lse5(pm.x - s123, pm.y, x4h + hv.w - s123, x3h + hv.z - s12, x2h + hv.y - a1, x1h + hv.x);
+    bool dead;
+    R yh, am;
+    double n_p;
+    if (p < nforce) {
+      yh = fq[0];
+      n_p = nq[0];
+      am = (R)(n_p - n_prev);  // the stored sweep's shift (exact: n_p = n_prev + (double)am there)
+      dead = false;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        fq[i] = fq[i + 1];
+        nq[i] = nq[i + 1];
+      }
+      fq[3] = (p + 4 < nforce && act) ? fY[(p + 4) * fsC] : Mth<R>::ninf();
+      nq[3] = p + 4 < nforce ? fN[(p + 4) * fs1] : 0.0;
+    } else {
+      R y = Mth<R>::ninf();
+      if (act) {
+        const R2 pm = partc[(p & 3) * C];  // durations >= 5, frame n_{p-4}
+        const auto hv = hhc[(p & pubm) * C];  // edge terms of durations 1..4
+        const R s12 = a2 + a1, s123 = a3 + s12;
+        y = lse5(pm.x - s123, pm.y, x4h + hv.w - s123, x3h + hv.z - s12, x2h + hv.y - a1, x1h + hv.x);
+      }
+      if (tr) tr[1] = clock64();
+      am = chain_max(y);
+      // the reference's guard (_numerics.py:59-75): a position whose every message is at or below
+      // NEG_INF + 1 in the reference frame (alpha: relative to the checkpoint normaliser in effect,
+      // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
+      dead = (am == Mth<R>::ninf()) || (n_prev + (double)am) - n_ref <= kGuardL2;
+      yh = dead ? Mth<R>::ninf() : y - am;
+      n_p = dead ? n_prev : n_prev + (double)am;
     }
-    if (tr) tr[1] = clock64();
-    const R am = chain_max(y);
-    // the reference's guard (_numerics.py:59-75): a position whose every message is at or below
-    // NEG_INF + 1 in the reference frame (alpha: relative to the checkpoint normaliser in effect,
-    // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
-    const bool dead = (am == Mth<R>::ninf()) || (n_prev + (double)am) - n_ref <= kGuardL2;
-    const R yh = dead ? Mth<R>::ninf() : y - am;
-    const double n_p = dead ? n_prev : n_prev + (double)am;
     // everything but X^[p] is published before the GEMV so those stores overlap it
     if (act) h.pubY[(p & pubm) * C + c] = yh;
     if (tid == 0) {
       h.pubA[p & pubm] = dead ? Mth<R>::ninf() : am;
       h.nring[p & (kNring - 1)] = n_p;
     }
-    // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
-    // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
-    if (x.dir == 0 && !dead && fabs((n_p - n_ref) * kLn2) > kClampLimit) ++n_clamp;
+    if (book) {
+      if (dead && dmin < 0) dmin = p;
+      // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
+      // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
+      if (!dead && fabs((n_p - n_ref) * kLn2) > kClampLimit) ++n_clamp;
+    }
     if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
       ck_cnt = 0;
       if (!dead) n_ref = n_p;
+      if (Nb && i_ck < a.n_ckpt) Nb[i_ck] = n_ref * kLn2;
+      ++i_ck;
     }
     const R xh = gemv(yh);
     if (tr) tr[2] = clock64();
@@ -912,8 +1017,28 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     a2 = a1;
     a1 = dead ? (R)0 : am;
     n_prev = n_p;
+    yh_last = yh;
   }
-  if (x.dir == 0 && tid == 0 && a.clamp) a.clamp[x.b] = n_clamp;
+  if (x.dir == 0 && !tk) {
+    // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats), streaming.py:216-229; the reference raises only
+    // when the final log-partition is at or below the guard, naming the first dead position
+    R sm = act ? Mth<R>::ex2(yh_last) : (R)0;
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    if (g.NCW > 1) {
+      if (lane == 0) h.wmax[warp] = sm;
+      nbar_sync(BAR_CH, g.NCW * 32);
+      sm = 0;
+      for (int w = 0; w < g.NCW; ++w) sm += h.wmax[w];
+    }
+    if (tid == 0) {
+      const double lz = (sm > (R)0) ? (n_prev + (double)Mth<R>::lg2(sm)) * kLn2 : -CUDART_INF;
+      if (a.logZ) a.logZ[x.b] = lz;
+      if (Nb)
+        for (int i = i_ck; i < a.n_ckpt; ++i) Nb[i] = n_ref * kLn2;  // frozen past L
+      if (a.dead_at) a.dead_at[x.b] = (lz - n_ref * kLn2 > kGuard) ? -1 : (dmin >= 0 ? dmin : L);
+      if (a.clamp) a.clamp[x.b] = n_clamp;
+    }
+  }
 }
 
 // ======================= near warps =======================
@@ -1101,19 +1226,9 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
       st_async_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q,
                    t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
     if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
-    if (!do_edge && q > Lq) {  // outputs of the positions after the last edge batch
-      const size_t rowbase = (size_t)x.b * (T + 1);
-      const int t = x.tpos(q);
-      if (act) {
-        a.Y[x.dir][(rowbase + t) * C + c] = h.pubY[sl * C + c];
-        a.X[x.dir][(rowbase + t) * C + c] = pXc[sl * C];
-      }
-      if (c == 0) {
-        a.n[x.dir][rowbase + t] = n_q;
-        if (x.dir == 0) a.amx[rowbase + t] = h.pubA[sl];
-      }
-    }
-    if (x.dir == 1 && q == L && c == 0) {
+    if (!do_edge && q > Lq)  // outputs of the positions after the last edge batch
+      put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q);
+    if (x.dir == 1 && q == L && c == 0 && !x.task) {
       const R* pX = h.pubX + sl * C;
       R mx = Mth<R>::ninf();
       for (int cc = 0; cc < C; ++cc) mx = fmax(mx, pX[cc]);
@@ -1657,7 +1772,12 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   const SweepGeo& g = a.geo;
   const int ci = blockIdx.x / g.G;
   SweepCtx x;
-  if (a.dirs == 3) {
+  x.task = nullptr;
+  if (a.tasks) {
+    x.task = a.tasks + ci;
+    x.b = x.task->b;
+    x.dir = x.task->dir;
+  } else if (a.dirs == 3) {
     x.b = ci >> 1;
     x.dir = ci & 1;
   } else {
@@ -1665,7 +1785,15 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
     x.dir = a.dirs == 1 ? 0 : 1;
   }
   x.rank = blockIdx.x % g.G;
-  x.L = (int)a.lengths[x.b];
+  x.Lb = (int)a.lengths[x.b];
+  if (x.task) {
+    x.L = x.task->steps;
+    x.t0 = x.task->t0;
+    if (x.L < 0) return;  // empty task (sequence shorter than the window): the whole cluster exits
+  } else {
+    x.L = x.Lb;
+    x.t0 = x.dir == 0 ? 0 : x.Lb;
+  }
   x.S = a.S + (size_t)x.b * (a.T + 1) * a.C;
   x.ps = a.ps ? a.ps + (size_t)x.b * a.T * a.C : nullptr;
   x.pe = a.pe ? a.pe + (size_t)x.b * a.T * a.C : nullptr;
@@ -1697,69 +1825,6 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   else if (TAILS)
     tail_main<R>(a, x, smem, HL, TL);
   if (TAILS) cluster_sync_all();
-}
-
-// ----------------------------------------------------------------------------
-// Reference bookkeeping of the forward (streaming.py:194-229) from the stored per-position
-// normalisers n_t and max shifts: checkpoint normalisers N_i (shift = max_c alpha at i*delta,
-// applied only while the sequence is alive, frozen past L), the first dead position (every
-// message at or below the guard relative to the running N), and logZ = LSE_c alpha[L,c].
-// One block per sequence; N_i is a short sequential recurrence, the dead scan is parallel.
-template <typename R>
-__global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* na, const R* amx, const int64_t* lengths,
-                                                   int T, int C, int delta, int n_ckpt, double* N, int32_t* dead_at,
-                                                   double* logZ) {
-  const int b = blockIdx.x;
-  const int L = (int)lengths[b];
-  const size_t rb = (size_t)b * (T + 1);
-  double* Nb = N + (size_t)b * n_ckpt;  // running N in effect from checkpoint i on (global: any n_ckpt)
-  __shared__ int dmin;
-  if (threadIdx.x == 0) {
-    double N_cur = 0.0;
-    Nb[0] = 0.0;
-    for (int i = 1; i < n_ckpt; ++i) {
-      const long long q = (long long)i * delta;
-      if (q <= L) {
-        const R am = amx[rb + q];
-        const double amax_abs = (am == Mth<R>::ninf()) ? -CUDART_INF : na[rb + q] * kLn2;
-        if (amax_abs - N_cur > kGuard) N_cur = amax_abs;
-      }
-      Nb[i] = N_cur;
-    }
-    dmin = 0x7fffffff;
-  }
-  __syncthreads();
-  // first dead position (streaming.py:198-200): every message at or below the guard; the chain
-  // marks those positions with a max shift of -inf
-  int best = 0x7fffffff;
-  for (int q = 1 + threadIdx.x; q <= L; q += blockDim.x)
-    if (amx[rb + q] == Mth<R>::ninf()) best = min(best, q);
-  atomicMin(&dmin, best);
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats)
-    R s = 0;
-    bool any = false;
-    for (int c = threadIdx.x; c < C; c += 32) {
-      const R y = Ya[(rb + L) * C + c];
-      if (y != Mth<R>::ninf()) any = true;
-      s += Mth<R>::ex2(y);
-    }
-    s = group_sum(s, 32);
-    any = __any_sync(0xffffffffu, any);
-    if (threadIdx.x == 0) {
-      const R amL = amx[rb + L];
-      const bool deadL = (amL == Mth<R>::ninf()) || !any;
-      const double lz = deadL ? -CUDART_INF : (na[rb + L] + (double)Mth<R>::lg2(s)) * kLn2;
-      logZ[b] = lz;
-      // the reference raises only when the final log-partition is at or below the guard
-      // (streaming.py:216-225), naming the first dead position, else L
-      const double Nfin = Nb[n_ckpt - 1 < (L / delta) ? n_ckpt - 1 : (L / delta)];
-      int da = -1;
-      if (!(lz - Nfin > kGuard)) da = dmin == 0x7fffffff ? L : dmin;
-      dead_at[b] = da;
-    }
-  }
 }
 
 }  // namespace scrf

@@ -142,8 +142,36 @@ def make_equiv(name, seed, T, K, C, B, mode, ragged=False, projections=False, ke
     print(f"  {name}: {time.time() - t0:.1f}s")
 
 
+def make_masked():
+    """Min-duration mask (duration_bias[0] = -2e9, at or below the NEG_INF guard) with K = 2:
+    position 1 is dead, later even positions are not. The reference's streaming path returns a
+    different log Z here than its own dense DP and K=2 fast path because clamp_log fires on
+    sentinel arithmetic (streaming.py:150-152, _numerics.py:41-56: RunStats counts the events);
+    the fixture holds the dense DP outputs (reference.py:174-283, no clamping) and, for the
+    record, the streaming path's log Z and clamp-event count."""
+    from streamcrf._numerics import RunStats
+    from streamcrf.diagnostics import position_marginals
+    from streamcrf.reference import dense_backward_marginals, dense_forward
+
+    _, params, cum = equivalence_instance(5, T=40, K=2, C=3, B=2, mode=P.CenteringMode.MEAN)
+    db = params.duration_bias.copy()
+    db[0, :] = -2.0e9
+    params = P.SemiCRFParams(params.transition, db)
+    object.__setattr__(cum, "lengths", np.array([40, 22]))
+    msgs = dense_forward(cum, params)
+    mu, grads = dense_backward_marginals(cum, params, msgs)
+    marg = position_marginals(mu, cum.lengths)
+    st = RunStats()
+    z_stream, _ = streaming_forward(cum, params, stats=st)
+    save("masked", logZ=msgs.logZ, grad_S=grads.grad_S, grad_T=grads.grad_T, grad_B=grads.grad_B,
+         position_marginals=marg.position_marginals, boundary_posterior=marg.boundary_posterior,
+         expected_segment_count=marg.expected_segment_count, S_digest=np.array(s_digest(cum.S)),
+         streaming_logZ=z_stream, streaming_clamp_events=np.int64(st.clamp_events))
+
+
 M = P.CenteringMode
 JOBS = {
+    "masked": make_masked,
     "small": lambda: make_small(),
     # c1 exactly as BASELINE.json config 1 (MEAN centering, SURVEY §8d), plus ragged+projections.
     "c1": lambda: make_equiv("c1", 0, 256, 8, 4, 4, M.MEAN),
