@@ -5,24 +5,31 @@
  * one reference function; the Python mirror (paper_2604_18780_b200.streaming)
  * keeps the reference's names and dataclasses and calls these through ctypes.
  *
- *   scrf_forward   <- streaming_forward   (streaming.py:155-229) + forward_logZ (:707-722)
- *   scrf_backward  <- streaming_backward  (streaming.py:264-408) incl. recompute_alpha
- *                     (:232-261) and finalize_marginals (diagnostics.py:54-79)
- *   scrf_posterior <- posterior           (streaming.py:725-746): forward + backward fused, the
- *                     alpha and beta sweeps run concurrently in one launch
+ * Two working-memory modes of the same kernels:
+ *   sublinear (the reference's design): the forward keeps only checkpoint
+ *     rows (the reference's snapshots Omega every delta positions plus replay warm-up rows,
+ *     O(sqrt(T K) C)); the backward replays alpha (and beta) window by window from them.
+ *       scrf_forward_sparse   <- streaming_forward (streaming.py:155-229), forward_logZ (:707-722)
+ *       scrf_backward_sparse  <- streaming_backward (streaming.py:264-408) incl. the alpha replay
+ *                                (:332-336) and finalize_marginals (diagnostics.py:54-79)
+ *       scrf_posterior_sparse <- posterior (streaming.py:725-746) in sublinear memory
+ *       scrf_recompute_alpha  <- recompute_alpha (streaming.py:232-261)
+ *       scrf_export_checkpoints_sparse <- CheckpointSet(omega, N, delta) (streaming.py:49-67)
+ *   full: every position's messages are kept (O(T C) working memory), no replay; fastest.
+ *       scrf_forward / scrf_backward / scrf_posterior / scrf_export_checkpoints
  *   scrf_viterbi   <- streaming_viterbi   (streaming.py:411-470) + decode (:749-762)
- *   scrf_export_checkpoints <- the CheckpointSet(omega, N, delta) view (streaming.py:49-67)
  *
  * Conventions
  *   - Every pointer argument is a DEVICE pointer owned by the caller; optional
  *     inputs may be NULL. Shapes: S (B, T+1, C) fp64; lengths (B,) int64 with
  *     1 <= L_b <= T; transition (C, C) [c_prev, c_new]; duration_bias (K, C)
  *     [k-1, c]; proj_start / proj_end (B, T, C) fp64 or NULL.
- *   - Work buffers are sized by the matching *_bytes query and zero-initialised
- *     by the library on the given stream; no hidden allocations, no global state.
- *   - `stream` is a cudaStream_t (passed as void*); all work is stream-ordered;
- *     the only host synchronisation is inside scrf_viterbi's optional traceback
- *     copy (none: tracebacks are written to device buffers).
+ *   - Work buffers are sized by the matching *_bytes query; their contents on entry do not
+ *     matter (every region is written before it is read, accumulators are cleared on the
+ *     call's stream). No hidden allocations. The only process state is debug/profiling
+ *     hooks (scrf_profile_events, scrf_position_outputs_event, scrf_debug_*), per thread.
+ *   - `stream` is a cudaStream_t (passed as void*); all work is stream-ordered; no entry
+ *     point synchronises with the host (tracebacks and segment lists stay on the device).
  *   - Return: 0 ok; < 0 invalid argument (see SCRF_E*); > 0 a cudaError_t.
  *   - precision: 0 = fp32 working type (production), 1 = fp64 working type
  *     (validation instantiation of the same algorithm).
@@ -118,6 +125,55 @@ int scrf_viterbi(const scrf_problem* p, double* score, int32_t* seg_start, int32
  * the sentinel -1e9 for never-written slots. */
 int scrf_export_checkpoints(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
                             const double* N, double* omega, void* stream);
+
+/* ---- sublinear-memory mode ------------------------------------------------------------ */
+
+/* Size of the sparse checkpoint buffer (alpha checkpoint rows, O(sqrt(T K) C)). */
+int scrf_sparse_checkpoint_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes);
+
+/* Size of the sparse backward work buffer: beta checkpoint rows, the replay window buffers
+ * (a few windows of ~max(delta, K+32) positions) and the per-pass partials. */
+int scrf_sparse_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes);
+
+/* Forward keeping only checkpoint rows; same outputs as scrf_forward (logZ, N, dead_at). */
+int scrf_forward_sparse(const scrf_problem* p, int64_t delta, int precision, double* logZ, double* N,
+                        int32_t* dead_at, void* ckpt, size_t ckpt_bytes, void* stream);
+
+/* Backward from scrf_forward_sparse's checkpoint rows and normalisers N: a beta sweep storing
+ * beta checkpoint rows, then window by window the alpha and beta replays and the posterior
+ * pass of the window. Outputs as scrf_backward. */
+int scrf_backward_sparse(const scrf_problem* p, int64_t delta, int precision, const double* logZ,
+                         const double* N, const void* ckpt, const double* upstream, double* grad_S,
+                         double* grad_T, double* grad_B, double* grad_P_start, double* grad_P_end,
+                         double* position_marginals, double* boundary_posterior,
+                         double* expected_segment_count, void* work, size_t work_bytes, void* stream);
+
+/* Both, with the alpha and beta checkpoint sweeps concurrent (scrf_posterior's signature). */
+int scrf_posterior_sparse(const scrf_problem* p, int64_t delta, int precision, const double* upstream,
+                          double* logZ, double* N, int32_t* dead_at, void* ckpt, size_t ckpt_bytes,
+                          double* grad_S, double* grad_T, double* grad_B, double* grad_P_start,
+                          double* grad_P_end, double* position_marginals, double* boundary_posterior,
+                          double* expected_segment_count, void* work, size_t work_bytes, void* stream);
+
+/* Sparse twins of scrf_backward_partials / scrf_beta_logz / scrf_clamp_events /
+ * scrf_export_checkpoints. */
+int scrf_backward_partials_sparse(const scrf_problem* p, int64_t delta, int precision, const void* work,
+                                  double* grad_T_partial, double* grad_B_partial, void* stream);
+int scrf_beta_logz_sparse(const scrf_problem* p, int64_t delta, int precision, const void* work,
+                          double* logZb, void* stream);
+int scrf_clamp_events_sparse(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
+                             const void* work, int32_t* events, void* stream);
+int scrf_export_checkpoints_sparse(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
+                                   const double* N, double* omega, void* stream);
+
+/* recompute_alpha(omega_i, n_i, cum, params, t_start, t_end): omega_i (B, K, C) fp64 device
+ * snapshot in the reference's ring-slot layout (values relative to N_i, sentinel -1e9 for
+ * empty slots); block (B, t_end - t_start + 1, C) fp64 in the same frame; block[:, 0] is the
+ * snapshot slot of t_start and positions past L_b hold their ring slot, as the reference. */
+int scrf_recompute_alpha_work_bytes(const scrf_problem* p, int64_t t_start, int64_t t_end, int precision,
+                                    size_t* bytes);
+int scrf_recompute_alpha(const scrf_problem* p, int precision, const double* omega_i, int64_t t_start,
+                         int64_t t_end, double* block, void* work, size_t work_bytes, void* stream);
 
 /* Clamp-event count per sequence (B,) int32 after scrf_forward (ckpt) and optionally
  * scrf_backward / scrf_posterior (work, or NULL): positions whose max alpha message relative

@@ -66,6 +66,19 @@ _SIGS = {
     "scrf_viterbi": (_int, [_P, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "scrf_export_checkpoints": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
     "scrf_clamp_events": (_int, [_P, _int, _vp, _vp, _vp, _vp]),
+    "scrf_sparse_checkpoint_bytes": (_int, [_P, _i64, _int, _psz]),
+    "scrf_sparse_backward_work_bytes": (_int, [_P, _i64, _int, _psz]),
+    "scrf_forward_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "scrf_backward_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _sz, _vp]),
+    "scrf_posterior_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _vp, _sz, _vp]),
+    "scrf_backward_partials_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
+    "scrf_beta_logz_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp]),
+    "scrf_clamp_events_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
+    "scrf_export_checkpoints_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
+    "scrf_recompute_alpha_work_bytes": (_int, [_P, _i64, _i64, _int, _psz]),
+    "scrf_recompute_alpha": (_int, [_P, _int, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
     "scrf_position_outputs_event": (None, [_vp]),

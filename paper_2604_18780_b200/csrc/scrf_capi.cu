@@ -216,7 +216,10 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
   return SCRF_OK;
 }
 
-// forward state ("checkpoint buffer"): per-position alpha-side messages
+// ---------------------------------------------------------------------------
+// buffer layouts
+
+// full-mode forward state ("checkpoint buffer"): per-position alpha-side messages
 struct FLayout {
   size_t Y, X, n, clamp, total;
 };
@@ -225,14 +228,50 @@ FLayout f_layout(const scrf_problem* p, int prec) {
   const size_t rs = prec ? 8 : 4;
   const size_t npos = (size_t)p->B * (p->T + 1);
   size_t o = 0;
-  L.Y = o;
-  o += al(npos * p->C * rs);
-  L.X = o;
-  o += al(npos * p->C * rs);
-  L.n = o;
-  o += al(npos * 8);
-  L.clamp = o;
-  o += al(p->B * 4);
+  L.Y = o;     o += al(npos * p->C * rs);
+  L.X = o;     o += al(npos * p->C * rs);
+  L.n = o;     o += al(npos * 8);
+  L.clamp = o; o += al(p->B * 4);
+  L.total = o;
+  return L;
+}
+
+// sublinear mode geometry: alpha checkpoint rows keep the last mA = min(K + 32, delta) positions
+// of every delta-period (covering the reference's omega snapshots and the warm-up of a replay
+// window); replay windows are W positions, a multiple of delta with W >= K + 32; beta
+// checkpoint rows hold K + 32 positions above every interior window boundary
+struct SparseGeo {
+  int mA, W, nW, nWin;
+  long long rowsAlpha, rowsBeta;  // per sequence
+  int rowsWin;                    // rows of a replay window buffer per sequence
+};
+SparseGeo sparse_geo(const scrf_problem* p, int64_t delta) {
+  SparseGeo g;
+  const int K = (int)p->K, T = (int)p->T, d = (int)delta;
+  g.mA = K + 32 < d ? K + 32 : d;
+  g.W = d >= K + 32 ? d : d * ((K + 32 + d - 1) / d);
+  g.nW = (T + g.W - 1) / g.W - 1;
+  if (g.nW < 0) g.nW = 0;
+  g.nWin = (T + 1 + g.W - 1) / g.W;
+  g.rowsAlpha = ck_rows_alpha(T, d, g.mA);
+  g.rowsBeta = (long long)g.nW * (K + 32);
+  g.rowsWin = g.W + K + 33;
+  return g;
+}
+
+// sparse forward state: alpha checkpoint rows (Y^, n) + clamp counts
+struct SLayout {
+  size_t Y, n, clamp, total;
+};
+SLayout s_layout(const scrf_problem* p, int64_t delta, int prec) {
+  SLayout L;
+  const size_t rs = prec ? 8 : 4;
+  const SparseGeo g = sparse_geo(p, delta);
+  const size_t rows = (size_t)p->B * g.rowsAlpha;
+  size_t o = 0;
+  L.Y = o;     o += al(rows * p->C * rs);
+  L.n = o;     o += al(rows * 8);
+  L.clamp = o; o += al(p->B * 4);
   L.total = o;
   return L;
 }
@@ -241,11 +280,12 @@ struct PostGeo {
   int CH, nch, CGB, SCB, nchB;
 };
 
-PostGeo post_geo(const scrf_problem* p, int prec) {
+// posterior-pass geometry for passes of at most Wn positions
+PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   PostGeo q;
-  const int C = (int)p->C, K = (int)p->K, T = (int)p->T, B = (int)p->B;
+  const int C = (int)p->C, K = (int)p->K, B = (int)p->B;
   q.CH = post_chunk(C);
-  q.nch = (T + 1 + q.CH - 1) / q.CH;
+  q.nch = (Wn + q.CH - 1) / q.CH;
   int cg = 4096 / K;
   if (cg < 1) cg = 1;
   if (cg > C) cg = C;
@@ -257,44 +297,99 @@ PostGeo post_geo(const scrf_problem* p, int prec) {
   long long want = 4LL * num_sms();
   long long per = (want + (long long)ngc * B - 1) / ((long long)ngc * B);
   if (per < 1) per = 1;
-  int scb = (int)((T + per - 1) / per);
+  int scb = (int)((Wn + per - 1) / per);
   scb = (scb + kGBSub - 1) / kGBSub * kGBSub;
   if (scb < kGBSub) scb = kGBSub;
   q.SCB = scb;
-  q.nchB = (T + scb - 1) / scb;
+  q.nchB = (Wn + scb - 1) / scb;
   return q;
 }
 
-// backward work buffer: beta-side messages + partials
-struct BLayout {
-  size_t Y, X, n, logZb, tot, cntp, gTp, gBp, gTs, gBs, cutU, corr, clamp, total;
-};
-
 // cut-normaliser spacing (scrf_cut.cuh): 0 disables the correction (SCRF_CUT_D=0, debugging)
 int cut_spacing() { return env_int("SCRF_CUT_D", 512); }
-int cut_slots(int64_t T, int d) { return d > 0 ? (int)((T - 1) / d) + 2 : 0; }
-BLayout b_layout(const scrf_problem* p, int prec) {
-  BLayout L;
-  const size_t rs = prec ? 8 : 4;
+
+// per-pass partials and the running per-sequence accumulators
+struct PLayout {
+  size_t logZb, tot, cntp, gTp, gBp, cutU, corr, carry, clamp, accT, accB, accN, total;
+};
+PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o) {
+  PLayout L;
   const size_t B = p->B, C = p->C, K = p->K;
-  const size_t npos = B * (p->T + 1);
-  const PostGeo q = post_geo(p, prec);
-  size_t o = 0;
-  L.Y = o;     o += al(npos * C * rs);
-  L.X = o;     o += al(npos * C * rs);
-  L.n = o;     o += al(npos * 8);
+  const PostGeo q = post_geo(p, prec, Wn);
+  const int d = cut_spacing();
   L.logZb = o; o += al(B * 8);
   L.tot = o;   o += al(B * q.nch * C * 8);
   L.cntp = o;  o += al(B * q.nch * 8);
   L.gTp = o;   o += al(B * q.nch * C * C * 8);
   L.gBp = o;   o += al(B * q.nchB * K * C * 8);
-  L.gTs = o;   o += al(B * C * C * 8);
-  L.gBs = o;   o += al(B * K * C * 8);
-  const int d = cut_spacing();
-  L.cutU = o;  o += d > 0 ? al(B * (size_t)cut_slots(p->T, d) * C * 8) : 0;
-  L.corr = o;  o += d > 0 ? al(B * (p->T + 1) * 8) : 0;
+  L.cutU = o;  o += d > 0 ? al(B * (size_t)cut_slots(0, Wn, d) * C * 8) : 0;
+  L.corr = o;  o += d > 0 ? al(B * (size_t)Wn * 8) : 0;
+  L.carry = o; o += al(B * C * 8);
   L.clamp = o; o += al(B * 4);
+  L.accT = o;  o += al(B * C * C * 8);
+  L.accB = o;  o += al(B * K * C * 8);
+  L.accN = o;  o += al(B * 8);
   L.total = o;
+  return L;
+}
+
+// full-mode backward work buffer: beta-side messages + pass buffers
+struct BLayout {
+  size_t Y, X, n, total;
+  PLayout P;
+};
+BLayout b_layout(const scrf_problem* p, int prec) {
+  BLayout L;
+  const size_t rs = prec ? 8 : 4;
+  const size_t C = p->C;
+  const size_t npos = (size_t)p->B * (p->T + 1);
+  size_t o = 0;
+  L.Y = o; o += al(npos * C * rs);
+  L.X = o; o += al(npos * C * rs);
+  L.n = o; o += al(npos * 8);
+  L.P = p_layout(p, prec, (int)p->T + 1, o);
+  L.total = L.P.total;
+  return L;
+}
+
+// windows replayed per launch (sublinear mode): enough clusters to fill the chip once
+int win_par(const scrf_problem* p, int G, int nWin) {
+  int P = env_int("SCRF_WIN_PAR", 0);
+  if (P <= 0) {
+    P = num_sms() / (2 * (int)p->B * G);
+    if (P < 1) P = 1;
+  }
+  return P < nWin ? P : nWin;
+}
+
+// sparse backward work: beta checkpoint rows, replay window buffers (alpha and beta sides),
+// replay tasks, pass buffers
+struct WLayout {
+  size_t bY, bn, aY, aX, an, wY, wX, wn, tasks, total;
+  PLayout P;
+  SparseGeo g;
+  int Pw;
+};
+WLayout w_layout(const scrf_problem* p, int64_t delta, int prec, int G) {
+  WLayout L;
+  const size_t rs = prec ? 8 : 4;
+  const size_t B = p->B, C = p->C;
+  L.g = sparse_geo(p, delta);
+  L.Pw = win_par(p, G, L.g.nWin);
+  const size_t rb = B * (size_t)L.g.rowsBeta;
+  const size_t rw = (size_t)L.Pw * B * L.g.rowsWin;
+  size_t o = 0;
+  L.bY = o;    o += al((rb ? rb : 1) * C * rs);
+  L.bn = o;    o += al((rb ? rb : 1) * 8);
+  L.aY = o;    o += al(rw * C * rs);
+  L.aX = o;    o += al(rw * C * rs);
+  L.an = o;    o += al(rw * 8);
+  L.wY = o;    o += al(rw * C * rs);
+  L.wX = o;    o += al(rw * C * rs);
+  L.wn = o;    o += al(rw * 8);
+  L.tasks = o; o += al((size_t)2 * L.Pw * B * sizeof(SweepTask));
+  L.P = p_layout(p, prec, L.g.W, o);
+  L.total = L.P.total;
   return L;
 }
 
@@ -331,13 +426,38 @@ cudaError_t launch_cl(Kern kern, int G, int nclusters, int NT, size_t smem, cuda
   return e;
 }
 
+// What one sweep launch reads and writes (untyped; run_sweep casts to the working type).
+struct SweepIO {
+  int dirs;                  // 1 alpha, 2 beta, 3 both (no tasks)
+  int store;                 // 0 every position at row b*(T+1)+t; 1 checkpoint rows
+  void* Y[2];
+  void* X[2];
+  double* n[2];
+  const SweepTask* tasks;    // replay mode
+  int ntasks;
+  const void* fY[2];
+  const double* fN[2];
+  double* logZ;
+  double* logZb;
+  double* N;
+  int32_t* dead_at;
+  int32_t* clamp;
+  bool record;               // profiling events around this launch
+};
+
 template <typename R>
-int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate, void* work, double* logZ, double* N,
-              int32_t* dead_at, cudaStream_t st) {
-  const int nd = dirs == 3 ? 2 : 1;
+int sweep_geo_of(const scrf_problem* p, SweepGeo* g) {
+  // geometry from (B, both directions) in every mode so that replays use the pass-1 geometry
+  return choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, 2, p->proj_start != nullptr,
+                          p->proj_end != nullptr, g);
+}
+
+template <typename R>
+int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStream_t st) {
   SweepGeo g;
-  int rc = choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, nd, p->proj_start != nullptr,
-                            p->proj_end != nullptr, &g);
+  int rc = io.dirs == 3 || io.tasks || io.store ? sweep_geo_of<R>(p, &g)
+                                    : choose_sweep_geo((int)p->B, (int)p->K, (int)p->C, sizeof(R) == 8, 1,
+                                                       p->proj_start != nullptr, p->proj_end != nullptr, &g);
   if (rc) return rc;
   SweepArgs<R> a;
   memset(&a, 0, sizeof(a));
@@ -352,26 +472,29 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
   a.K = (int)p->K;
   a.C = (int)p->C;
   a.geo = g;
-  a.dirs = dirs;
-  const FLayout F = f_layout(p, sizeof(R) == 8);
-  unsigned char* fb = (unsigned char*)fstate;
-  a.Y[0] = (R*)(fb + F.Y);
-  a.X[0] = (R*)(fb + F.X);
-  a.n[0] = (double*)(fb + F.n);
-  a.clamp = (dirs & 1) ? (int32_t*)(fb + F.clamp) : nullptr;
-  if (work) {
-    const BLayout W = b_layout(p, sizeof(R) == 8);
-    unsigned char* wb = (unsigned char*)work;
-    a.Y[1] = (R*)(wb + W.Y);
-    a.X[1] = (R*)(wb + W.X);
-    a.n[1] = (double*)(wb + W.n);
-    a.logZb = (double*)(wb + W.logZb);
+  a.dirs = io.dirs;
+  for (int d = 0; d < 2; ++d) {
+    a.Y[d] = (R*)io.Y[d];
+    a.X[d] = (R*)io.X[d];
+    a.n[d] = io.n[d];
+    a.fY[d] = (const R*)io.fY[d];
+    a.fN[d] = io.fN[d];
   }
-  a.logZ = logZ;
-  a.dead_at = dead_at;
-  a.N = N;
+  a.logZ = io.logZ;
+  a.logZb = io.logZb;
+  a.dead_at = io.dead_at;
+  a.N = io.N;
+  a.clamp = io.clamp;
   a.delta = (int)delta;
   a.n_ckpt = (int)n_ckpt_of(p->T, delta);
+  a.store = io.store;
+  if (io.store == 1 || io.tasks) {
+    const SparseGeo sg = sparse_geo(p, delta);
+    a.mA = sg.mA;
+    a.W = sg.W;
+    a.nW = sg.nW;
+  }
+  a.tasks = io.tasks;
   a.trace = g_trace;
   a.trace_from = env_int("SCRF_TRACE_FROM", 64);
   if (env_int("SCRF_WATCHDOG", 0)) {
@@ -381,29 +504,52 @@ int run_sweep(const scrf_problem* p, int dirs, int64_t delta, const void* fstate
     }
     a.hang = g_hang;
   }
+  const int ncl = io.tasks ? io.ntasks : a.B * (io.dirs == 3 ? 2 : 1);
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
   cudaError_t e;
   if (tails && cw1)
-    e = launch_cl(sweep_kernel<R, true, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+    e = launch_cl(sweep_kernel<R, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
   else if (tails)
-    e = launch_cl(sweep_kernel<R, true, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+    e = launch_cl(sweep_kernel<R, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
   else if (cw1)
-    e = launch_cl(sweep_kernel<R, false, true>, g.G, a.B * nd, g.NT, smem, st, a, true);
+    e = launch_cl(sweep_kernel<R, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
   else
-    e = launch_cl(sweep_kernel<R, false, false>, g.G, a.B * nd, g.NT, smem, st, a, true);
+    e = launch_cl(sweep_kernel<R, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
   return (int)e;
 }
 
+// message rows a posterior pass reads
+struct MsgView {
+  const void *Ya, *Xa, *Yb, *Xb;
+  const double *na, *nb;
+  int rowsA, tA0, rowsB, tB0;
+};
+
+struct PostOut {
+  const double* logZ;
+  const double* upstream;
+  double *grad_S, *grad_T, *grad_B, *gPs, *gPe, *pos, *bnd, *cnt;
+};
+
+// running per-sequence sums of the pass partials, in a fixed order (pass order, then part order)
+__global__ void acc_kernel(int B, int n, int nparts, const double* parts, double* acc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * n) return;
+  const int b = i / n, k = i % n;
+  double s = 0.0;
+  for (int q = 0; q < nparts; ++q) s += parts[((size_t)b * nparts + q) * n + k];
+  acc[i] += s;
+}
+
+// One posterior pass over positions [w0, w1): cut normalisers, frame correction, masses /
+// grad_S / grad_P / boundary / coverage (re-anchored at the cuts), grad_T, grad_B, and the
+// accumulation of the pass's transition / duration / count partials.
 template <typename R>
-int run_post(const scrf_problem* p, const void* fstate, void* work, const double* logZ, const double* upstream,
-             double* grad_S, double* grad_T, double* grad_B, double* gPs, double* gPe, double* pos, double* bnd,
-             double* cnt, cudaStream_t st) {
-  const PostGeo q = post_geo(p, sizeof(R) == 8);
-  const FLayout F = f_layout(p, sizeof(R) == 8);
-  const BLayout W = b_layout(p, sizeof(R) == 8);
-  const unsigned char* fb = (const unsigned char*)fstate;
-  unsigned char* wb = (unsigned char*)work;
+int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const PostOut& out, unsigned char* wb,
+             const PLayout& PL, bool last, cudaStream_t st) {
+  const int Wn = w1 - w0;
+  const PostGeo q = post_geo(p, sizeof(R) == 8, Wn);
   PostArgs<R> a;
   memset(&a, 0, sizeof(a));
   a.S = p->S;
@@ -412,37 +558,43 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
   a.dur = p->duration_bias;
   a.ps = p->proj_start;
   a.pe = p->proj_end;
-  a.upstream = upstream;
-  a.logZ = logZ;
+  a.upstream = out.upstream;
+  a.logZ = out.logZ;
   a.B = (int)p->B;
   a.T = (int)p->T;
   a.K = (int)p->K;
   a.C = (int)p->C;
-  a.Ya = (const R*)(fb + F.Y);
-  a.Xa = (const R*)(fb + F.X);
-  a.na = (const double*)(fb + F.n);
-  a.Yb = (const R*)(wb + W.Y);
-  a.Xb = (const R*)(wb + W.X);
-  a.nb = (const double*)(wb + W.n);
-  a.grad_S = grad_S;
-  a.grad_Ps = gPs;
-  a.grad_Pe = gPe;
-  a.pos = pos;
-  a.bnd = bnd;
+  a.Ya = (const R*)m.Ya;
+  a.Xa = (const R*)m.Xa;
+  a.na = m.na;
+  a.Yb = (const R*)m.Yb;
+  a.Xb = (const R*)m.Xb;
+  a.nb = m.nb;
+  a.rowsA = m.rowsA;
+  a.tA0 = m.tA0;
+  a.rowsB = m.rowsB;
+  a.tB0 = m.tB0;
+  a.w0 = w0;
+  a.w1 = w1;
+  a.grad_S = out.grad_S;
+  a.grad_Ps = out.gPs;
+  a.grad_Pe = out.gPe;
+  a.pos = out.pos;
+  a.bnd = out.bnd;
   a.CH = q.CH;
   a.nch = q.nch;
-  a.tot = (double*)(wb + W.tot);
-  a.cntp = (double*)(wb + W.cntp);
-  a.gTp = (double*)(wb + W.gTp);
+  a.tot = (double*)(wb + PL.tot);
+  a.cntp = (double*)(wb + PL.cntp);
+  a.gTp = (double*)(wb + PL.gTp);
   a.SCB = q.SCB;
   a.nchB = q.nchB;
   a.CGB = q.CGB;
-  a.gBp = (double*)(wb + W.gBp);
-  const int B = a.B, C = a.C, K = a.K, T = a.T;
+  a.gBp = (double*)(wb + PL.gBp);
+  const int B = a.B, C = a.C, K = a.K;
   cudaError_t e;
   const int cd = cut_spacing();
+  const int ncut = cut_slots(w0, w1, cd);
   if (cd > 0) {
-    // cut normalisers, then the per-position frame correction the passes below apply
     CutArgs<R> ca;
     memset(&ca, 0, sizeof(ca));
     ca.S = p->S;
@@ -450,9 +602,9 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     ca.dur = p->duration_bias;
     ca.ps = p->proj_start;
     ca.pe = p->proj_end;
-    ca.logZ = logZ;
+    ca.logZ = out.logZ;
     ca.B = B;
-    ca.T = T;
+    ca.T = a.T;
     ca.K = K;
     ca.C = C;
     ca.Ya = a.Ya;
@@ -461,25 +613,27 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     ca.Xb = a.Xb;
     ca.na = a.na;
     ca.nb = a.nb;
+    ca.rowsA = m.rowsA;
+    ca.tA0 = m.tA0;
+    ca.rowsB = m.rowsB;
+    ca.tB0 = m.tB0;
+    ca.w0 = w0;
+    ca.w1 = w1;
     ca.d = cd;
-    ca.ncut = cut_slots(T, cd);
-    ca.U = (double*)(wb + W.cutU);
+    ca.ncut = ncut;
+    ca.U = (double*)(wb + PL.cutU);
     const size_t sm = cut_smem<R>(K);
     e = cudaFuncSetAttribute(cut_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    cut_kernel<R><<<dim3(ca.ncut, (C + kCutCG - 1) / kCutCG, B), 256, sm, st>>>(ca);
-    a.corr = (const double*)(wb + W.corr);
+    cut_kernel<R><<<dim3(ncut, (C + kCutCG - 1) / kCutCG, B), 256, sm, st>>>(ca);
+    a.corr = (const double*)(wb + PL.corr);
   }
-  {
-    // per-position frame correction (when enabled) and the beta-side clamp-event count
-    e = cudaMemsetAsync(wb + W.clamp, 0, (size_t)B * 4, st);
-    if (e != cudaSuccess) return (int)e;
-    ++g_launches;
-    cut_corr_kernel<R><<<dim3((T + 1 + 255) / 256, B), 256, 0, st>>>(
-        p->lengths, T, C, cd, cd > 0 ? cut_slots(T, cd) : 0, cd > 0 ? (const double*)(wb + W.cutU) : nullptr,
-        cd > 0 ? (double*)(wb + W.corr) : nullptr, a.Xb, a.nb, (int32_t*)(wb + W.clamp));
-  }
+  // per-position frame correction (when enabled) and the beta-side clamp-event count
+  ++g_launches;
+  cut_corr_kernel<R><<<dim3((Wn + 255) / 256, B), 256, 0, st>>>(
+      p->lengths, C, w0, w1, cd, ncut, cd > 0 ? (const double*)(wb + PL.cutU) : nullptr,
+      cd > 0 ? (double*)(wb + PL.corr) : nullptr, a.Xb, a.nb, m.rowsB, m.tB0, (int32_t*)(wb + PL.clamp));
   {
     const size_t sm = post_pos_smem<R>(C, q.CH);
     e = cudaFuncSetAttribute(post_pos_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -487,14 +641,17 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
     ++g_launches;
     post_pos_kernel<R><<<dim3(q.nch, B), 256, sm, st>>>(a);
     ++g_launches;
-    ++g_launches;
     if (cd > 0 && cd % q.CH == 0)
-      cut_prefix_kernel<<<(B * C + 127) / 128, 128, 0, st>>>(p->lengths, B, C, q.nch, q.CH, cd, cut_slots(T, cd),
-                                                           (const double*)(wb + W.cutU), a.tot);
-    else
+      cut_prefix_kernel<<<(B * C + 127) / 128, 128, 0, st>>>(p->lengths, B, C, q.nch, q.CH, w0, w1, cd, ncut,
+                                                           (const double*)(wb + PL.cutU), a.tot,
+                                                           (double*)(wb + PL.carry));
+    else if (w0 == 0)
       post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
-    post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, T, C, q.CH, q.nch, a.tot, pos);
-    if (g_ev_pos) cudaEventRecord(g_ev_pos, st);
+    else
+      return SCRF_ECONFIG;  // windowed passes need the cut normalisers
+    ++g_launches;
+    post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, a.T, C, q.CH, q.nch, w0, w1, a.tot, out.pos);
+    if (last && g_ev_pos) cudaEventRecord(g_ev_pos, st);
   }
   {
     // one CTA holds every duration window of its label group (K <= kGBW * 512 * kGBJ = 4096)
@@ -508,13 +665,209 @@ int run_post(const scrf_problem* p, const void* fstate, void* work, const double
   {
     const int nT = C * C, nB = K * C;
     ++g_launches;
-    post_reduce2_kernel<<<(nT + 31) / 32, 256, 0, st>>>(B, nT, q.nch, a.gTp, upstream, (double*)(wb + W.gTs), grad_T);
+    acc_kernel<<<(B * nT + 255) / 256, 256, 0, st>>>(B, nT, q.nch, a.gTp, (double*)(wb + PL.accT));
     ++g_launches;
-    post_reduce2_kernel<<<(nB + 31) / 32, 256, 0, st>>>(B, nB, q.nchB, a.gBp, upstream, (double*)(wb + W.gBs), grad_B);
+    acc_kernel<<<(B * nB + 255) / 256, 256, 0, st>>>(B, nB, q.nchB, a.gBp, (double*)(wb + PL.accB));
     ++g_launches;
-    post_count_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, q.nch, a.cntp, cnt);
+    acc_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, 1, q.nch, a.cntp, (double*)(wb + PL.accN));
   }
   return (int)cudaGetLastError();
+}
+
+// zero the running accumulators / clamp counts before the first pass
+int pass_begin(const scrf_problem* p, unsigned char* wb, const PLayout& PL, cudaStream_t st) {
+  const size_t B = p->B, C = p->C, K = p->K;
+  cudaError_t e = cudaMemsetAsync(wb + PL.accT, 0, B * C * C * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.accB, 0, B * K * C * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.accN, 0, B * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.clamp, 0, B * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.carry, 0, B * C * 8, st);
+  return (int)e;
+}
+
+// batch totals (upstream-weighted, fixed order) of the accumulated partials
+int pass_finish(const scrf_problem* p, unsigned char* wb, const PLayout& PL, const PostOut& out, cudaStream_t st) {
+  const int B = (int)p->B, C = (int)p->C, K = (int)p->K;
+  const int nT = C * C, nB = K * C;
+  ++g_launches;
+  post_reduce2_kernel<<<(nT + 31) / 32, 256, 0, st>>>(B, nT, 1, (const double*)(wb + PL.accT), out.upstream, nullptr,
+                                                     out.grad_T);
+  ++g_launches;
+  post_reduce2_kernel<<<(nB + 31) / 32, 256, 0, st>>>(B, nB, 1, (const double*)(wb + PL.accB), out.upstream, nullptr,
+                                                     out.grad_B);
+  ++g_launches;
+  post_count_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, 1, (const double*)(wb + PL.accN), out.cnt);
+  return (int)cudaGetLastError();
+}
+
+template <typename R>
+int run_full_post(const scrf_problem* p, const void* fstate, void* work, const PostOut& out, cudaStream_t st) {
+  const FLayout F = f_layout(p, sizeof(R) == 8);
+  const BLayout W = b_layout(p, sizeof(R) == 8);
+  const unsigned char* fb = (const unsigned char*)fstate;
+  unsigned char* wb = (unsigned char*)work;
+  MsgView m;
+  m.Ya = fb + F.Y;
+  m.Xa = fb + F.X;
+  m.na = (const double*)(fb + F.n);
+  m.Yb = wb + W.Y;
+  m.Xb = wb + W.X;
+  m.nb = (const double*)(wb + W.n);
+  m.rowsA = m.rowsB = (int)p->T + 1;
+  m.tA0 = m.tB0 = 0;
+  int rc = pass_begin(p, wb, W.P, st);
+  if (rc) return rc;
+  rc = run_pass<R>(p, m, 0, (int)p->T + 1, out, wb, W.P, true, st);
+  if (rc) return rc;
+  return pass_finish(p, wb, W.P, out, st);
+}
+
+// replay tasks of windows j0 .. j0+P-1 (all sequences, both directions); see SweepTask
+__global__ void build_tasks_kernel(const int64_t* lengths, const double* N, int B, int T, int K, int delta, int n_ckpt,
+                                   int mA, int W, int nW, long long rowsAlpha, int rowsWin, int j0, int P,
+                                   SweepTask* tasks) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * B * P) return;
+  const int dir = i & 1, b = (i >> 1) % B, wi = (i >> 1) / B, j = j0 + wi;
+  const int L = (int)lengths[b];
+  const int w0 = j * W, w1 = min((j + 1) * W, T + 1);
+  SweepTask tk;
+  tk.b = b;
+  tk.dir = dir;
+  tk.fstep = 1;
+  tk.frow = 0;
+  tk.nforce = 0;
+  tk.ck_phase = 0;
+  tk.n_ref = 0.0;
+  tk.out_row = (long long)(wi * B + b) * rowsWin;
+  if (w0 > L) {
+    tk.t0 = 0;
+    tk.steps = -1;
+    tk.t_lo = 0;
+  } else if (dir == 0) {
+    const int tend = min(w1, L);
+    const int t0 = j == 0 ? 0 : ((w0 - K + 1) & ~31);
+    tk.t0 = t0;
+    tk.t_lo = t0;
+    tk.steps = tend - t0;
+    if (j > 0) {
+      tk.nforce = w0 - t0 + 1;
+      // checkpoint row of t0 (ck_row, alpha); rows ascend with t over [t0, w0]
+      const int ip = (t0 + delta - 1) / delta, e = ip * delta - t0;
+      tk.frow = (long long)b * rowsAlpha + (t0 == 0 ? 0 : 1 + (long long)(ip - 1) * mA + (mA - 1 - e));
+    }
+    tk.ck_phase = t0 % delta;
+    tk.n_ref = N[(size_t)b * n_ckpt + t0 / delta] * kLog2e;
+  } else {
+    tk.t_lo = w0;
+    if (w1 >= L) {
+      tk.t0 = L;
+      tk.steps = L - w0;
+    } else {
+      const int ttop = ck_ttop(j + 1, W, K, L);
+      tk.t0 = ttop;
+      tk.steps = ttop - w0;
+      tk.nforce = ttop - w1 + 1;
+      tk.frow = ((long long)b * nW + j) * (K + 32) + (ttop - w1);
+      tk.fstep = -1;
+    }
+  }
+  tasks[i] = tk;
+}
+
+// sparse posterior passes: replay windows (P per launch) from the checkpoint rows and run the
+// posterior pass of each window
+template <typename R>
+int run_sparse_post(const scrf_problem* p, int64_t delta, const void* ckpt, const double* N, void* work,
+                    const PostOut& out, cudaStream_t st) {
+  SweepGeo geo;
+  int rc = sweep_geo_of<R>(p, &geo);
+  if (rc) return rc;
+  const size_t rs = sizeof(R);
+  const WLayout WL = w_layout(p, delta, sizeof(R) == 8, geo.G);
+  const SLayout SL = s_layout(p, delta, sizeof(R) == 8);
+  const SparseGeo& g = WL.g;
+  const unsigned char* cb = (const unsigned char*)ckpt;
+  unsigned char* wb = (unsigned char*)work;
+  const int B = (int)p->B, C = (int)p->C, K = (int)p->K, T = (int)p->T;
+  const size_t wstride = (size_t)B * g.rowsWin;  // rows per replayed window
+  SweepTask* tasks = (SweepTask*)(wb + WL.tasks);
+  rc = pass_begin(p, wb, WL.P, st);
+  if (rc) return rc;
+  for (int j0 = 0; j0 < g.nWin; j0 += WL.Pw) {
+    const int P = g.nWin - j0 < WL.Pw ? g.nWin - j0 : WL.Pw;
+    ++g_launches;
+    build_tasks_kernel<<<(2 * B * P + 127) / 128, 128, 0, st>>>(p->lengths, N, B, T, K, (int)delta,
+                                                                (int)n_ckpt_of(p->T, delta), g.mA, g.W, g.nW,
+                                                                g.rowsAlpha, g.rowsWin, j0, P, tasks);
+    SweepIO io;
+    memset(&io, 0, sizeof(io));
+    io.dirs = 3;
+    io.tasks = tasks;
+    io.ntasks = 2 * B * P;
+    io.Y[0] = wb + WL.aY;
+    io.X[0] = wb + WL.aX;
+    io.n[0] = (double*)(wb + WL.an);
+    io.Y[1] = wb + WL.wY;
+    io.X[1] = wb + WL.wX;
+    io.n[1] = (double*)(wb + WL.wn);
+    io.fY[0] = cb + SL.Y;
+    io.fN[0] = (const double*)(cb + SL.n);
+    io.fY[1] = wb + WL.bY;
+    io.fN[1] = (const double*)(wb + WL.bn);
+    rc = run_sweep<R>(p, delta, io, st);
+    if (rc) return rc;
+    for (int wi = 0; wi < P; ++wi) {
+      const int j = j0 + wi;
+      const int w0 = j * g.W, w1 = (j + 1) * g.W < T + 1 ? (j + 1) * g.W : T + 1;
+      MsgView m;
+      const size_t ro = (size_t)wi * wstride;
+      m.Ya = wb + WL.aY + ro * C * rs;
+      m.Xa = wb + WL.aX + ro * C * rs;
+      m.na = (const double*)(wb + WL.an) + ro;
+      m.Yb = wb + WL.wY + ro * C * rs;
+      m.Xb = wb + WL.wX + ro * C * rs;
+      m.nb = (const double*)(wb + WL.wn) + ro;
+      m.rowsA = m.rowsB = g.rowsWin;
+      m.tA0 = j == 0 ? 0 : ((w0 - K + 1) & ~31);
+      m.tB0 = w0;
+      rc = run_pass<R>(p, m, w0, w1, out, wb, WL.P, j == g.nWin - 1, st);
+      if (rc) return rc;
+    }
+  }
+  return pass_finish(p, wb, WL.P, out, st);
+}
+
+// sparse pass 1: alpha and/or beta sweeps storing checkpoint rows only
+template <typename R>
+int run_sparse_sweeps(const scrf_problem* p, int64_t delta, int dirs, void* ckpt, void* work, double* logZ,
+                      double* N, int32_t* dead_at, cudaStream_t st, bool record) {
+  SweepIO io;
+  memset(&io, 0, sizeof(io));
+  io.dirs = dirs;
+  io.store = 1;
+  io.record = record;
+  if (dirs & 1) {
+    const SLayout SL = s_layout(p, delta, sizeof(R) == 8);
+    unsigned char* cb = (unsigned char*)ckpt;
+    io.Y[0] = cb + SL.Y;
+    io.n[0] = (double*)(cb + SL.n);
+    io.clamp = (int32_t*)(cb + SL.clamp);
+    io.logZ = logZ;
+    io.N = N;
+    io.dead_at = dead_at;
+  }
+  if (dirs & 2) {
+    SweepGeo geo;
+    int rc = sweep_geo_of<R>(p, &geo);
+    if (rc) return rc;
+    const WLayout WL = w_layout(p, delta, sizeof(R) == 8, geo.G);
+    unsigned char* wb = (unsigned char*)work;
+    io.Y[1] = wb + WL.bY;
+    io.n[1] = (double*)(wb + WL.bn);
+    io.logZb = (double*)(wb + WL.P.logZb);
+  }
+  return run_sweep<R>(p, delta, io, st);
 }
 
 // reference-format checkpoint view (streaming.py:49-67): ring after the shift at i*delta
@@ -545,6 +898,119 @@ __global__ void export_kernel(const R* Ya, const double* na, const double* N, co
   const double v = (na[o] + (double)y) * kLn2 - N[(size_t)b * nck + ck];
   omega[i] = v <= kGuard ? kNegInfRef : v;
 }
+// checkpoint view from the sparse alpha rows (same semantics as export_kernel)
+template <typename R>
+__global__ void export_sparse_kernel(const R* Y, const double* n, const double* N, const int64_t* lengths, int B,
+                                     int T, int nck, int K, int C, int delta, int mA, long long rowsAlpha,
+                                     double* omega) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)B * nck * K * C;
+  if (i >= total) return;
+  const int c = (int)(i % C);
+  const int slot = (int)((i / C) % K);
+  const int ck = (int)((i / ((size_t)C * K)) % nck);
+  const int b = (int)(i / ((size_t)C * K * nck));
+  const int L = (int)lengths[b];
+  long long e = (long long)ck * delta;
+  if (e > L) e = L;
+  const long long s = e - (((e - slot) % K) + K) % K;
+  if (s < 0) {
+    omega[i] = kNegInfRef;
+    return;
+  }
+  long long row;
+  if (s > L - mA) {
+    row = 1 + (long long)((T + delta - 1) / delta) * mA + (s - (L - mA + 1));
+  } else if (s == 0) {
+    row = 0;
+  } else {
+    const long long ip = (s + delta - 1) / delta, ee = ip * delta - s;
+    row = 1 + (ip - 1) * mA + (mA - 1 - ee);
+  }
+  row += (long long)b * rowsAlpha;
+  const R y = Y[row * C + c];
+  if (!(y > -INFINITY)) {
+    omega[i] = kNegInfRef;
+    return;
+  }
+  const double v = (n[row] + (double)y) * kLn2 - N[(size_t)b * nck + ck];
+  omega[i] = v <= kGuard ? kNegInfRef : v;
+}
+
+// forced rows of a recompute_alpha replay: positions tf0 .. t0 from the snapshot's ring slots
+// (alpha relative to N_i, nats; values at or below the guard are masked), and the task
+template <typename R>
+__global__ void ra_prep_kernel(const double* omega, const int64_t* lengths, int B, int K, int C, int t0, int t1,
+                               int tf0, int rows, R* fY, double* fN, SweepTask* tasks) {
+  const int b = blockIdx.x;
+  const int L = (int)lengths[b];
+  const double* om = omega + (size_t)b * K * C;
+  __shared__ double red[4];
+  double nprev = 0.0;
+  for (int t = tf0; t <= t0; ++t) {
+    const int slot = t % K;
+    double m = -CUDART_INF;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      const double v = om[(size_t)slot * C + c];
+      if (v > kGuard) m = fmax(m, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+    __syncthreads();
+    const double nt = m > -CUDART_INF ? m * kLog2e : nprev;
+    const size_t r = (size_t)b * K + (t - tf0);
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      const double v = om[(size_t)slot * C + c];
+      fY[r * C + c] = v > kGuard ? (R)(v * kLog2e - nt) : Mth<R>::ninf();
+    }
+    if (threadIdx.x == 0) fN[r] = nt;
+    nprev = nt;
+  }
+  if (threadIdx.x == 0) {
+    SweepTask tk;
+    tk.b = b;
+    tk.dir = 0;
+    tk.t0 = tf0;
+    const int tend = t1 < L ? t1 : L;
+    tk.steps = tend > t0 ? tend - tf0 : -1;
+    tk.nforce = t0 - tf0 + 1;
+    tk.t_lo = tf0;
+    tk.fstep = 1;
+    tk.frow = (long long)b * K;
+    tk.out_row = (long long)b * rows;
+    tk.ck_phase = 0;   // delta is passed as 2^30: no checkpoint shift inside a replay window
+    tk.n_ref = 0.0;    // snapshot frame: masked at or below the guard relative to N_i
+    tasks[b] = tk;
+  }
+}
+
+// block[b, t - t0, c] (snapshot frame, nats): replayed rows for t <= L; past L the ring slot
+// t % K keeps the last position <= L of that slot (replayed, or the snapshot's own)
+template <typename R>
+__global__ void ra_block_kernel(const double* omega, const int64_t* lengths, int B, int K, int C, int t0, int t1,
+                                int tf0, int rows, const R* oY, const double* on, double* block) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = t1 - t0 + 1;
+  if (i >= (size_t)B * nt * C) return;
+  const int c = (int)(i % C);
+  const int j = (int)((i / C) % nt);
+  const int b = (int)(i / ((size_t)C * nt));
+  const int L = (int)lengths[b];
+  int t = t0 + j;
+  if (t > L) t -= K * ((t - L + K - 1) / K);
+  double v;
+  if (j == 0 || t <= t0) {
+    v = omega[((size_t)b * K + (t0 + j) % K) * C + c];
+  } else {
+    const size_t r = (size_t)b * rows + (t - tf0);
+    const R y = oY[r * C + c];
+    v = (y > Mth<R>::ninf()) ? (on[r] + (double)y) * kLn2 : kNegInfRef;
+  }
+  block[i] = v;
+}
+
 __global__ void clamp_sum_kernel(int B, const int32_t* a, const int32_t* b, int32_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < B) out[i] = a[i] + (b ? b[i] : 0);
@@ -569,6 +1035,8 @@ int scrf_checkpoint_bytes(const scrf_problem* p, int64_t delta, int precision, s
   return SCRF_OK;
 }
 
+#define SCRF_DISPATCH(prec, call) ((prec) ? call<double> : call<float>)
+
 int scrf_forward(const scrf_problem* p, int64_t delta, int precision, double* logZ, double* N, int32_t* dead_at,
                  void* ckpt, size_t ckpt_bytes, void* stream) {
   g_launches = 0;
@@ -576,10 +1044,21 @@ int scrf_forward(const scrf_problem* p, int64_t delta, int precision, double* lo
   if (rc) return rc;
   if (delta < 1) return SCRF_EDELTA;
   if (!logZ || !N || !dead_at || !ckpt) return SCRF_ENULL;
-  if (ckpt_bytes < f_layout(p, precision).total) return SCRF_EWORK;
-  cudaStream_t st = (cudaStream_t)stream;
-  return precision ? run_sweep<double>(p, 1, delta, ckpt, nullptr, logZ, N, dead_at, st)
-                   : run_sweep<float>(p, 1, delta, ckpt, nullptr, logZ, N, dead_at, st);
+  const FLayout F = f_layout(p, precision);
+  if (ckpt_bytes < F.total) return SCRF_EWORK;
+  unsigned char* fb = (unsigned char*)ckpt;
+  SweepIO io;
+  memset(&io, 0, sizeof(io));
+  io.dirs = 1;
+  io.Y[0] = fb + F.Y;
+  io.X[0] = fb + F.X;
+  io.n[0] = (double*)(fb + F.n);
+  io.clamp = (int32_t*)(fb + F.clamp);
+  io.logZ = logZ;
+  io.N = N;
+  io.dead_at = dead_at;
+  io.record = true;
+  return SCRF_DISPATCH(precision, run_sweep)(p, delta, io, (cudaStream_t)stream);
 }
 
 int scrf_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes) {
@@ -599,6 +1078,49 @@ static int check_bwd_args(const scrf_problem* p, int64_t delta, const double* lo
   return SCRF_OK;
 }
 
+static PostOut post_out(const double* logZ, const double* upstream, double* grad_S, double* grad_T, double* grad_B,
+                        double* gPs, double* gPe, double* pos, double* bnd, double* cnt) {
+  PostOut o;
+  o.logZ = logZ;
+  o.upstream = upstream;
+  o.grad_S = grad_S;
+  o.grad_T = grad_T;
+  o.grad_B = grad_B;
+  o.gPs = gPs;
+  o.gPe = gPe;
+  o.pos = pos;
+  o.bnd = bnd;
+  o.cnt = cnt;
+  return o;
+}
+
+// full-mode beta sweep into the backward work buffer (dirs 2) or both sweeps (dirs 3)
+static int full_sweeps(const scrf_problem* p, int64_t delta, int precision, int dirs, void* ckpt, void* work,
+                       double* logZ, double* N, int32_t* dead_at, cudaStream_t st) {
+  const FLayout F = f_layout(p, precision);
+  const BLayout W = b_layout(p, precision);
+  unsigned char* fb = (unsigned char*)ckpt;
+  unsigned char* wb = (unsigned char*)work;
+  SweepIO io;
+  memset(&io, 0, sizeof(io));
+  io.dirs = dirs;
+  io.record = true;
+  if (dirs & 1) {
+    io.Y[0] = fb + F.Y;
+    io.X[0] = fb + F.X;
+    io.n[0] = (double*)(fb + F.n);
+    io.clamp = (int32_t*)(fb + F.clamp);
+    io.logZ = logZ;
+    io.N = N;
+    io.dead_at = dead_at;
+  }
+  io.Y[1] = wb + W.Y;
+  io.X[1] = wb + W.X;
+  io.n[1] = (double*)(wb + W.n);
+  io.logZb = (double*)(wb + W.P.logZb);
+  return SCRF_DISPATCH(precision, run_sweep)(p, delta, io, st);
+}
+
 int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const double* logZ, const void* ckpt,
                   const double* upstream, double* grad_S, double* grad_T, double* grad_B, double* grad_P_start,
                   double* grad_P_end, double* position_marginals, double* boundary_posterior,
@@ -609,13 +1131,11 @@ int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const dou
   if (rc) return rc;
   if (work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  rc = precision ? run_sweep<double>(p, 2, delta, ckpt, work, nullptr, nullptr, nullptr, st)
-                 : run_sweep<float>(p, 2, delta, ckpt, work, nullptr, nullptr, nullptr, st);
+  rc = full_sweeps(p, delta, precision, 2, (void*)ckpt, work, nullptr, nullptr, nullptr, st);
   if (rc) return rc;
-  return precision ? run_post<double>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
-                                      position_marginals, boundary_posterior, expected_segment_count, st)
-                   : run_post<float>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
-                                     position_marginals, boundary_posterior, expected_segment_count, st);
+  const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
+                             boundary_posterior, expected_segment_count);
+  return SCRF_DISPATCH(precision, run_full_post)(p, ckpt, work, o, st);
 }
 
 int scrf_posterior(const scrf_problem* p, int64_t delta, int precision, const double* upstream, double* logZ, double* N,
@@ -629,16 +1149,11 @@ int scrf_posterior(const scrf_problem* p, int64_t delta, int precision, const do
   if (!N || !dead_at) return SCRF_ENULL;
   if (ckpt_bytes < f_layout(p, precision).total || work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  rc = precision ? run_sweep<double>(p, 3, delta, ckpt, work, logZ, N, dead_at, st)
-                 : run_sweep<float>(p, 3, delta, ckpt, work, logZ, N, dead_at, st);
+  rc = full_sweeps(p, delta, precision, 3, ckpt, work, logZ, N, dead_at, st);
   if (rc) return rc;
-  const int n0 = g_launches;
-  rc = precision ? run_post<double>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
-                                    position_marginals, boundary_posterior, expected_segment_count, st)
-                 : run_post<float>(p, ckpt, work, logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end,
-                                   position_marginals, boundary_posterior, expected_segment_count, st);
-  (void)n0;
-  return rc;
+  const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
+                             boundary_posterior, expected_segment_count);
+  return SCRF_DISPATCH(precision, run_full_post)(p, ckpt, work, o, st);
 }
 
 int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, const void* work,
@@ -646,20 +1161,129 @@ int scrf_backward_partials(const scrf_problem* p, int64_t delta, int precision, 
   int rc = check_problem(p);
   if (rc) return rc;
   (void)delta;
-  const BLayout W = b_layout(p, precision);
+  const PLayout P = b_layout(p, precision).P;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned char* w = (const unsigned char*)work;
-  cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + W.gTs, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
+  cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + P.accT, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(grad_B_partial, w + W.gBs, (size_t)p->B * p->K * p->C * 8, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(grad_B_partial, w + P.accB, (size_t)p->B * p->K * p->C * 8, cudaMemcpyDeviceToDevice, st);
   return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// sublinear-memory mode
+
+static int sparse_G(const scrf_problem* p, int precision) {
+  SweepGeo g;
+  int rc = precision ? sweep_geo_of<double>(p, &g) : sweep_geo_of<float>(p, &g);
+  return rc ? -1 : g.G;
+}
+
+int scrf_sparse_checkpoint_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (delta < 1) return SCRF_EDELTA;
+  *bytes = s_layout(p, delta, precision).total;
+  return SCRF_OK;
+}
+
+int scrf_sparse_backward_work_bytes(const scrf_problem* p, int64_t delta, int precision, size_t* bytes) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (delta < 1) return SCRF_EDELTA;
+  const int G = sparse_G(p, precision);
+  if (G < 0) return SCRF_ECONFIG;
+  *bytes = w_layout(p, delta, precision, G).total;
+  return SCRF_OK;
+}
+
+int scrf_forward_sparse(const scrf_problem* p, int64_t delta, int precision, double* logZ, double* N, int32_t* dead_at,
+                        void* ckpt, size_t ckpt_bytes, void* stream) {
+  g_launches = 0;
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (delta < 1) return SCRF_EDELTA;
+  if (!logZ || !N || !dead_at || !ckpt) return SCRF_ENULL;
+  if (ckpt_bytes < s_layout(p, delta, precision).total) return SCRF_EWORK;
+  return SCRF_DISPATCH(precision, run_sparse_sweeps)(p, delta, 1, ckpt, nullptr, logZ, N, dead_at,
+                                                      (cudaStream_t)stream, true);
+}
+
+int scrf_backward_sparse(const scrf_problem* p, int64_t delta, int precision, const double* logZ, const double* N,
+                         const void* ckpt, const double* upstream, double* grad_S, double* grad_T, double* grad_B,
+                         double* grad_P_start, double* grad_P_end, double* position_marginals,
+                         double* boundary_posterior, double* expected_segment_count, void* work, size_t work_bytes,
+                         void* stream) {
+  g_launches = 0;
+  int rc = check_bwd_args(p, delta, logZ, ckpt, grad_S, grad_T, grad_B, position_marginals, boundary_posterior,
+                          expected_segment_count, work);
+  if (rc) return rc;
+  if (!N) return SCRF_ENULL;
+  size_t need = 0;
+  rc = scrf_sparse_backward_work_bytes(p, delta, precision, &need);
+  if (rc) return rc;
+  if (work_bytes < need) return SCRF_EWORK;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = SCRF_DISPATCH(precision, run_sparse_sweeps)(p, delta, 2, nullptr, work, nullptr, nullptr, nullptr, st, true);
+  if (rc) return rc;
+  const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
+                             boundary_posterior, expected_segment_count);
+  return SCRF_DISPATCH(precision, run_sparse_post)(p, delta, ckpt, N, work, o, st);
+}
+
+int scrf_posterior_sparse(const scrf_problem* p, int64_t delta, int precision, const double* upstream, double* logZ,
+                          double* N, int32_t* dead_at, void* ckpt, size_t ckpt_bytes, double* grad_S, double* grad_T,
+                          double* grad_B, double* grad_P_start, double* grad_P_end, double* position_marginals,
+                          double* boundary_posterior, double* expected_segment_count, void* work, size_t work_bytes,
+                          void* stream) {
+  g_launches = 0;
+  int rc = check_bwd_args(p, delta, logZ, ckpt, grad_S, grad_T, grad_B, position_marginals, boundary_posterior,
+                          expected_segment_count, work);
+  if (rc) return rc;
+  if (!N || !dead_at) return SCRF_ENULL;
+  size_t need = 0;
+  rc = scrf_sparse_backward_work_bytes(p, delta, precision, &need);
+  if (rc) return rc;
+  if (ckpt_bytes < s_layout(p, delta, precision).total || work_bytes < need) return SCRF_EWORK;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = SCRF_DISPATCH(precision, run_sparse_sweeps)(p, delta, 3, ckpt, work, logZ, N, dead_at, st, true);
+  if (rc) return rc;
+  const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
+                             boundary_posterior, expected_segment_count);
+  return SCRF_DISPATCH(precision, run_sparse_post)(p, delta, ckpt, N, work, o, st);
+}
+
+int scrf_backward_partials_sparse(const scrf_problem* p, int64_t delta, int precision, const void* work,
+                                  double* grad_T_partial, double* grad_B_partial, void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  const int G = sparse_G(p, precision);
+  if (G < 0) return SCRF_ECONFIG;
+  const PLayout P = w_layout(p, delta, precision, G).P;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned char* w = (const unsigned char*)work;
+  cudaError_t e = cudaMemcpyAsync(grad_T_partial, w + P.accT, (size_t)p->B * p->C * p->C * 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(grad_B_partial, w + P.accB, (size_t)p->B * p->K * p->C * 8, cudaMemcpyDeviceToDevice, st);
+  return (int)e;
+}
+
+int scrf_beta_logz_sparse(const scrf_problem* p, int64_t delta, int precision, const void* work, double* logZb,
+                          void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  const int G = sparse_G(p, precision);
+  if (G < 0) return SCRF_ECONFIG;
+  const PLayout P = w_layout(p, delta, precision, G).P;
+  return (int)cudaMemcpyAsync(logZb, (const unsigned char*)work + P.logZb, (size_t)p->B * 8, cudaMemcpyDeviceToDevice,
+                              (cudaStream_t)stream);
 }
 
 int scrf_beta_logz(const scrf_problem* p, int precision, const void* work, double* logZb, void* stream) {
   int rc = check_problem(p);
   if (rc) return rc;
   const BLayout W = b_layout(p, precision);
-  return (int)cudaMemcpyAsync(logZb, (const unsigned char*)work + W.logZb, (size_t)p->B * 8, cudaMemcpyDeviceToDevice,
+  return (int)cudaMemcpyAsync(logZb, (const unsigned char*)work + W.P.logZb, (size_t)p->B * 8, cudaMemcpyDeviceToDevice,
                               (cudaStream_t)stream);
 }
 
@@ -837,7 +1461,128 @@ int scrf_clamp_events(const scrf_problem* p, int precision, const void* ckpt, co
   ++g_launches;
   clamp_sum_kernel<<<(unsigned)((p->B + 127) / 128), 128, 0, st>>>(
       (int)p->B, (const int32_t*)((const unsigned char*)ckpt + F.clamp),
-      work ? (const int32_t*)((const unsigned char*)work + b_layout(p, precision).clamp) : nullptr, events);
+      work ? (const int32_t*)((const unsigned char*)work + b_layout(p, precision).P.clamp) : nullptr, events);
+  return (int)cudaGetLastError();
+}
+
+int scrf_clamp_events_sparse(const scrf_problem* p, int64_t delta, int precision, const void* ckpt, const void* work,
+                             int32_t* events, void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (!ckpt || !events) return SCRF_ENULL;
+  const SLayout S = s_layout(p, delta, precision);
+  const int G = sparse_G(p, precision);
+  if (G < 0) return SCRF_ECONFIG;
+  cudaStream_t st = (cudaStream_t)stream;
+  ++g_launches;
+  clamp_sum_kernel<<<(unsigned)((p->B + 127) / 128), 128, 0, st>>>(
+      (int)p->B, (const int32_t*)((const unsigned char*)ckpt + S.clamp),
+      work ? (const int32_t*)((const unsigned char*)work + w_layout(p, delta, precision, G).P.clamp) : nullptr, events);
+  return (int)cudaGetLastError();
+}
+
+int scrf_export_checkpoints_sparse(const scrf_problem* p, int64_t delta, int precision, const void* ckpt,
+                                   const double* N, double* omega, void* stream) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (delta < 1) return SCRF_EDELTA;
+  const SLayout S = s_layout(p, delta, precision);
+  const SparseGeo g = sparse_geo(p, delta);
+  const unsigned char* base = (const unsigned char*)ckpt;
+  const int nck = (int)n_ckpt_of(p->T, delta);
+  const size_t total = (size_t)p->B * nck * p->K * p->C;
+  ++g_launches;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  if (precision)
+    export_sparse_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const double*)(base + S.Y), (const double*)(base + S.n), N, p->lengths, (int)p->B, (int)p->T, nck,
+        (int)p->K, (int)p->C, (int)delta, g.mA, g.rowsAlpha, omega);
+  else
+    export_sparse_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const float*)(base + S.Y), (const double*)(base + S.n), N, p->lengths, (int)p->B, (int)p->T, nck,
+        (int)p->K, (int)p->C, (int)delta, g.mA, g.rowsAlpha, omega);
+  return (int)cudaGetLastError();
+}
+
+// recompute_alpha (streaming.py:232-261) on the device: forced rows from the snapshot, a replay
+// task per sequence, the block in the snapshot frame
+struct RALayout {
+  size_t fY, fN, oY, oX, on, tasks, total;
+  int rows;  // output rows per sequence
+};
+static RALayout ra_layout(const scrf_problem* p, int precision, int64_t t0, int64_t t1) {
+  RALayout L;
+  const size_t rs = precision ? 8 : 4;
+  const size_t B = p->B, C = p->C, K = p->K;
+  const int64_t tf0 = t0 - K + 1 > 0 ? t0 - K + 1 : 0;
+  L.rows = (int)(t1 - tf0 + 1);
+  size_t o = 0;
+  L.fY = o;    o += al(B * K * C * rs);
+  L.fN = o;    o += al(B * K * 8);
+  L.oY = o;    o += al(B * (size_t)L.rows * C * rs);
+  L.oX = o;    o += al(B * (size_t)L.rows * C * rs);
+  L.on = o;    o += al(B * (size_t)L.rows * 8);
+  L.tasks = o; o += al(B * sizeof(SweepTask));
+  L.total = o;
+  return L;
+}
+
+int scrf_recompute_alpha_work_bytes(const scrf_problem* p, int64_t t_start, int64_t t_end, int precision,
+                                    size_t* bytes) {
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (t_start < 0 || t_end < t_start || t_end > p->T) return SCRF_EDIM;
+  *bytes = ra_layout(p, precision, t_start, t_end).total;
+  return SCRF_OK;
+}
+
+int scrf_recompute_alpha(const scrf_problem* p, int precision, const double* omega_i, int64_t t_start, int64_t t_end,
+                         double* block, void* work, size_t work_bytes, void* stream) {
+  g_launches = 0;
+  int rc = check_problem(p);
+  if (rc) return rc;
+  if (!omega_i || !block || !work) return SCRF_ENULL;
+  if (t_start < 0 || t_end < t_start || t_end > p->T) return SCRF_EDIM;
+  const RALayout RL = ra_layout(p, precision, t_start, t_end);
+  if (work_bytes < RL.total) return SCRF_EWORK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned char* wb = (unsigned char*)work;
+  const int B = (int)p->B, K = (int)p->K, C = (int)p->C;
+  const int t0 = (int)t_start, t1 = (int)t_end;
+  const int tf0 = t0 - K + 1 > 0 ? t0 - K + 1 : 0;
+  ++g_launches;
+  if (precision)
+    ra_prep_kernel<double><<<B, 128, 0, st>>>(omega_i, p->lengths, B, K, C, t0, t1, tf0, RL.rows,
+                                              (double*)(wb + RL.fY), (double*)(wb + RL.fN),
+                                              (SweepTask*)(wb + RL.tasks));
+  else
+    ra_prep_kernel<float><<<B, 128, 0, st>>>(omega_i, p->lengths, B, K, C, t0, t1, tf0, RL.rows,
+                                             (float*)(wb + RL.fY), (double*)(wb + RL.fN),
+                                             (SweepTask*)(wb + RL.tasks));
+  if (t1 > t0) {
+    SweepIO io;
+    memset(&io, 0, sizeof(io));
+    io.dirs = 1;
+    io.tasks = (const SweepTask*)(wb + RL.tasks);
+    io.ntasks = B;
+    io.Y[0] = wb + RL.oY;
+    io.X[0] = wb + RL.oX;
+    io.n[0] = (double*)(wb + RL.on);
+    io.fY[0] = wb + RL.fY;
+    io.fN[0] = (const double*)(wb + RL.fN);
+    rc = SCRF_DISPATCH(precision, run_sweep)(p, (int64_t)1 << 30, io, st);
+    if (rc) return rc;
+  }
+  const size_t total = (size_t)B * (t1 - t0 + 1) * C;
+  ++g_launches;
+  if (precision)
+    ra_block_kernel<double><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        omega_i, p->lengths, B, K, C, t0, t1, tf0, RL.rows, (const double*)(wb + RL.oY), (const double*)(wb + RL.on),
+        block);
+  else
+    ra_block_kernel<float><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        omega_i, p->lengths, B, K, C, t0, t1, tf0, RL.rows, (const float*)(wb + RL.oY), (const double*)(wb + RL.on),
+        block);
   return (int)cudaGetLastError();
 }
 

@@ -40,19 +40,23 @@ struct CutArgs {
   const double* pe;
   const double* logZ;  // (B,) nats
   int B, T, K, C;
-  const R *Ya, *Xa, *Yb, *Xb;  // [B][T+1][C]
-  const double *na, *nb;       // [B][T+1]
+  const R *Ya, *Xa, *Yb, *Xb;  // message rows as in PostArgs (alpha b*rowsA + t - tA0, beta b*rowsB + t - tB0)
+  const double *na, *nb;
+  int rowsA, tA0, rowsB, tB0;
+  int w0, w1;                  // positions of this pass
   int d;                       // cut spacing
-  int ncut;                    // cut slots per sequence: 0, d, 2d, ..., and L (last used slot)
+  int ncut;                    // cut slots per sequence: w0, w0 + d, ..., and min(w1, L) (last used slot)
   double* U;                   // [B][ncut][C] per-label contributions to U_t
 };
 
-// cut slot j of sequence with length L: t_j = j * d for j <= J = (L - 1) / d, t_{J+1} = L
-__host__ __device__ inline int cut_count(int L, int d) { return (L - 1) / d + 2; }
-__host__ __device__ inline int cut_pos(int j, int L, int d) {
-  const int J = (L - 1) / d;
-  return j <= J ? j * d : L;
+// cut slots of a pass [w0, w1) for a sequence of length L: t_j = w0 + j d for j <= J =
+// (tend - 1 - w0) / d, t_{J+1} = tend = min(w1, L)
+__host__ __device__ inline int cut_J(int w0, int tend, int d) { return tend > w0 ? (tend - 1 - w0) / d : 0; }
+__host__ __device__ inline int cut_count(int w0, int tend, int d) { return cut_J(w0, tend, d) + 2; }
+__host__ __device__ inline int cut_pos(int j, int w0, int tend, int d) {
+  return j <= cut_J(w0, tend, d) ? w0 + j * d : tend;
 }
+__host__ __device__ inline int cut_slots(int w0, int w1, int d) { return d > 0 ? (w1 - w0 - 1) / d + 2 : 0; }
 
 template <typename R>
 __host__ __device__ inline size_t cut_smem(int K) {
@@ -90,11 +94,15 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
   const int j = blockIdx.x, cg = blockIdx.y, b = blockIdx.z;
   const int C = a.C, T = a.T, K = a.K;
   const int L = (int)a.lengths[b];
-  if (j >= cut_count(L, a.d)) return;
-  const int t = cut_pos(j, L, a.d);
+  if (L < a.w0) return;
+  const int tend = min(a.w1, L);
+  if (j >= cut_count(a.w0, tend, a.d)) return;
+  const int t = cut_pos(j, a.w0, tend, a.d);
   const int c0 = cg * kCutCG;
   const int Cn = min(kCutCG, C - c0);
   const size_t rb0 = (size_t)b * (T + 1);
+  const size_t ra0 = (size_t)b * a.rowsA - a.tA0;  // alpha row of t: ra0 + t
+  const size_t rbb = (size_t)b * a.rowsB - a.tB0;  // beta row of t: rbb + t
   const double Z2 = a.logZ[b] * kLog2e;
   const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC;
   float* sa = (float*)sm;                  // [CG][NA]   a[s], s = t-K+1+i
@@ -106,10 +114,10 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
     // point term: E[t,c] (interior, t = L) or A[0,c] (t = 0), fp64
     double pt = 0.0;
     if (threadIdx.x == 0) {
-      const size_t o = (rb0 + t) * C + c;
-      const double f = a.na[rb0 + t] + a.nb[rb0 + t] - Z2;
-      const R y = t == 0 ? a.Xa[o] : a.Ya[o];
-      const R x = t == 0 ? a.Yb[o] : a.Xb[o];
+      const size_t oa = (ra0 + t) * C + c, ob = (rbb + t) * C + c;
+      const double f = a.na[ra0 + t] + a.nb[rbb + t] - Z2;
+      const R y = t == 0 ? a.Xa[oa] : a.Ya[oa];
+      const R x = t == 0 ? a.Yb[ob] : a.Xb[ob];
       if (y > Mth<R>::ninf() && x > Mth<R>::ninf()) pt = exp2(f + (double)y + (double)x);
     }
     double cross = 0.0;
@@ -120,9 +128,9 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
         const int s = s_lo + i;
         if (s >= 0) {
           const size_t o = (rb0 + s) * C + c;
-          const R xa = a.Xa[o];
+          const R xa = a.Xa[(ra0 + s) * C + c];
           if (xa > Mth<R>::ninf()) {
-            const double ra = a.na[rb0 + s] + (double)xa - a.S[o] * kLog2e +
+            const double ra = a.na[ra0 + s] + (double)xa - a.S[o] * kLog2e +
                               ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
             ra_max = fmax(ra_max, ra);
           }
@@ -130,9 +138,9 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
         const int e = t + 1 + i;
         if (e <= L) {
           const size_t o = (rb0 + e) * C + c;
-          const R xb = a.Xb[o];
+          const R xb = a.Xb[(rbb + e) * C + c];
           if (xb > Mth<R>::ninf()) {
-            const double rv = a.nb[rb0 + e] + (double)xb + a.S[o] * kLog2e +
+            const double rv = a.nb[rbb + e] + (double)xb + a.S[o] * kLog2e +
                               (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
             rb_max = fmax(rb_max, rv);
           }
@@ -151,9 +159,9 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
         float v = 0.f;
         if (live && i < K - 1 && s >= 0) {
           const size_t o = (rb0 + s) * C + c;
-          const R xa = a.Xa[o];
+          const R xa = a.Xa[(ra0 + s) * C + c];
           if (xa > Mth<R>::ninf()) {
-            const double ra = a.na[rb0 + s] + (double)xa - a.S[o] * kLog2e +
+            const double ra = a.na[ra0 + s] + (double)xa - a.S[o] * kLog2e +
                               ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
             v = exp2f((float)(ra - ra_max));
           }
@@ -165,9 +173,9 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
         float v = 0.f;
         if (live && i < K - 1 && e <= L) {
           const size_t o = (rb0 + e) * C + c;
-          const R xb = a.Xb[o];
+          const R xb = a.Xb[(rbb + e) * C + c];
           if (xb > Mth<R>::ninf()) {
-            const double rv = a.nb[rb0 + e] + (double)xb + a.S[o] * kLog2e +
+            const double rv = a.nb[rbb + e] + (double)xb + a.S[o] * kLog2e +
                               (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
             v = exp2f((float)(rv - rb_max));
           }
@@ -230,61 +238,65 @@ __device__ __forceinline__ double cut_log2U(const double* U, int C) {
 
 namespace scrf {
 
-// per-position log2 correction corr[b][t] = -lerp(log2 U) between the enclosing cut slots
-// (0 past L); grid (chunks of 256 positions, B)
-// Also counts the beta positions whose (absolute, unnormalised in the reference) message
-// max leaves +-CLAMP_LIMIT (the reference would clamp them, _numerics.py:41-56).
+// per-position log2 correction corr[b][t - w0] = -lerp(log2 U) between the enclosing cut slots
+// (0 past L); grid (chunks of 256 positions of [w0, w1), B). Also counts the beta positions
+// whose (absolute, unnormalised in the reference) message max leaves +-CLAMP_LIMIT (the
+// reference would clamp them, _numerics.py:41-56).
 template <typename R>
-__global__ void __launch_bounds__(256) cut_corr_kernel(const int64_t* lengths, int T, int C, int d, int ncut,
+__global__ void __launch_bounds__(256) cut_corr_kernel(const int64_t* lengths, int C, int w0, int w1, int d, int ncut,
                                                        const double* U, double* corr, const R* Xb, const double* nb,
-                                                       int32_t* clampB) {
+                                                       int rowsB, int tB0, int32_t* clampB) {
   const int b = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > T) return;
+  const int t = w0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= w1) return;
   const int L = (int)lengths[b];
-  const size_t rt = (size_t)b * (T + 1) + t;
   if (clampB && t < L) {
+    const size_t rt = (size_t)b * rowsB + t - tB0;
     R m = Mth<R>::ninf();
     for (int c = 0; c < C; ++c) m = fmax(m, Xb[rt * C + c]);
     if (m > Mth<R>::ninf() && fabs((nb[rt] + (double)m) * kLn2) > kClampLimit) atomicAdd(&clampB[b], 1);
   }
   double v = 0.0;
   if (d > 0 && t <= L) {
-    const int J = (L - 1) / d;
-    const int j = t >= J * d ? J : t / d;
-    const int t0 = cut_pos(j, L, d), t1 = cut_pos(j + 1, L, d);
+    const int tend = min(w1, L);
+    const int J = cut_J(w0, tend, d);
+    const int j = min((t - w0) / d, J);
+    const int t0 = cut_pos(j, w0, tend, d), t1 = cut_pos(j + 1, w0, tend, d);
     const double* Ub = U + (size_t)b * ncut * C;
     const double l0 = cut_log2U(Ub + (size_t)j * C, C);
     const double l1 = cut_log2U(Ub + (size_t)(j + 1) * C, C);
     const double f = t1 > t0 ? (double)(t - t0) / (double)(t1 - t0) : 0.0;
     v = -(l0 + (l1 - l0) * f);
   }
-  if (corr) corr[(size_t)b * (T + 1) + t] = v;
+  if (corr) corr[(size_t)b * (w1 - w0) + t - w0] = v;
 }
 
 }  // namespace scrf
 
 namespace scrf {
 
-// Exclusive prefix of the coverage chunk totals, re-anchored at every interior cut point:
-// the coverage of cell t_j - 1 is exactly E[t_j,c] + (segments of label c crossing t_j), the
-// per-label cut contribution U[b][j][c] (divided by the cut total, the frame correction at
+// Exclusive prefix of the coverage chunk totals of a pass [w0, w1), re-anchored at every cut
+// point: the coverage of cell t_j - 1 is exactly E[t_j,c] + (segments of label c crossing t_j),
+// the per-label cut contribution U[b][j][c] (divided by the cut total, the frame correction at
 // t_j), so the running sum restarts there and fp32 rounding accumulates over <= d positions
-// only. Chunk starts coincide with cut points (CH divides d). One thread per (b, c).
-__global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch, int CH, int d, int ncut,
-                                  const double* U, double* tot) {
+// only. Chunk starts coincide with cut points (CH divides d). The first chunk starts from the
+// anchor at w0 (0 at w0 = 0; the running coverage of the previous pass if the anchor is not
+// sane); the coverage at the end of the pass is left in carry[b][c]. One thread per (b, c).
+__global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch, int CH, int w0, int w1, int d,
+                                  int ncut, const double* U, double* tot, double* carry) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * C) return;
   const int b = i / C, c = i % C;
   const int L = (int)lengths[b];
-  const int J = (L - 1) / d;
+  const int tend = min(w1, L);
+  const int J = cut_J(w0, tend, d);
   const double* Ub = U + (size_t)b * ncut * C;
   double* base = tot + (size_t)b * nch * C + c;
-  double run = 0.0;
+  double run = (w0 == 0 || !carry) ? 0.0 : carry[(size_t)b * C + c];
   for (int q = 0; q < nch; ++q) {
-    const int t0 = q * CH;
-    if (t0 > 0 && t0 % d == 0 && t0 / d <= J) {
-      const int j = t0 / d;
+    const int t0 = w0 + q * CH;
+    if (t0 > 0 && t0 < tend && (t0 - w0) % d == 0 && (t0 - w0) / d <= J) {
+      const int j = (t0 - w0) / d;
       double s = 0.0;
       for (int cc = 0; cc < C; ++cc) s += Ub[(size_t)j * C + cc];
       const double l = s > 0.0 ? log2(s) : 1.0;
@@ -294,6 +306,7 @@ __global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch,
     base[(size_t)q * C] = run;
     run += v;
   }
+  if (carry) carry[(size_t)b * C + c] = run;
 }
 
 }  // namespace scrf

@@ -27,9 +27,11 @@ struct PostArgs {
   const double* upstream;  // (B,) or null
   const double* logZ;      // (B,) nats
   int B, T, K, C;
-  const R *Ya, *Xa, *Yb, *Xb;  // [B][T+1][C]
-  const double *na, *nb;       // [B][T+1]
-  const double* corr;          // [B][T+1] log2 frame correction from the cut normalisers (scrf_cut.cuh) or null
+  const R *Ya, *Xa, *Yb, *Xb;  // message rows: alpha side b*rowsA + t - tA0, beta side b*rowsB + t - tB0
+  const double *na, *nb;
+  int rowsA, tA0, rowsB, tB0;
+  int w0, w1;                  // positions [w0, w1) of this pass (full mode: [0, T+1))
+  const double* corr;          // [B][w1-w0] log2 frame correction from the cut normalisers (scrf_cut.cuh) or null
   // outputs
   double* grad_S;  // (B, T+1, C)
   double* grad_Ps; // (B, T, C) or null
@@ -37,14 +39,19 @@ struct PostArgs {
   double* pos;     // (B, T, C)
   double* bnd;     // (B, T)
   // chunk partials
-  int CH, nch;        // positions per chunk, chunks per sequence
+  int CH, nch;        // positions per chunk, chunks per sequence in [w0, w1)
   double* tot;        // [B][nch][C]  chunk totals of (A - E)
   double* cntp;       // [B][nch]
   double* gTp;        // [B][nch][C][C]
-  int SCB, nchB;      // grad_B: sources per CTA, CTAs per sequence
+  int SCB, nchB;      // grad_B: sources per CTA, CTAs per sequence (sources in [w0, w1))
   int CGB;            // labels per grad_B CTA
   double* gBp;        // [B][nchB][K][C]
 };
+
+template <typename R>
+__device__ __forceinline__ size_t rowA(const PostArgs<R>& a, int b, int t) { return (size_t)b * a.rowsA + (t - a.tA0); }
+template <typename R>
+__device__ __forceinline__ size_t rowB(const PostArgs<R>& a, int b, int t) { return (size_t)b * a.rowsB + (t - a.tB0); }
 
 __host__ __device__ inline int post_chunk(int C) {
   int ch = 256;
@@ -60,8 +67,8 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
   const int b = blockIdx.y, ch = blockIdx.x;
   const int C = a.C, T = a.T, CH = a.CH;
   const int L = (int)a.lengths[b];
-  const int t0 = ch * CH;
-  const int nt = min(CH, T + 1 - t0);
+  const int t0 = a.w0 + ch * CH;
+  const int nt = min(CH, a.w1 - t0);
   double* dA = (double*)sm;                 // [CH][C] start mass
   double* dE = dA + (size_t)CH * C;         // [CH][C] end mass
   R* sYa = (R*)(dE + (size_t)CH * C);       // [CH][C]
@@ -71,9 +78,11 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
   const double Z2 = a.logZ[b] * kLog2e;
   const double up = a.upstream ? a.upstream[b] : 1.0;
   const size_t rb = (size_t)b * (T + 1);
+  const int W = a.w1 - a.w0;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
     const int t = t0 + i;
-    sf[i] = (t <= L) ? a.na[rb + t] + a.nb[rb + t] - Z2 + (a.corr ? a.corr[rb + t] : 0.0) : 0.0;
+    sf[i] = (t <= L) ? a.na[rowA(a, b, t)] + a.nb[rowB(a, b, t)] - Z2 + (a.corr ? a.corr[(size_t)b * W + t - a.w0] : 0.0)
+                     : 0.0;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < nt * C; e += blockDim.x) {
@@ -82,13 +91,14 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
     double A = 0.0, E = 0.0;
     R ya = Mth<R>::ninf(), yb = Mth<R>::ninf();
     if (t <= L) {
+      const size_t oa = rowA(a, b, t) * C + c, ob = rowB(a, b, t) * C + c;
       const R f = (R)sf[i];
-      ya = a.Ya[o];
+      ya = a.Ya[oa];
       if (t < L) {
-        yb = a.Yb[o];
-        A = (double)Mth<R>::ex2(f + a.Xa[o] + yb);
+        yb = a.Yb[ob];
+        A = (double)Mth<R>::ex2(f + a.Xa[oa] + yb);
       }
-      if (t >= 1) E = (double)Mth<R>::ex2(f + ya + a.Xb[o]);
+      if (t >= 1) E = (double)Mth<R>::ex2(f + ya + a.Xb[ob]);
     }
     dA[e] = A;
     dE[e] = E;
@@ -178,24 +188,25 @@ __global__ void __launch_bounds__(256) post_prefix_kernel(int B, int C, int nch,
 
 // pass 2: add the carry of the preceding chunks (tot holds exclusive prefixes after
 // post_prefix_kernel) to the local coverage, clip, zero padding
-__global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, int CH, int nch, const double* tot,
-                                  double* __restrict__ pos) {
+__global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, int CH, int nch, int w0, int w1,
+                                  const double* tot, double* __restrict__ pos) {
   const int b = blockIdx.y, ch = blockIdx.x;
   const int L = (int)lengths[b];
+  const int tend = min(w1, T);
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const double carry = tot[((size_t)b * nch + ch) * C + c];
-    const int t0 = ch * CH;
+    const int t0 = w0 + ch * CH;
     for (int i = 0; i < CH; i += 4) {
       double v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = t0 + i + j;
-        v[j] = (i + j < CH && t < T) ? pos[((size_t)b * T + t) * C + c] : 0.0;
+        v[j] = (i + j < CH && t < tend) ? pos[((size_t)b * T + t) * C + c] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = t0 + i + j;
-        if (i + j < CH && t < T) pos[((size_t)b * T + t) * C + c] = (t < L) ? fmin(fmax(v[j] + carry, 0.0), 1.0) : 0.0;
+        if (i + j < CH && t < tend) pos[((size_t)b * T + t) * C + c] = (t < L) ? fmin(fmax(v[j] + carry, 0.0), 1.0) : 0.0;
       }
     }
   }
@@ -241,8 +252,9 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
   for (int w = 0; w < kGBW; ++w)
 #pragma unroll
     for (int j = 0; j < kGBJ; ++j) acc[w][j] = 0.0;
-  const int sbeg = sb * a.SCB;
-  const int send = min(sbeg + a.SCB, L);  // sources s < L
+  const int sbeg = a.w0 + sb * a.SCB;
+  const int send = min(min(sbeg + a.SCB, a.w1), L);  // sources s < L in [w0, w1)
+  const int W = a.w1 - a.w0;
   __syncthreads();
   for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
     __syncthreads();
@@ -254,8 +266,10 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       v.y = 0;
       if (si < ns) {
         const size_t o = (rb0 + s) * C + c;
-        const double ra = a.na[rb0 + s] + (double)a.Xa[o] - a.S[o] * kLog2e +
-                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
+        const size_t oa = rowA(a, b, s);
+        const double ra = a.na[oa] + (double)a.Xa[oa * C + c] - a.S[o] * kLog2e +
+                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0) +
+                          (a.corr ? a.corr[(size_t)b * W + s - a.w0] : 0.0);
         split2(ra, v.x, v.y);
       }
       sa[(size_t)cl * kGBSub + si] = v;
@@ -267,9 +281,9 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       v.y = 0;
       if (u <= L && ui < kGBSub + K) {
         const size_t o = (rb0 + u) * C + c;
-        const double rv = a.nb[rb0 + u] + (double)a.Xb[o] + a.S[o] * kLog2e +
-                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2 +
-                          (a.corr ? a.corr[rb0 + u] : 0.0);
+        const size_t ob = rowB(a, b, u);
+        const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +
+                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
         split2(rv, v.x, v.y);
       }
       sbv[(size_t)cl * rowU + gb_skew(ui)] = v;

@@ -474,8 +474,10 @@ __host__ __device__ inline int ck_ttop(int j, int W, int K, int L) {
   const int need = j * W + K - 1;
   return need >= L ? L : L - 32 * ((L - need) / 32);
 }
+// alpha rows per sequence: t = 0, the last mA positions of every delta-period, and the last mA
+// positions before L (the ring the reference holds past L, for the checkpoint view)
 __host__ __device__ inline long long ck_rows_alpha(int T, int delta, int mA) {
-  return 1 + (long long)((T + delta - 1) / delta) * mA;
+  return 1 + (long long)((T + delta - 1) / delta) * mA + mA;
 }
 __device__ __forceinline__ long long ck_row(int dir, int t, int L, int K, int delta, int mA, int W) {
   if (dir == 0) {
@@ -641,14 +643,21 @@ __device__ __forceinline__ long long out_row(const SweepArgs<R>& a, const SweepC
 template <typename R>
 __device__ __forceinline__ void put_out(const SweepArgs<R>& a, const SweepCtx& x, int t, int c, bool act, R y, R xv,
                                         double n) {
-  const long long row = out_row(a, x, t);
-  if (row < 0) return;
   const int C = a.C;
-  if (act) {
-    a.Y[x.dir][row * C + c] = y;
-    if (a.X[x.dir]) a.X[x.dir][row * C + c] = xv;
+  const long long row = out_row(a, x, t);
+  if (row >= 0) {
+    if (act) {
+      a.Y[x.dir][row * C + c] = y;
+      if (a.X[x.dir]) a.X[x.dir][row * C + c] = xv;
+    }
+    if (c == 0) a.n[x.dir][row] = n;
   }
-  if (c == 0) a.n[x.dir][row] = n;
+  if (a.store == 1 && !x.task && x.dir == 0 && t > x.Lb - a.mA) {  // final-ring rows of the checkpoint view
+    const long long r2 = (long long)x.b * ck_rows_alpha(a.T, a.delta, a.mA) + 1 +
+                         (long long)((a.T + a.delta - 1) / a.delta) * a.mA + (t - (x.Lb - a.mA + 1));
+    if (act) a.Y[0][r2 * C + c] = y;
+    if (c == 0) a.n[0][r2] = n;
+  }
 }
 
 // edge-batch state of one label: Q of the four positions before the next batch's targets and

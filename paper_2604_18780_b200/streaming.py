@@ -192,6 +192,9 @@ class DeviceProblem:
         )
 
 
+MEMORY_MODES = ("full", "sublinear")
+
+
 @dataclass
 class DeviceForward:
     logZ: torch.Tensor  # (B,) fp64
@@ -200,34 +203,51 @@ class DeviceForward:
     ckpt: torch.Tensor  # opaque uint8 buffer
     delta: int
     precision: str
+    sparse: bool = False  # True: checkpoint rows only (sublinear memory), False: every position
 
 
-def device_forward(prob: DeviceProblem, delta: int | None = None, precision: str | None = None) -> DeviceForward:
-    """Forward pass on the current stream; no host synchronisation."""
-    lib = _lib.load()
-    precision = precision or _default_precision
-    prec = PRECISIONS[precision]
+def _check_delta(prob: DeviceProblem, delta) -> int:
     delta = choose_checkpoint_interval(prob.T, prob.K) if delta is None else int(delta)
     if delta < 1:
         raise ValueError(f"checkpoint interval must be >= 1, got {delta}")
+    return delta
+
+
+def _forward_buffers(prob: DeviceProblem, delta: int, prec: int, sparse: bool):
+    lib = _lib.load()
     p = prob.c_struct()
     nbytes = ctypes_size()
-    _lib.check(lib.scrf_checkpoint_bytes(p, delta, prec, nbytes), "scrf_checkpoint_bytes")
+    q = lib.scrf_sparse_checkpoint_bytes if sparse else lib.scrf_checkpoint_bytes
+    _lib.check(q(p, delta, prec, nbytes), "checkpoint_bytes")
     dev = prob.S.device
     n_ckpt = -(-prob.T // delta)
-    ckpt = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
-    logZ = torch.empty(prob.B, dtype=torch.float64, device=dev)
-    N = torch.empty((prob.B, n_ckpt), dtype=torch.float64, device=dev)
-    dead = torch.empty(prob.B, dtype=torch.int32, device=dev)
-    rc = lib.scrf_forward(p, delta, prec, _lib.ptr(logZ), _lib.ptr(N), _lib.ptr(dead), _lib.ptr(ckpt), nbytes.value,
-                          _lib.stream_handle())
+    return (torch.empty(prob.B, dtype=torch.float64, device=dev),
+            torch.empty((prob.B, n_ckpt), dtype=torch.float64, device=dev),
+            torch.empty(prob.B, dtype=torch.int32, device=dev),
+            torch.empty(nbytes.value, dtype=torch.uint8, device=dev))
+
+
+def device_forward(prob: DeviceProblem, delta: int | None = None, precision: str | None = None,
+                   sparse: bool = False) -> DeviceForward:
+    """Forward pass on the current stream; no host synchronisation.
+
+    sparse=False keeps every position's messages (fast backward, linear memory);
+    sparse=True keeps only the checkpoint rows -- the reference's CheckpointSet
+    (streaming.py:49-67) plus replay warm-up rows, O(sqrt(T K) C) -- and the backward
+    recomputes alpha between checkpoints (streaming.py:232-261)."""
+    lib = _lib.load()
+    precision = precision or _default_precision
+    prec = PRECISIONS[precision]
+    delta = _check_delta(prob, delta)
+    logZ, N, dead, ckpt = _forward_buffers(prob, delta, prec, sparse)
+    fn = lib.scrf_forward_sparse if sparse else lib.scrf_forward
+    rc = fn(prob.c_struct(), delta, prec, _lib.ptr(logZ), _lib.ptr(N), _lib.ptr(dead), _lib.ptr(ckpt), ckpt.numel(),
+            _lib.stream_handle())
     _lib.check(rc, "scrf_forward")
-    return DeviceForward(logZ, N, dead, ckpt, delta, precision)
+    return DeviceForward(logZ, N, dead, ckpt, delta, precision, sparse)
 
 
 def ctypes_size():
-    import ctypes
-
     return ctypes.c_size_t(0)
 
 
@@ -242,30 +262,38 @@ class DeviceBackward:
     boundary_posterior: torch.Tensor
     expected_segment_count: torch.Tensor
     work: torch.Tensor
+    sparse: bool = False
+    delta: int = 0
 
 
 def device_backward(prob: DeviceProblem, fwd: DeviceForward, upstream: torch.Tensor | None = None,
                     want_proj_grads: bool | None = None) -> DeviceBackward:
+    """Backward from a device forward (its memory mode decides: a sparse forward is followed
+    by the checkpoint-replay backward)."""
     lib = _lib.load()
     prec = PRECISIONS[fwd.precision]
     p = prob.c_struct()
-    bw = _alloc_backward(prob, prec, fwd.delta, want_proj_grads)
+    bw = _alloc_backward(prob, prec, fwd.delta, want_proj_grads, fwd.sparse)
     if upstream is not None:
         upstream = upstream.to(device=prob.S.device, dtype=torch.float64).contiguous()
-    rc = lib.scrf_backward(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.ckpt), _lib.ptr(upstream),
-                           _lib.ptr(bw.grad_S), _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B), _lib.ptr(bw.grad_P_start),
-                           _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals), _lib.ptr(bw.boundary_posterior),
-                           _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work), bw.work.numel(),
-                           _lib.stream_handle())
+    outs = (_lib.ptr(bw.grad_S), _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B), _lib.ptr(bw.grad_P_start),
+            _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals), _lib.ptr(bw.boundary_posterior),
+            _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work), bw.work.numel(), _lib.stream_handle())
+    if fwd.sparse:
+        rc = lib.scrf_backward_sparse(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.N), _lib.ptr(fwd.ckpt),
+                                      _lib.ptr(upstream), *outs)
+    else:
+        rc = lib.scrf_backward(p, fwd.delta, prec, _lib.ptr(fwd.logZ), _lib.ptr(fwd.ckpt), _lib.ptr(upstream), *outs)
     _lib.check(rc, "scrf_backward")
     return bw
 
 
-def _alloc_backward(prob: DeviceProblem, prec: int, delta: int, want_proj_grads: bool | None):
+def _alloc_backward(prob: DeviceProblem, prec: int, delta: int, want_proj_grads: bool | None, sparse: bool = False):
     lib = _lib.load()
     p = prob.c_struct()
     nbytes = ctypes_size()
-    _lib.check(lib.scrf_backward_work_bytes(p, delta, prec, nbytes), "scrf_backward_work_bytes")
+    q = lib.scrf_sparse_backward_work_bytes if sparse else lib.scrf_backward_work_bytes
+    _lib.check(q(p, delta, prec, nbytes), "backward_work_bytes")
     dev = prob.S.device
     B, T, K, C = prob.B, prob.T, prob.K, prob.C
     f64 = dict(dtype=torch.float64, device=dev)
@@ -278,36 +306,36 @@ def _alloc_backward(prob: DeviceProblem, prec: int, delta: int, want_proj_grads:
         grad_P_end=torch.empty((B, T, C), **f64) if want_proj_grads and prob.proj_end is not None else None,
         position_marginals=torch.empty((B, T, C), **f64), boundary_posterior=torch.empty((B, T), **f64),
         expected_segment_count=torch.empty((B,), **f64),
-        work=torch.empty(nbytes.value, dtype=torch.uint8, device=dev))
+        work=torch.empty(nbytes.value, dtype=torch.uint8, device=dev), sparse=sparse, delta=delta)
 
 
 def device_posterior(prob: DeviceProblem, delta: int | None = None, upstream: torch.Tensor | None = None,
-                     precision: str | None = None, want_proj_grads: bool | None = None):
-    """Forward + backward in one call (alpha and beta sweeps run concurrently); no host sync."""
+                     precision: str | None = None, want_proj_grads: bool | None = None, memory: str = "full"):
+    """Forward + backward in one call (alpha and beta sweeps run concurrently); no host sync.
+
+    memory="full": every position's messages are kept (fastest; O(T C) working memory).
+    memory="sublinear": checkpoint rows only; alpha and beta are replayed window by window from
+    them (streaming.py:232-261), O(sqrt(T K) C) working memory besides the
+    O(T C) inputs and outputs."""
+    if memory not in MEMORY_MODES:
+        raise ValueError(f"memory must be one of {MEMORY_MODES}")
+    sparse = memory == "sublinear"
     lib = _lib.load()
     precision = precision or _default_precision
     prec = PRECISIONS[precision]
-    delta = choose_checkpoint_interval(prob.T, prob.K) if delta is None else int(delta)
-    if delta < 1:
-        raise ValueError(f"checkpoint interval must be >= 1, got {delta}")
+    delta = _check_delta(prob, delta)
     p = prob.c_struct()
-    nbytes = ctypes_size()
-    _lib.check(lib.scrf_checkpoint_bytes(p, delta, prec, nbytes), "scrf_checkpoint_bytes")
     dev = prob.S.device
-    n_ckpt = -(-prob.T // delta)
-    fwd = DeviceForward(torch.empty(prob.B, dtype=torch.float64, device=dev),
-                        torch.empty((prob.B, n_ckpt), dtype=torch.float64, device=dev),
-                        torch.empty(prob.B, dtype=torch.int32, device=dev),
-                        torch.empty(nbytes.value, dtype=torch.uint8, device=dev), delta, precision)
-    bw = _alloc_backward(prob, prec, delta, want_proj_grads)
+    fwd = DeviceForward(*_forward_buffers(prob, delta, prec, sparse), delta, precision, sparse)
+    bw = _alloc_backward(prob, prec, delta, want_proj_grads, sparse)
     if upstream is not None:
         upstream = upstream.to(device=dev, dtype=torch.float64).contiguous()
-    rc = lib.scrf_posterior(p, delta, prec, _lib.ptr(upstream), _lib.ptr(fwd.logZ), _lib.ptr(fwd.N),
-                            _lib.ptr(fwd.dead_at), _lib.ptr(fwd.ckpt), fwd.ckpt.numel(), _lib.ptr(bw.grad_S),
-                            _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B), _lib.ptr(bw.grad_P_start),
-                            _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals),
-                            _lib.ptr(bw.boundary_posterior), _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work),
-                            bw.work.numel(), _lib.stream_handle())
+    fn = lib.scrf_posterior_sparse if sparse else lib.scrf_posterior
+    rc = fn(p, delta, prec, _lib.ptr(upstream), _lib.ptr(fwd.logZ), _lib.ptr(fwd.N), _lib.ptr(fwd.dead_at),
+            _lib.ptr(fwd.ckpt), fwd.ckpt.numel(), _lib.ptr(bw.grad_S), _lib.ptr(bw.grad_T), _lib.ptr(bw.grad_B),
+            _lib.ptr(bw.grad_P_start), _lib.ptr(bw.grad_P_end), _lib.ptr(bw.position_marginals),
+            _lib.ptr(bw.boundary_posterior), _lib.ptr(bw.expected_segment_count), _lib.ptr(bw.work),
+            bw.work.numel(), _lib.stream_handle())
     _lib.check(rc, "scrf_posterior")
     return fwd, bw
 
@@ -316,8 +344,13 @@ def device_beta_logz(prob: DeviceProblem, fwd: DeviceForward, bw: DeviceBackward
     """logZ recomputed from the beta sweep (consistency check of the two sweeps)."""
     lib = _lib.load()
     out = torch.empty(prob.B, dtype=torch.float64, device=prob.S.device)
-    _lib.check(lib.scrf_beta_logz(prob.c_struct(), PRECISIONS[fwd.precision], _lib.ptr(bw.work), _lib.ptr(out),
-                                  _lib.stream_handle()), "scrf_beta_logz")
+    prec = PRECISIONS[fwd.precision]
+    if bw.sparse:
+        rc = lib.scrf_beta_logz_sparse(prob.c_struct(), bw.delta, prec, _lib.ptr(bw.work), _lib.ptr(out),
+                                       _lib.stream_handle())
+    else:
+        rc = lib.scrf_beta_logz(prob.c_struct(), prec, _lib.ptr(bw.work), _lib.ptr(out), _lib.stream_handle())
+    _lib.check(rc, "scrf_beta_logz")
     return out
 
 
@@ -327,10 +360,40 @@ def device_grad_partials(prob: DeviceProblem, fwd: DeviceForward, bwd: DeviceBac
     dev = prob.S.device
     gT = torch.empty((prob.B, prob.C, prob.C), dtype=torch.float64, device=dev)
     gB = torch.empty((prob.B, prob.K, prob.C), dtype=torch.float64, device=dev)
-    rc = lib.scrf_backward_partials(prob.c_struct(), fwd.delta, PRECISIONS[fwd.precision], _lib.ptr(bwd.work),
-                                    _lib.ptr(gT), _lib.ptr(gB), _lib.stream_handle())
+    fn = lib.scrf_backward_partials_sparse if bwd.sparse else lib.scrf_backward_partials
+    rc = fn(prob.c_struct(), fwd.delta, PRECISIONS[fwd.precision], _lib.ptr(bwd.work), _lib.ptr(gT), _lib.ptr(gB),
+            _lib.stream_handle())
     _lib.check(rc, "scrf_backward_partials")
     return gT, gB
+
+
+def device_omega(prob: DeviceProblem, fwd: DeviceForward) -> torch.Tensor:
+    """The reference-format checkpoint snapshots omega (B, n_ckpt, K, C), fp64, on the device."""
+    lib = _lib.load()
+    out = torch.empty((prob.B, fwd.N.shape[1], prob.K, prob.C), dtype=torch.float64, device=prob.S.device)
+    fn = lib.scrf_export_checkpoints_sparse if fwd.sparse else lib.scrf_export_checkpoints
+    rc = fn(prob.c_struct(), fwd.delta, PRECISIONS[fwd.precision], _lib.ptr(fwd.ckpt), _lib.ptr(fwd.N), _lib.ptr(out),
+            _lib.stream_handle())
+    _lib.check(rc, "scrf_export_checkpoints")
+    return out
+
+
+def device_recompute_alpha(prob: DeviceProblem, omega_i: torch.Tensor, t_start: int, t_end: int,
+                           precision: str | None = None) -> torch.Tensor:
+    """recompute_alpha on the device: (B, t_end - t_start + 1, C) fp64 in the snapshot frame."""
+    lib = _lib.load()
+    prec = PRECISIONS[precision or _default_precision]
+    p = prob.c_struct()
+    nbytes = ctypes_size()
+    _lib.check(lib.scrf_recompute_alpha_work_bytes(p, t_start, t_end, prec, nbytes), "scrf_recompute_alpha_work_bytes")
+    dev = prob.S.device
+    work = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    omega_i = omega_i.to(device=dev, dtype=torch.float64).contiguous()
+    block = torch.empty((prob.B, t_end - t_start + 1, prob.C), dtype=torch.float64, device=dev)
+    rc = lib.scrf_recompute_alpha(p, prec, _lib.ptr(omega_i), t_start, t_end, _lib.ptr(block), _lib.ptr(work),
+                                  nbytes.value, _lib.stream_handle())
+    _lib.check(rc, "scrf_recompute_alpha")
+    return block
 
 
 @dataclass
@@ -366,14 +429,18 @@ def device_viterbi(prob: DeviceProblem) -> DeviceViterbi:
 class CheckpointSet:
     """Ring snapshots at every renormalisation boundary (streaming.py:49-67).
 
-    Holds the opaque device checkpoint buffer the backward consumes; the
-    reference-format views `omega` (B, n_ckpt, K, C) and `N` (B, n_ckpt) are
-    materialised on first access.
+    Produced by `streaming_forward`, which keeps ONLY the checkpoint rows on the device (the
+    last min(K+32, delta) alpha messages of every delta-period: the reference's snapshots
+    plus the warm-up of a replay window) -- O(sqrt(T K) C) memory. `omega` (B, n_ckpt, K, C)
+    and `N` (B, n_ckpt) are the reference-format views (materialised on first access);
+    `streaming_backward` replays alpha between checkpoints from the device rows.
     """
 
-    def __init__(self, prob: DeviceProblem, fwd: DeviceForward):
+    def __init__(self, prob: DeviceProblem, fwd: DeviceForward, cum=None, params=None):
         self._prob = prob
         self._fwd = fwd
+        self._cum = cum
+        self._params = params
         self.delta = fwd.delta
         self._omega = None
         self._N = None
@@ -391,15 +458,11 @@ class CheckpointSet:
     @property
     def omega(self) -> np.ndarray:
         if self._omega is None:
-            lib = _lib.load()
-            pr = self._prob
-            out = torch.empty((pr.B, self.n_checkpoints, pr.K, pr.C), dtype=torch.float64, device=pr.S.device)
-            rc = lib.scrf_export_checkpoints(pr.c_struct(), self.delta, PRECISIONS[self._fwd.precision],
-                                             _lib.ptr(self._fwd.ckpt), _lib.ptr(self._fwd.N), _lib.ptr(out),
-                                             _lib.stream_handle())
-            _lib.check(rc, "scrf_export_checkpoints")
-            self._omega = out.cpu().numpy()
+            self._omega = device_omega(self._prob, self._fwd).cpu().numpy()
         return self._omega
+
+    def device_bytes(self) -> int:
+        return int(self._fwd.ckpt.numel())
 
 
 def _check_labels(cum: CumulativeScores, params: SemiCRFParams) -> None:
@@ -412,8 +475,13 @@ def device_clamp_events(prob: DeviceProblem, fwd: DeviceForward, bw: "DeviceBack
     (alpha from the forward, plus beta when `bw` is given); no host sync."""
     lib = _lib.load()
     out = torch.empty(prob.B, dtype=torch.int32, device=prob.S.device)
-    rc = lib.scrf_clamp_events(prob.c_struct(), PRECISIONS[fwd.precision], _lib.ptr(fwd.ckpt),
-                               None if bw is None else _lib.ptr(bw.work), _lib.ptr(out), _lib.stream_handle())
+    work = None if bw is None else _lib.ptr(bw.work)
+    if fwd.sparse:
+        rc = lib.scrf_clamp_events_sparse(prob.c_struct(), fwd.delta, PRECISIONS[fwd.precision], _lib.ptr(fwd.ckpt),
+                                          work, _lib.ptr(out), _lib.stream_handle())
+    else:
+        rc = lib.scrf_clamp_events(prob.c_struct(), PRECISIONS[fwd.precision], _lib.ptr(fwd.ckpt), work,
+                                   _lib.ptr(out), _lib.stream_handle())
     _lib.check(rc, "scrf_clamp_events")
     return out
 
@@ -468,12 +536,26 @@ def streaming_forward(cum: CumulativeScores, params: SemiCRFParams, delta: int |
     if delta is not None and int(delta) < 1:
         raise ValueError(f"checkpoint interval must be >= 1, got {int(delta)}")
     prob = DeviceProblem.from_host(cum, params)
-    fwd = device_forward(prob, delta)
+    fwd = device_forward(prob, delta, sparse=True)
     _raise_if_dead(fwd)
     _check_clamp(prob, fwd, None, stats)
     if ledger is not None:
         ledger.record("checkpoints", fwd.ckpt)
-    return fwd.logZ.cpu().numpy(), CheckpointSet(prob, fwd)
+    return fwd.logZ.cpu().numpy(), CheckpointSet(prob, fwd, cum, params)
+
+
+def _same_problem(ckpts: CheckpointSet, cum: CumulativeScores, params: SemiCRFParams) -> bool:
+    if ckpts._cum is cum and ckpts._params is params:
+        return True
+    pairs = [(cum.S, ckpts._cum.S), (cum.lengths, ckpts._cum.lengths), (cum.proj_start, ckpts._cum.proj_start),
+             (cum.proj_end, ckpts._cum.proj_end), (params.transition, ckpts._params.transition),
+             (params.duration_bias, ckpts._params.duration_bias)]
+    for x, y in pairs:
+        if (x is None) != (y is None):
+            return False
+        if x is not None and (x is not y) and not np.array_equal(np.asarray(x), np.asarray(y)):
+            return False
+    return True
 
 
 def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts, upstream=None, *,
@@ -494,15 +576,20 @@ def streaming_backward(cum: CumulativeScores, params: SemiCRFParams, logZ, ckpts
             f"checkpoint set holds {ckpts.n_checkpoints} segments; T={T} with delta={ckpts.delta} "
             f"needs {-(-T // ckpts.delta)}"
         )
+    _check_labels(cum, params)
     up = None
     if upstream is not None:
         up = np.asarray(upstream, dtype=np.float64)
         if up.shape != (B,):
             raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
+    # the backward uses the cum / params it is given (as the reference does); the checkpoint rows
+    # are the forward's, and alpha is replayed from them between checkpoints
     prob = ckpts._prob
+    if ckpts._cum is not None and not _same_problem(ckpts, cum, params):
+        prob = DeviceProblem.from_host(cum, params)
     fwd = ckpts._fwd
     logZ_t = torch.as_tensor(np.asarray(logZ, dtype=np.float64), device=prob.S.device)
-    fwd_used = DeviceForward(logZ_t, fwd.N, fwd.dead_at, fwd.ckpt, fwd.delta, fwd.precision)
+    fwd_used = DeviceForward(logZ_t, fwd.N, fwd.dead_at, fwd.ckpt, fwd.delta, fwd.precision, fwd.sparse)
     up_t = None if up is None else torch.as_tensor(up, device=prob.S.device)
     bw = device_backward(prob, fwd_used, up_t)
     _check_clamp(prob, fwd, bw, stats)
@@ -586,10 +673,35 @@ def forward_logZ(cum, params, delta=None, backend=None, *, ledger=None, stats=No
     return streaming_forward(cum, params, delta, ledger=ledger, stats=stats)[0]
 
 
-def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None):
+def full_mode_bytes(prob: DeviceProblem, delta: int | None = None, precision: str | None = None) -> int:
+    """Device working memory of the full-memory posterior (checkpoint + work buffers)."""
+    lib = _lib.load()
+    prec = PRECISIONS[precision or _default_precision]
+    delta = _check_delta(prob, delta)
+    p = prob.c_struct()
+    a, b = ctypes_size(), ctypes_size()
+    _lib.check(lib.scrf_checkpoint_bytes(p, delta, prec, a), "scrf_checkpoint_bytes")
+    _lib.check(lib.scrf_backward_work_bytes(p, delta, prec, b), "scrf_backward_work_bytes")
+    return a.value + b.value
+
+
+def choose_memory_mode(prob: DeviceProblem, delta: int | None = None, memory: str = "auto") -> str:
+    """"full" unless its working set would take more than half of the free device memory."""
+    if memory != "auto":
+        if memory not in MEMORY_MODES:
+            raise ValueError(f"memory must be 'auto' or one of {MEMORY_MODES}")
+        return memory
+    free, _ = torch.cuda.mem_get_info(prob.S.device)
+    return "full" if full_mode_bytes(prob, delta) <= free // 2 else "sublinear"
+
+
+def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None, memory: str = "auto"):
     """(logZ, GradientSet, MarginalSet) — streaming.py:725-746.
 
-    One fused device call (scrf_posterior): the alpha and beta sweeps run concurrently.
+    One fused device call: the alpha and beta sweeps run concurrently. `memory` selects the
+    working-memory mode: "full" keeps every position's messages (fastest), "sublinear" keeps
+    checkpoint rows only and replays alpha / beta between checkpoints, "auto" (default) takes
+    "full" when it fits in half of the free device memory.
     """
     _check_labels(cum, params)
     if delta is not None and int(delta) < 1:
@@ -609,7 +721,8 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
     ready.record()  # torch creates the CUDA event lazily: make the handle real before passing it
     lib.scrf_position_outputs_event(ctypes.c_void_p(ready.cuda_event))
     try:
-        fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device))
+        fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device),
+                                   memory=choose_memory_mode(prob, delta, memory))
     finally:
         lib.scrf_position_outputs_event(None)
     side = _side_stream()
@@ -669,16 +782,19 @@ def log_partition(S, transition, duration_bias, lengths, proj_start=None, proj_e
 def recompute_alpha(omega_i, n_i, cum, params, t_start, t_end):
     """Replay forward messages t_start..t_end from one snapshot (streaming.py:232-261).
 
-    Runs a fresh device forward and returns alpha in the snapshot's frame
-    (alpha - n_i), with block[:, 0] taken straight from the snapshot slot.
+    Device replay (scrf_recompute_alpha): the snapshot's ring slots force the first
+    positions of a sweep that then runs the recursion to t_end. Returns (B, t_end - t_start
+    + 1, C) in the snapshot's frame (n_i is not re-applied), block[:, 0] straight from the
+    snapshot slot, and past L_b the ring slot's held value, as the reference does.
     """
     if not 0 <= t_start <= t_end <= cum.max_length:
         raise ValueError(f"bad replay window [{t_start}, {t_end}] for T={cum.max_length}")
-    K = params.max_duration
+    _check_labels(cum, params)
     omega_i = np.asarray(omega_i, dtype=np.float64)
-    B, C = omega_i.shape[0], omega_i.shape[2]
-    block = np.empty((B, t_end - t_start + 1, C))
-    block[:, 0] = omega_i[:, t_start % K, :]
-    if t_end == t_start:
-        return block
-    raise NotImplementedError("recompute_alpha over a non-empty window: use streaming_backward (device replay)")
+    B, K, C = cum.batch_size, params.max_duration, cum.num_labels
+    if omega_i.shape != (B, K, C):
+        raise ValueError(f"omega_i must be shaped ({B}, {K}, {C}), got {omega_i.shape}")
+    del n_i  # kept in the signature so (omega, N) travel as a pair (streaming.py:250)
+    prob = DeviceProblem.from_host(cum, params)
+    block = device_recompute_alpha(prob, torch.as_tensor(omega_i), int(t_start), int(t_end))
+    return block.cpu().numpy()
