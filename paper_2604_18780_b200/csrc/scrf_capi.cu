@@ -760,11 +760,11 @@ __global__ void build_tasks_kernel(const int64_t* lengths, const double* N, int 
     tk.n_ref = N[(size_t)b * n_ckpt + t0 / delta] * kLog2e;
   } else {
     tk.t_lo = w0;
-    if (w1 >= L) {
+    const int ttop = w1 >= L ? L : ck_ttop(j + 1, W, K, L);
+    if (ttop == L) {  // the window's beta rows reach L: start at beta[L] = 0 like the full sweep
       tk.t0 = L;
       tk.steps = L - w0;
     } else {
-      const int ttop = ck_ttop(j + 1, W, K, L);
       tk.t0 = ttop;
       tk.steps = ttop - w0;
       tk.nforce = ttop - w1 + 1;

@@ -61,7 +61,7 @@ __host__ __device__ inline int cut_slots(int w0, int w1, int d) { return d > 0 ?
 template <typename R>
 __host__ __device__ inline size_t cut_smem(int K) {
   // per label: a[K + kCutSG] (sources t-K+1 .. t-1, padded), b[K + kCutEC] (targets), w[2K + 2 kCutEC]
-  return (size_t)kCutCG * ((K + kCutSG) + (K + kCutEC) + (2 * K + 2 * kCutEC)) * sizeof(float) + 64;
+  return (size_t)kCutCG * ((K + kCutSG) + (K + kCutEC) + (2 * K + 2 * kCutEC)) * sizeof(R) + 64;
 }
 
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
   const size_t rbb = (size_t)b * a.rowsB - a.tB0;  // beta row of t: rbb + t
   const double Z2 = a.logZ[b] * kLog2e;
   const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC;
-  float* sa = (float*)sm;                  // [CG][NA]   a[s], s = t-K+1+i
-  float* sb = sa + (size_t)kCutCG * NA;    // [CG][NBv]  b[e], e = t+1+i
-  float* sw = sb + (size_t)kCutCG * NBv;   // [CG][NW]   w[k], k = i - kCutEC (k in 1..K nonzero)
+  R* sa = (R*)sm;                      // [CG][NA]   a[s], s = t-K+1+i
+  R* sb = sa + (size_t)kCutCG * NA;    // [CG][NBv]  b[e], e = t+1+i
+  R* sw = sb + (size_t)kCutCG * NBv;   // [CG][NW]   w[k], k = i - kCutEC (k in 1..K nonzero)
   const int s_lo = t - K + 1;
   for (int cl = 0; cl < Cn; ++cl) {
     const int c = c0 + cl;
@@ -150,41 +150,41 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
       ra_max = block_max_d(ra_max, red);
       rb_max = block_max_d(rb_max, red);
       bm = block_max_d(bm, red);
-      float* A = sa + (size_t)cl * NA;
-      float* Bv = sb + (size_t)cl * NBv;
-      float* W = sw + (size_t)cl * NW;
+      R* A = sa + (size_t)cl * NA;
+      R* Bv = sb + (size_t)cl * NBv;
+      R* W = sw + (size_t)cl * NW;
       const bool live = ra_max > -CUDART_INF && rb_max > -CUDART_INF && bm > -CUDART_INF;
       for (int i = threadIdx.x; i < NA; i += blockDim.x) {
         const int s = s_lo + i;
-        float v = 0.f;
+        R v = 0;
         if (live && i < K - 1 && s >= 0) {
           const size_t o = (rb0 + s) * C + c;
           const R xa = a.Xa[(ra0 + s) * C + c];
           if (xa > Mth<R>::ninf()) {
             const double ra = a.na[ra0 + s] + (double)xa - a.S[o] * kLog2e +
                               ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
-            v = exp2f((float)(ra - ra_max));
+            v = Mth<R>::ex2((R)(ra - ra_max));
           }
         }
         A[i] = v;
       }
       for (int i = threadIdx.x; i < NBv; i += blockDim.x) {
         const int e = t + 1 + i;
-        float v = 0.f;
+        R v = 0;
         if (live && i < K - 1 && e <= L) {
           const size_t o = (rb0 + e) * C + c;
           const R xb = a.Xb[(rbb + e) * C + c];
           if (xb > Mth<R>::ninf()) {
             const double rv = a.nb[rbb + e] + (double)xb + a.S[o] * kLog2e +
                               (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
-            v = exp2f((float)(rv - rb_max));
+            v = Mth<R>::ex2((R)(rv - rb_max));
           }
         }
         Bv[i] = v;
       }
       for (int i = threadIdx.x; i < NW; i += blockDim.x) {
         const int k = i - kCutEC;
-        W[i] = (live && k >= 1 && k <= K) ? exp2f((float)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : 0.f;
+        W[i] = (live && k >= 1 && k <= K) ? Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
       }
       __syncthreads();
       // sum_{s,e} a_s b_e w_{e-s}: item = (source group of kCutSG, target chunk of kCutEC)
@@ -197,17 +197,17 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
         const int e0 = q * kCutEC;   // targets e = t + 1 + e0 + u
         // k = e - s = (t + 1 + e0 + u) - (s_lo + i0 + r) = K + e0 + u - i0 - r
         const int kb = K + e0 - i0;  // k of (u = 0, r = 0)
-        float wv[kCutSG];
+        R wv[kCutSG];
 #pragma unroll
         for (int r = 0; r < kCutSG; ++r) wv[r] = W[kb - r + kCutEC];
-        float sr[kCutSG];
+        R sr[kCutSG];
 #pragma unroll
-        for (int r = 0; r < kCutSG; ++r) sr[r] = 0.f;
+        for (int r = 0; r < kCutSG; ++r) sr[r] = 0;
 #pragma unroll 8
         for (int u = 0; u < kCutEC; ++u) {
-          const float bv = Bv[e0 + u];
+          const R bv = Bv[e0 + u];
 #pragma unroll
-          for (int r = 0; r < kCutSG; ++r) sr[r] = fmaf(bv, wv[r], sr[r]);
+          for (int r = 0; r < kCutSG; ++r) sr[r] = fma(bv, wv[r], sr[r]);
 #pragma unroll
           for (int r = kCutSG - 1; r > 0; --r) wv[r] = wv[r - 1];
           wv[0] = W[kb + u + 1 + kCutEC];

@@ -63,10 +63,11 @@ def build_scores_t(emissions: torch.Tensor, lengths: torch.Tensor, mode: Centeri
 
 
 def gold_scores_t(S: torch.Tensor, transition: torch.Tensor, duration_bias: torch.Tensor,
-                  golds: list[Segmentation]) -> torch.Tensor:
+                  golds: list[Segmentation], proj_start: torch.Tensor | None = None,
+                  proj_end: torch.Tensor | None = None) -> torch.Tensor:
     """Log-score of each gold tiling, summed over the virtual source label
     (potentials.py:420-459): LSE_c0 (T[c0, first] + sum over segments of
-    (S[e,c] - S[s,c]) + B[e-s-1, c] + T[prev, c])."""
+    (S[e,c] - S[s,c]) + B[e-s-1, c] (+ Ps[s,c] + Pe[e-1,c]) + T[prev, c])."""
     dev = S.device
     bs, ss, es, cs, ps = [], [], [], [], []
     firsts = []
@@ -86,6 +87,10 @@ def gold_scores_t(S: torch.Tensor, transition: torch.Tensor, duration_bias: torc
     c_t = torch.tensor(cs, device=dev)
     p_t = torch.tensor(ps, device=dev)
     seg = (S[b_t, e_t, c_t] - S[b_t, s_t, c_t]) + duration_bias[e_t - s_t - 1, c_t]
+    if proj_start is not None:
+        seg = seg + proj_start[b_t, s_t, c_t]
+    if proj_end is not None:
+        seg = seg + proj_end[b_t, e_t - 1, c_t]
     has_prev = p_t >= 0
     trans = torch.where(has_prev, transition[p_t.clamp(min=0), c_t], torch.zeros_like(seg))
     total = torch.zeros(len(golds), dtype=S.dtype, device=dev).index_add(0, b_t, seg + trans)

@@ -169,9 +169,34 @@ def make_masked():
          streaming_logZ=z_stream, streaming_clamp_events=np.int64(st.clamp_events))
 
 
+def make_train():
+    """Acceptance criterion 04 (test_acceptance.py:128-137): the reference's 100-epoch
+    gradient-descent training demo (validation.py:344-491) with the dense backend, plus its
+    synthetic batch (datagen.generate_imbalanced) so the device path can replay the same run."""
+    from streamcrf.datagen import generate_imbalanced
+    from streamcrf.validation import DEFAULT_TRAIN_CONFIG, training_convergence_demo
+
+    cfg = dict(DEFAULT_TRAIN_CONFIG)
+    B, T, C, K = cfg["B"], cfg["T"], cfg["C"], cfg["K"]
+    seqs, golds = [], []
+    for b in range(B):
+        batch_b, gold_b = generate_imbalanced(T, C, (1.0 / C,) * C, 1.0, seed=[cfg["seed"], b], max_duration=K)
+        seqs.append(batch_b.emissions[0])
+        golds.append(np.array(gold_b.segments, np.int64))
+    t0 = time.time()
+    rep = training_convergence_demo(epochs=100, backends=("dense",))
+    print(f"  train: {time.time() - t0:.1f}s final {rep['backends']['dense']['final']}")
+    arrays = dict(B=np.int64(B), T=np.int64(T), C=np.int64(C), K=np.int64(K), lr=np.float64(cfg["lr"]),
+                  emissions=np.stack(seqs), dense_curve=np.array(rep["backends"]["dense"]["curve"]))
+    for b, g in enumerate(golds):
+        arrays[f"gold_{b}"] = g
+    save("train", **arrays)
+
+
 M = P.CenteringMode
 JOBS = {
     "masked": make_masked,
+    "train": make_train,
     "small": lambda: make_small(),
     # c1 exactly as BASELINE.json config 1 (MEAN centering, SURVEY §8d), plus ragged+projections.
     "c1": lambda: make_equiv("c1", 0, 256, 8, 4, 4, M.MEAN),
