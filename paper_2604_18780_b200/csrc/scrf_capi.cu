@@ -280,18 +280,30 @@ struct PostGeo {
   int CH, nch, CGB, SCB, nchB;
 };
 
+// grad_B in exp space for the fp32 working type (SCRF_GRADB_EXACT=1: one ex2 per term)
+bool gradB_blocked() { return env_int("SCRF_GRADB_EXACT", 0) == 0; }
+
 // posterior-pass geometry for passes of at most Wn positions
 PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   PostGeo q;
   const int C = (int)p->C, K = (int)p->K, B = (int)p->B;
   q.CH = post_chunk(C);
   q.nch = (Wn + q.CH - 1) / q.CH;
-  int cg = 4096 / K;
-  if (cg < 1) cg = 1;
-  if (cg > C) cg = C;
   const size_t limit = (size_t)smem_optin();
-  while (cg > 1 && (prec ? post_gradB_smem<double>(K, cg) : post_gradB_smem<float>(K, cg)) > limit) --cg;
-  while (cg > 1 && (long long)cg * ((K + kGBJ - 1) / kGBJ) > (long long)kGBW * 512) --cg;
+  int cg;
+  if (prec == 0 && gradB_blocked()) {
+    // exp-space blocked kernel: one warp per (label, 128 durations), <= 2 items per warp
+    cg = 32 / gbb_npass(K);
+    if (cg < 1) cg = 1;
+    if (cg > C) cg = C;
+    while (cg > 1 && post_gradB_blk_smem(K, cg) > limit) --cg;
+  } else {
+    cg = 4096 / K;
+    if (cg < 1) cg = 1;
+    if (cg > C) cg = C;
+    while (cg > 1 && (prec ? post_gradB_smem<double>(K, cg) : post_gradB_smem<float>(K, cg)) > limit) --cg;
+    while (cg > 1 && (long long)cg * ((K + kGBJ - 1) / kGBJ) > (long long)kGBW * 512) --cg;
+  }
   q.CGB = cg;
   const int ngc = (C + cg - 1) / cg;
   long long want = 4LL * num_sms();
@@ -508,14 +520,25 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
   cudaError_t e;
-  if (tails && cw1)
-    e = launch_cl(sweep_kernel<R, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-  else if (tails)
-    e = launch_cl(sweep_kernel<R, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
-  else if (cw1)
-    e = launch_cl(sweep_kernel<R, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-  else
-    e = launch_cl(sweep_kernel<R, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+  if (io.tasks) {
+    if (tails && cw1)
+      e = launch_cl(sweep_kernel<R, true, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else if (tails)
+      e = launch_cl(sweep_kernel<R, true, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else if (cw1)
+      e = launch_cl(sweep_kernel<R, false, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else
+      e = launch_cl(sweep_kernel<R, false, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
+  } else {
+    if (tails && cw1)
+      e = launch_cl(sweep_kernel<R, true, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else if (tails)
+      e = launch_cl(sweep_kernel<R, true, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else if (cw1)
+      e = launch_cl(sweep_kernel<R, false, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+    else
+      e = launch_cl(sweep_kernel<R, false, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+  }
   return (int)e;
 }
 
@@ -653,7 +676,15 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, a.T, C, q.CH, q.nch, w0, w1, a.tot, out.pos);
     if (last && g_ev_pos) cudaEventRecord(g_ev_pos, st);
   }
-  {
+  if (sizeof(R) == 4 && gradB_blocked()) {
+    if ((long long)q.CGB * gbb_npass(K) > 32) return SCRF_ECONFIG;
+    const size_t sm = post_gradB_blk_smem(K, q.CGB);
+    e = cudaFuncSetAttribute(post_gradB_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
+    ++g_launches;
+    post_gradB_blk_kernel<<<dim3(q.nchB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(
+        *reinterpret_cast<const PostArgs<float>*>(&a));
+  } else {
     // one CTA holds every duration window of its label group (K <= kGBW * 512 * kGBJ = 4096)
     if ((long long)q.CGB * ((K + kGBJ - 1) / kGBJ) > (long long)kGBW * 512) return SCRF_ECONFIG;
     const size_t sm = post_gradB_smem<R>(K, q.CGB);

@@ -58,10 +58,15 @@ __host__ __device__ inline int cut_pos(int j, int w0, int tend, int d) {
 }
 __host__ __device__ inline int cut_slots(int w0, int w1, int d) { return d > 0 ? (w1 - w0 - 1) / d + 2 : 0; }
 
+// w is stored skewed (one pad word per 8): the lanes of a warp read w at indices 8 apart
+// (consecutive source groups), which the skew spreads over distinct banks
+__host__ __device__ inline int cut_wphys(int x) { return x + (x >> 3); }
+
 template <typename R>
 __host__ __device__ inline size_t cut_smem(int K) {
   // per label: a[K + kCutSG] (sources t-K+1 .. t-1, padded), b[K + kCutEC] (targets), w[2K + 2 kCutEC]
-  return (size_t)kCutCG * ((K + kCutSG) + (K + kCutEC) + (2 * K + 2 * kCutEC)) * sizeof(R) + 64;
+  return (size_t)kCutCG * ((K + kCutSG) + (K + kCutEC) + cut_wphys(2 * K + 2 * kCutEC)) * sizeof(R) +
+         (size_t)(K / kCutSG + K / kCutEC + 4) + 64;
 }
 
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -104,10 +109,14 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
   const size_t ra0 = (size_t)b * a.rowsA - a.tA0;  // alpha row of t: ra0 + t
   const size_t rbb = (size_t)b * a.rowsB - a.tB0;  // beta row of t: rbb + t
   const double Z2 = a.logZ[b] * kLog2e;
-  const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC;
+  const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC, NWp = cut_wphys(NW);
   R* sa = (R*)sm;                      // [CG][NA]   a[s], s = t-K+1+i
   R* sb = sa + (size_t)kCutCG * NA;    // [CG][NBv]  b[e], e = t+1+i
   R* sw = sb + (size_t)kCutCG * NBv;   // [CG][NW]   w[k], k = i - kCutEC (k in 1..K nonzero)
+  const int nsg = (K - 1 + kCutSG - 1) / kCutSG;
+  const int nec = (K - 1 + kCutEC - 1) / kCutEC;
+  unsigned char* nzA = (unsigned char*)(sw + (size_t)kCutCG * cut_wphys(2 * K + 2 * kCutEC));  // [nsg]
+  unsigned char* nzB = nzA + nsg;                                                             // [nec]
   const int s_lo = t - K + 1;
   for (int cl = 0; cl < Cn; ++cl) {
     const int c = c0 + cl;
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
       bm = block_max_d(bm, red);
       R* A = sa + (size_t)cl * NA;
       R* Bv = sb + (size_t)cl * NBv;
-      R* W = sw + (size_t)cl * NW;
+      R* W = sw + (size_t)cl * NWp;
       const bool live = ra_max > -CUDART_INF && rb_max > -CUDART_INF && bm > -CUDART_INF;
       for (int i = threadIdx.x; i < NA; i += blockDim.x) {
         const int s = s_lo + i;
@@ -184,33 +193,52 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
       }
       for (int i = threadIdx.x; i < NW; i += blockDim.x) {
         const int k = i - kCutEC;
-        W[i] = (live && k >= 1 && k <= K) ? Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
+        W[cut_wphys(i)] = (live && k >= 1 && k <= K) ? Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
       }
       __syncthreads();
-      // sum_{s,e} a_s b_e w_{e-s}: item = (source group of kCutSG, target chunk of kCutEC)
-      const int nsg = (K - 1 + kCutSG - 1) / kCutSG;
-      const int nec = (K - 1 + kCutEC - 1) / kCutEC;
+      // sum_{s,e} a_s b_e w_{e-s}: item = (source group of kCutSG, target chunk of kCutEC).
+      // Groups whose a (or chunks whose b) all underflowed contribute exactly 0 and are skipped:
+      // path mass decays geometrically away from the cut, so few items remain on real data.
+      for (int i = threadIdx.x; i < nsg + nec; i += blockDim.x) {
+        bool nz = false;
+        if (i < nsg) {
+          for (int r = 0; r < kCutSG; ++r) nz |= A[i * kCutSG + r] != (R)0;
+          nzA[i] = nz;
+        } else {
+          const int q = i - nsg;
+          for (int u = 0; u < kCutEC; ++u) nz |= Bv[q * kCutEC + u] != (R)0;
+          nzB[q] = nz;
+        }
+      }
+      __syncthreads();
       double acc = 0.0;
+      // lanes of a warp take consecutive source groups of one target chunk (b[e] reads are
+      // broadcasts, w reads conflict-free through the skew); chunks entirely past the
+      // duration limit (e - s > K for every pair) are skipped
       for (int it = threadIdx.x; it < nsg * nec; it += blockDim.x) {
-        const int g = it / nec, q = it % nec;
+        const int q = it / nsg, g = it % nsg;
+        if (q * kCutEC > g * kCutSG + kCutSG - 1 || !nzA[g] || !nzB[q]) continue;
         const int i0 = g * kCutSG;   // sources s = s_lo + i0 + r, r < kCutSG
         const int e0 = q * kCutEC;   // targets e = t + 1 + e0 + u
         // k = e - s = (t + 1 + e0 + u) - (s_lo + i0 + r) = K + e0 + u - i0 - r
         const int kb = K + e0 - i0;  // k of (u = 0, r = 0)
-        R wv[kCutSG];
-#pragma unroll
-        for (int r = 0; r < kCutSG; ++r) wv[r] = W[kb - r + kCutEC];
         R sr[kCutSG];
 #pragma unroll
         for (int r = 0; r < kCutSG; ++r) sr[r] = 0;
-#pragma unroll 8
-        for (int u = 0; u < kCutEC; ++u) {
-          const R bv = Bv[e0 + u];
+        // sub-blocks of 16 targets, fully unrolled: the window of w values the 16 x kCutSG
+        // terms need sits in registers (no shifting), one b load per target
+        constexpr int kU = 16;
+#pragma unroll 1
+        for (int u0 = 0; u0 < kCutEC; u0 += kU) {
+          R wb[kCutSG - 1 + kU];  // wb[j] = w[kb + u0 - (kCutSG - 1) + j]
 #pragma unroll
-          for (int r = 0; r < kCutSG; ++r) sr[r] = fma(bv, wv[r], sr[r]);
+          for (int jj = 0; jj < kCutSG - 1 + kU; ++jj) wb[jj] = W[cut_wphys(kb + u0 - (kCutSG - 1) + jj + kCutEC)];
 #pragma unroll
-          for (int r = kCutSG - 1; r > 0; --r) wv[r] = wv[r - 1];
-          wv[0] = W[kb + u + 1 + kCutEC];
+          for (int u = 0; u < kU; ++u) {
+            const R bv = Bv[e0 + u0 + u];
+#pragma unroll
+            for (int r = 0; r < kCutSG; ++r) sr[r] = fma(bv, wb[u - r + kCutSG - 1], sr[r]);
+          }
         }
         double tot = 0.0;
 #pragma unroll
@@ -293,18 +321,28 @@ __global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch,
   const double* Ub = U + (size_t)b * ncut * C;
   double* base = tot + (size_t)b * nch * C + c;
   double run = (w0 == 0 || !carry) ? 0.0 : carry[(size_t)b * C + c];
-  for (int q = 0; q < nch; ++q) {
-    const int t0 = w0 + q * CH;
-    if (t0 > 0 && t0 < tend && (t0 - w0) % d == 0 && (t0 - w0) / d <= J) {
-      const int j = (t0 - w0) / d;
-      double s = 0.0;
-      for (int cc = 0; cc < C; ++cc) s += Ub[(size_t)j * C + cc];
-      const double l = s > 0.0 ? log2(s) : 1.0;
-      if (fabs(l) <= 1e-2) run = Ub[(size_t)j * C + c] / s;
+  // batches of 16 chunk totals loaded before any store (the loads pipeline instead of
+  // serialising behind the stores to the same array)
+  constexpr int kQB = 16;
+  for (int qb = 0; qb < nch; qb += kQB) {
+    double v[kQB];
+#pragma unroll
+    for (int i = 0; i < kQB; ++i) v[i] = qb + i < nch ? base[(size_t)(qb + i) * C] : 0.0;
+#pragma unroll
+    for (int i = 0; i < kQB; ++i) {
+      const int q = qb + i;
+      if (q >= nch) break;
+      const int t0 = w0 + q * CH;
+      if (t0 > 0 && t0 < tend && (t0 - w0) % d == 0 && (t0 - w0) / d <= J) {
+        const int j = (t0 - w0) / d;
+        double s = 0.0;
+        for (int cc = 0; cc < C; ++cc) s += Ub[(size_t)j * C + cc];
+        const double l = s > 0.0 ? log2(s) : 1.0;
+        if (fabs(l) <= 1e-2) run = Ub[(size_t)j * C + c] / s;
+      }
+      base[(size_t)q * C] = run;
+      run += v[i];
     }
-    const double v = base[(size_t)q * C];
-    base[(size_t)q * C] = run;
-    run += v;
   }
   if (carry) carry[(size_t)b * C + c] = run;
 }

@@ -333,6 +333,203 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
   }
 }
 
+// grad_B partial in exp space (fp32 working type): CTA (b, source range, label group), one warp
+// per (label, pass of 128 durations). Per block of 32 sources the source values are detrended by
+// the block's slope lam (alpha grows at ~lam per position, the beta side falls at the same rate):
+//   d_i = (ra[s0+i] - r0) - lam i,     e_v = (rb[s0+kb+v] + r0) + lam v     (r0 = the block's first ra)
+//   term(s0+i, k) = 2^(d_i + e_v - lam (k - kb) + B[k-1]),  v = i + k - kb
+// so with x_i = 2^(d_i - Gd), y_v = 2^(e_v - Ge) a block contributes
+//   2^(Gd + Ge - lam (k - kb) + B[k-1]) * sum_i x_i y_{i+k-kb}
+// -- 32 FMA per term group of a lane (4 durations x 32 sources from one 35-value y window)
+// instead of one ex2 per term. Blocks whose detrended range exceeds kGBRange take the exact
+// per-term path (no term can be lost to fp32 underflow then).
+constexpr int kGBPass = 128;   // durations per warp item (4 per lane)
+constexpr float kGBRange = 100.f;
+__host__ __device__ inline int gbb_npass(int K) { return (K + kGBPass - 1) / kGBPass; }
+__host__ __device__ inline int gbb_nU(int K) { return kGBSub + gbb_npass(K) * kGBPass + 32; }
+__host__ __device__ inline int gbb_row(int K) { return gb_skew(gbb_nU(K)) + 1; }
+constexpr int kGBBWarp = 32 + 32 + 168 + 168;  // per-warp scratch: x, d, y window, e (floats)
+
+__host__ __device__ inline size_t post_gradB_blk_smem(int K, int CG) {
+  return (size_t)CG * kGBSub * 2 * sizeof(float) + (size_t)CG * gbb_row(K) * 2 * sizeof(float) +
+         (size_t)CG * gbb_npass(K) * kGBPass * sizeof(float) + (size_t)16 * kGBBWarp * sizeof(float) + 64;
+}
+
+__global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.z, cg = blockIdx.y, sb = blockIdx.x;
+  const int C = a.C, T = a.T, K = a.K, CG = a.CGB;
+  const int L = (int)a.lengths[b];
+  const int c0 = cg * CG;
+  const int Cn = min(CG, C - c0);
+  const int npass = gbb_npass(K);
+  const int nU = gbb_nU(K);
+  const int rowU = gbb_row(K);
+  const int KP = npass * kGBPass;
+  float2* sa = (float2*)sm;                          // [CG][kGBSub]
+  float2* sbv = sa + (size_t)CG * kGBSub;            // [CG][rowU] (skewed)
+  float* B2 = (float*)(sbv + (size_t)CG * rowU);     // [CG][KP], -inf past K
+  float* wsc = (float*)(((uintptr_t)(B2 + (size_t)CG * KP) + 15) & ~(uintptr_t)15);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* xs = wsc + (size_t)warp * kGBBWarp;  // [32]
+  float* ds = xs + 32;                        // [32]
+  float* yw = ds + 32;                        // [168] (16-byte aligned)
+  float* es = yw + 168;                       // [168]
+  const double Z2 = a.logZ[b] * kLog2e;
+  const size_t rb0 = (size_t)b * (T + 1);
+  const int W = a.w1 - a.w0;
+  for (int i = threadIdx.x; i < Cn * KP; i += blockDim.x) {
+    const int cl = i / KP, k = i % KP;
+    B2[i] = k < K ? (float)(a.dur[(size_t)k * C + c0 + cl] * kLog2e) : -CUDART_INF_F;
+  }
+  const int nitems = Cn * npass;
+  double acc[2][4];
+#pragma unroll
+  for (int w = 0; w < 2; ++w)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[w][j] = 0.0;
+  const int sbeg = a.w0 + sb * a.SCB;
+  const int send = min(min(sbeg + a.SCB, a.w1), L);
+  __syncthreads();
+  for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
+    __syncthreads();
+    const int ns = min(kGBSub, send - s0);
+    for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
+      const int cl = i / kGBSub, si = i % kGBSub, s = s0 + si, c = c0 + cl;
+      float2 v = make_float2(-CUDART_INF_F, 0.f);
+      if (si < ns) {
+        const size_t o = (rb0 + s) * C + c;
+        const size_t oa = rowA(a, b, s);
+        const double ra = a.na[oa] + (double)a.Xa[oa * C + c] - a.S[o] * kLog2e +
+                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0) +
+                          (a.corr ? a.corr[(size_t)b * W + s - a.w0] : 0.0);
+        split2(ra, v.x, v.y);
+      }
+      sa[(size_t)cl * kGBSub + si] = v;
+    }
+    for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
+      const int cl = i / nU, ui = i % nU, u = s0 + 1 + ui, c = c0 + cl;
+      float2 v = make_float2(-CUDART_INF_F, 0.f);
+      if (u <= L && ui < kGBSub + K) {
+        const size_t o = (rb0 + u) * C + c;
+        const size_t ob = rowB(a, b, u);
+        const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +
+                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
+        split2(rv, v.x, v.y);
+      }
+      sbv[(size_t)cl * rowU + gb_skew(ui)] = v;
+    }
+    __syncthreads();
+    for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
+      const int cl = it / npass, pass = it % npass;
+      const int kb = pass * kGBPass + 1;  // durations kb .. kb + 127 (lane owns kb + 4 lane + j)
+      const float2* A = sa + (size_t)cl * kGBSub;
+      const float2* Bv = sbv + (size_t)cl * rowU;
+      const float* b2 = B2 + (size_t)cl * KP;
+      float bk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bk[j] = b2[kb - 1 + 4 * lane + j];
+      for (int jb = 0; jb * 32 < ns; ++jb) {
+        // sources of the block, detrended
+        const float2 r = A[jb * 32 + lane];
+        const bool fin = r.x != -CUDART_INF_F;
+        const unsigned fm = __ballot_sync(0xffffffffu, fin);
+        if (!fm) continue;
+        const int f0 = __ffs(fm) - 1, f1 = 31 - __clz(fm);
+        const float r0x = __shfl_sync(0xffffffffu, r.x, f0), r0y = __shfl_sync(0xffffffffu, r.y, f0);
+        const float r1x = __shfl_sync(0xffffffffu, r.x, f1), r1y = __shfl_sync(0xffffffffu, r.y, f1);
+        const float lam = f1 > f0 ? ((r1x - r0x) + (r1y - r0y)) / (float)(f1 - f0) : 0.f;
+        const float d = fin ? ((r.x - r0x) + (r.y - r0y)) - lam * (float)lane : -CUDART_INF_F;
+        float gd = d, dmin = fin ? d : CUDART_INF_F;
+        for (int o = 16; o > 0; o >>= 1) {
+          gd = fmaxf(gd, __shfl_xor_sync(0xffffffffu, gd, o));
+          dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        }
+        xs[lane] = fin ? Mth<float>::ex2(d - gd) : 0.f;
+        ds[lane] = d;
+        // targets u = s0 + 32 jb + kb + v, v in [0, 159): e_v = (rb + r0) + lam v
+        float ge = -CUDART_INF_F, emin = CUDART_INF_F;
+        float ev[5];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int v = lane + 32 * m;
+          ev[m] = -CUDART_INF_F;
+          if (v < 159) {
+            const float2 q = Bv[gb_skew(jb * 32 + kb - 1 + v)];
+            if (q.x != -CUDART_INF_F) {
+              ev[m] = ((q.x + r0x) + (q.y + r0y)) + lam * (float)v;
+              emin = fminf(emin, ev[m]);
+            }
+          }
+          ge = fmaxf(ge, ev[m]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          ge = fmaxf(ge, __shfl_xor_sync(0xffffffffu, ge, o));
+          emin = fminf(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+        }
+        if (ge == -CUDART_INF_F) continue;  // every target of this pass is past L
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int v = lane + 32 * m;
+          if (v < 168) {
+            yw[v] = ev[m] != -CUDART_INF_F ? Mth<float>::ex2(ev[m] - ge) : 0.f;
+            es[v] = ev[m];
+          }
+        }
+        __syncwarp();
+        const bool exact = (gd - dmin > kGBRange) || (ge - emin > kGBRange);
+        float out[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!exact) {
+          // lane: durations kb + 4 lane + j, sum_i x_i y_{i + 4 lane + j}
+          float y[36];
+          const float4* y4 = (const float4*)(yw + 4 * lane);
+#pragma unroll
+          for (int q = 0; q < 9; ++q) {
+            const float4 t4 = y4[q];
+            y[4 * q] = t4.x;
+            y[4 * q + 1] = t4.y;
+            y[4 * q + 2] = t4.z;
+            y[4 * q + 3] = t4.w;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float xi = xs[i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) out[j] = fmaf(xi, y[i + j], out[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float E = (gd + ge) - lam * (float)(4 * lane + j) + bk[j];
+            if (out[j] > 0.f && E != -CUDART_INF_F) acc[slot & 1][j] += (double)(out[j] * Mth<float>::ex2(E));
+          }
+        } else {
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            const float di = ds[i];
+            if (di == -CUDART_INF_F) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float e = es[i + 4 * lane + j];
+              if (e != -CUDART_INF_F) out[j] += Mth<float>::ex2((di + e) - lam * (float)(4 * lane + j) + bk[j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[slot & 1][j] += (double)out[j];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
+    const int cl = it / npass, pass = it % npass;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = pass * kGBPass + 4 * lane + j;  // duration k + 1
+      if (k < K) a.gBp[(((size_t)b * a.nchB + sb) * K + k) * C + c0 + cl] = acc[slot & 1][j];
+    }
+  }
+}
+
 template <typename R>
 __host__ __device__ inline size_t post_gradB_smem(int K, int CG) {
   return (size_t)CG * kGBSub * 2 * sizeof(R) + (size_t)CG * gb_row(K) * 2 * sizeof(R) + (size_t)CG * K * sizeof(R) + 16;

@@ -811,7 +811,7 @@ __device__ __noinline__ R gemv_exact(const double* trans, int dir, int C, int NC
 // chain syncs; count NB. Every id is used with one count only.
 
 // ======================= chain warps =======================
-template <typename R, bool CW1>
+template <typename R, bool CW1, bool REPLAY>
 __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int NB) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
@@ -897,24 +897,28 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
 
   // replay: the first nforce positions take the stored messages (Y^, n) instead of the
   // computed ones; X^ (the transition GEMV) and everything downstream are recomputed, so the
-  // replay reproduces the sweep that stored them (same positions mod 32, same arithmetic)
-  const SweepTask* tk = x.task;
-  const int nforce = tk ? tk->nforce : 0;
+  // replay reproduces the sweep that stored them (same positions mod 32, same arithmetic).
+  // Forced rows are prefetched one position ahead.
+  const SweepTask* tk = REPLAY ? x.task : nullptr;
+  const int nforce = REPLAY ? tk->nforce : 0;
   const int cs = act ? c : 0;
-  const R* fY = tk ? a.fY[x.dir] + (long long)tk->frow * C + cs : nullptr;
-  const long long fsC = tk ? (long long)tk->fstep * C : 0;
-  const int fs1 = tk ? tk->fstep : 0;
-  const double* fN = tk ? a.fN[x.dir] + tk->frow : nullptr;
-  R fq[4];
-  double nq[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    fq[i] = (i < nforce && act) ? fY[i * fsC] : Mth<R>::ninf();
-    nq[i] = i < nforce ? fN[i * fs1] : 0.0;
+  const R* fY = REPLAY ? a.fY[x.dir] + (long long)tk->frow * C + cs : nullptr;
+  const double* fN = REPLAY ? a.fN[x.dir] + tk->frow : nullptr;
+  const long long fsC = REPLAY ? (long long)tk->fstep * C : 0;
+  const int fs1 = REPLAY ? tk->fstep : 0;
+  R fq = Mth<R>::ninf();
+  double nq = 0.0;
+  if (REPLAY && nforce > 0) {
+    fq = act ? fY[0] : Mth<R>::ninf();
+    nq = fN[0];
   }
   // position 0: alpha[0] = 0 (virtual source) / beta[L] = 0, or the first forced position
-  const R yh0 = nforce > 0 ? fq[0] : (x.dir == 0 ? (R)0 : Mth<R>::ninf());
-  const double n0 = nforce > 0 ? nq[0] : 0.0;
+  const R yh0 = nforce > 0 ? fq : (x.dir == 0 ? (R)0 : Mth<R>::ninf());
+  const double n0 = nforce > 0 ? nq : 0.0;
+  if (REPLAY && nforce > 1) {
+    fq = act ? fY[fsC] : Mth<R>::ninf();
+    nq = fN[fs1];
+  }
   R x1h = (nforce > 0 || x.dir == 0) ? gemv(nforce > 0 ? yh0 : (R)0) : (R)0;  // X^[p-1]
   R x2h = Mth<R>::ninf();                    // X^[p-2]
   R x3h = Mth<R>::ninf();                    // X^[p-3]
@@ -928,28 +932,22 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     h.nring[0] = n0;
   }
   nbar_arrive(BAR_A + 0, NA + NAE);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    fq[i] = fq[i + 1];
-    nq[i] = nq[i + 1];
-  }
-  fq[3] = (4 < nforce && act) ? fY[4 * fsC] : Mth<R>::ninf();
-  nq[3] = 4 < nforce ? fN[4 * fs1] : 0.0;
   R a1 = 0, a2 = 0, a3 = 0;  // frame shifts amax_{p-1}, amax_{p-2}, amax_{p-3}
   double n_prev = n0;
   // alpha: checkpoint normaliser in effect (log2) and the position counter since the last
   // checkpoint (streaming.py:205-214); beta: 0 (absolute frame)
-  double n_ref = tk ? tk->n_ref : 0.0;
-  int ck_cnt = tk ? tk->ck_phase : 0;
-  // reference bookkeeping of the forward (alpha, full sweeps): checkpoint normalisers N_i,
-  // the first dead position, clamp events
-  const bool book = x.dir == 0 && !tk && tid == 0;
-  double* Nb = (book && a.N) ? a.N + (size_t)x.b * a.n_ckpt : nullptr;
-  if (Nb) Nb[0] = 0.0;
-  int i_ck = 1;
-  int dmin = -1;
-  int n_clamp = 0;
-  R yh_last = yh0;
+  double n_ref = REPLAY ? tk->n_ref : 0.0;
+  int ck_cnt = REPLAY ? tk->ck_phase : 0;
+  // reference bookkeeping of a full alpha sweep (checkpoint normalisers N_i, first dead
+  // position, clamp events): rare events, so the state lives in shared memory (h.wmax
+  // words 8..10), not in registers of this latency-bound loop
+  const bool book = !REPLAY && x.dir == 0 && tid == 0;
+  int* bk = (int*)(h.wmax + 8);  // [0] first dead position, [1] clamp events
+  if (book) {
+    bk[0] = -1;
+    bk[1] = 0;
+    if (a.N) a.N[(size_t)x.b * a.n_ckpt] = 0.0;
+  }
   const R2* partc = h.part + cs;
   const typename Vec4<R>::T* hhc = h.hh + cs;
   const int pubm = g.PubS - 1;
@@ -960,23 +958,23 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     constexpr long long* tr = nullptr;
 #endif
     if (tr) tr[0] = clock64();
+    // guard threshold of this position in the chain's frame, computed before the wait (the
+    // guard is 1e9 wide: fp32 is exact enough for it)
+    const R thr = (R)(n_ref + kGuardL2 - n_prev);
     nbar_sync(BAR_B + (p & 3), NB);
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(4, p);
     bool dead;
     R yh, am;
     double n_p;
-    if (p < nforce) {
-      yh = fq[0];
-      n_p = nq[0];
+    if (REPLAY && p < nforce) {
+      yh = fq;
+      n_p = nq;
       am = (R)(n_p - n_prev);  // the stored sweep's shift (exact: n_p = n_prev + (double)am there)
       dead = false;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        fq[i] = fq[i + 1];
-        nq[i] = nq[i + 1];
+      if (p + 1 < nforce) {
+        fq = act ? fY[(p + 1) * fsC] : Mth<R>::ninf();
+        nq = fN[(p + 1) * fs1];
       }
-      fq[3] = (p + 4 < nforce && act) ? fY[(p + 4) * fsC] : Mth<R>::ninf();
-      nq[3] = p + 4 < nforce ? fN[(p + 4) * fs1] : 0.0;
     } else {
       R y = Mth<R>::ninf();
       if (act) {
@@ -990,7 +988,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       // the reference's guard (_numerics.py:59-75): a position whose every message is at or below
       // NEG_INF + 1 in the reference frame (alpha: relative to the checkpoint normaliser in effect,
       // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
-      dead = (am == Mth<R>::ninf()) || (n_prev + (double)am) - n_ref <= kGuardL2;
+      dead = (am == Mth<R>::ninf()) || am <= thr;
       yh = dead ? Mth<R>::ninf() : y - am;
       n_p = dead ? n_prev : n_prev + (double)am;
     }
@@ -1000,24 +998,24 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       h.pubA[p & pubm] = dead ? Mth<R>::ninf() : am;
       h.nring[p & (kNring - 1)] = n_p;
     }
-    if (book) {
-      if (dead && dmin < 0) dmin = p;
-      // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
-      // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
-      if (!dead && fabs((n_p - n_ref) * kLn2) > kClampLimit) ++n_clamp;
-    }
-    if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
-      ck_cnt = 0;
-      if (!dead) n_ref = n_p;
-      if (Nb && i_ck < a.n_ckpt) Nb[i_ck] = n_ref * kLn2;
-      ++i_ck;
-    }
     const R xh = gemv(yh);
     if (tr) tr[2] = clock64();
     if (act) h.pubX[(p & pubm) * C + c] = xh;
     nbar_arrive(BAR_A + (p & 3), NA + ((p & 3) == 0 ? NAE : 0));
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(5, p);
     if (tr) tr[3] = clock64();
+    // bookkeeping after the hand-off (off the critical path)
+    if (book) {
+      if (dead && bk[0] < 0) bk[0] = p;
+      // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
+      // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
+      if (!dead && fabs(n_p - n_ref) > kClampLimit * kLog2e) ++bk[1];
+    }
+    if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
+      ck_cnt = 0;
+      if (!dead) n_ref = n_p;
+      if (book && a.N && p / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + p / a.delta] = n_ref * kLn2;
+    }
     x4h = x3h;
     x3h = x2h;
     x2h = x1h;
@@ -1026,12 +1024,11 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     a2 = a1;
     a1 = dead ? (R)0 : am;
     n_prev = n_p;
-    yh_last = yh;
   }
-  if (x.dir == 0 && !tk) {
+  if (!REPLAY && x.dir == 0) {
     // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats), streaming.py:216-229; the reference raises only
     // when the final log-partition is at or below the guard, naming the first dead position
-    R sm = act ? Mth<R>::ex2(yh_last) : (R)0;
+    R sm = act ? Mth<R>::ex2(h.pubY[(L & pubm) * C + c]) : (R)0;
     for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
     if (g.NCW > 1) {
       if (lane == 0) h.wmax[warp] = sm;
@@ -1042,10 +1039,10 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     if (tid == 0) {
       const double lz = (sm > (R)0) ? (n_prev + (double)Mth<R>::lg2(sm)) * kLn2 : -CUDART_INF;
       if (a.logZ) a.logZ[x.b] = lz;
-      if (Nb)
-        for (int i = i_ck; i < a.n_ckpt; ++i) Nb[i] = n_ref * kLn2;  // frozen past L
-      if (a.dead_at) a.dead_at[x.b] = (lz - n_ref * kLn2 > kGuard) ? -1 : (dmin >= 0 ? dmin : L);
-      if (a.clamp) a.clamp[x.b] = n_clamp;
+      if (a.N)
+        for (int i = L / a.delta + 1; i < a.n_ckpt; ++i) a.N[(size_t)x.b * a.n_ckpt + i] = n_ref * kLn2;  // frozen past L
+      if (a.dead_at) a.dead_at[x.b] = (lz - n_ref * kLn2 > kGuard) ? -1 : (bk[0] >= 0 ? bk[0] : L);
+      if (a.clamp) a.clamp[x.b] = bk[1];
     }
   }
 }
@@ -1282,7 +1279,7 @@ __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<
   }
 }
 
-template <typename R, bool TAILS, bool CW1>
+template <typename R, bool TAILS, bool CW1, bool REPLAY>
 __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                           const TailLayout& TL) {
   using R2 = typename Vec2<R>::T;
@@ -1353,7 +1350,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   if (TAILS) cluster_sync_all();
 
   if (warp < g.NCW)
-    head_chain<R, CW1>(a, x, h, NA, NAE, NB);
+    head_chain<R, CW1, REPLAY>(a, x, h, NA, NAE, NB);
   else if (warp < g.NCW + g.NNW)
     head_near<R, TAILS>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
@@ -1775,14 +1772,14 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
 
 // ----------------------------------------------------------------------------
 
-template <typename R, bool TAILS, bool CW1>
+template <typename R, bool TAILS, bool CW1, bool REPLAY>
 __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SweepGeo& g = a.geo;
   const int ci = blockIdx.x / g.G;
   SweepCtx x;
   x.task = nullptr;
-  if (a.tasks) {
+  if (REPLAY) {
     x.task = a.tasks + ci;
     x.b = x.task->b;
     x.dir = x.task->dir;
@@ -1830,7 +1827,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   }
 #endif
   if (x.rank == 0)
-    head_main<R, TAILS, CW1>(a, x, smem, HL, TL);
+    head_main<R, TAILS, CW1, REPLAY>(a, x, smem, HL, TL);
   else if (TAILS)
     tail_main<R>(a, x, smem, HL, TL);
   if (TAILS) cluster_sync_all();
