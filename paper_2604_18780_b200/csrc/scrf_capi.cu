@@ -293,7 +293,7 @@ PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   int cg;
   if (prec == 0 && gradB_blocked()) {
     // exp-space blocked kernel: one warp per (label, 128 durations), <= 2 items per warp
-    cg = 32 / gbb_npass(K);
+    cg = 16 / gbb_npass(K);
     if (cg < 1) cg = 1;
     if (cg > C) cg = C;
     while (cg > 1 && post_gradB_blk_smem(K, cg) > limit) --cg;
@@ -306,8 +306,10 @@ PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   }
   q.CGB = cg;
   const int ngc = (C + cg - 1) / cg;
-  long long want = 4LL * num_sms();
-  long long per = (want + (long long)ngc * B - 1) / ((long long)ngc * B);
+  // blocked grad_B: one full wave at 2 CTAs per SM; exact kernel: ~4 CTAs per SM
+  const bool blk = prec == 0 && gradB_blocked();
+  long long want = (blk ? 2LL : 4LL) * num_sms();
+  long long per = blk ? want / ((long long)ngc * B) : (want + (long long)ngc * B - 1) / ((long long)ngc * B);
   if (per < 1) per = 1;
   int scb = (int)((Wn + per - 1) / per);
   scb = (scb + kGBSub - 1) / kGBSub * kGBSub;
@@ -613,6 +615,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   a.nchB = q.nchB;
   a.CGB = q.CGB;
   a.gBp = (double*)(wb + PL.gBp);
+  a.gb_range = (float)env_int("SCRF_GB_RANGE", (int)kGBRange);
   const int B = a.B, C = a.C, K = a.K;
   cudaError_t e;
   const int cd = cut_spacing();

@@ -46,6 +46,7 @@ struct PostArgs {
   int SCB, nchB;      // grad_B: sources per CTA, CTAs per sequence (sources in [w0, w1))
   int CGB;            // labels per grad_B CTA
   double* gBp;        // [B][nchB][K][C]
+  float gb_range;     // exp-space grad_B: detrended range above which a block takes the exact path
 };
 
 template <typename R>
@@ -342,13 +343,17 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
 //   2^(Gd + Ge - lam (k - kb) + B[k-1]) * sum_i x_i y_{i+k-kb}
 // -- 32 FMA per term group of a lane (4 durations x 32 sources from one 35-value y window)
 // instead of one ex2 per term. Blocks whose detrended range exceeds kGBRange take the exact
-// per-term path (no term can be lost to fp32 underflow then).
-constexpr int kGBPass = 128;   // durations per warp item (4 per lane)
-constexpr float kGBRange = 100.f;
+// per-term path. x and y are lifted by 2^60 each, so factors down to 2^-120 of their block
+// maximum stay normal fp32 and their products (<= 2^125 summed) neither overflow nor flush.
+constexpr int kGBD = 8;                 // durations per lane
+constexpr int kGBPass = 32 * kGBD;      // durations per warp item
+constexpr float kGBRange = 180.f;
+constexpr float kGBLift = 60.f;  // x and y carry 2^60 each: products of +-126-wide factors stay normal
 __host__ __device__ inline int gbb_npass(int K) { return (K + kGBPass - 1) / kGBPass; }
 __host__ __device__ inline int gbb_nU(int K) { return kGBSub + gbb_npass(K) * kGBPass + 32; }
 __host__ __device__ inline int gbb_row(int K) { return gb_skew(gbb_nU(K)) + 1; }
-constexpr int kGBBWarp = 32 + 32 + 168 + 168;  // per-warp scratch: x, d, y window, e (floats)
+constexpr int kGBNV = kGBPass + 32;     // target window per item (v < kGBPass + 31, padded)
+constexpr int kGBBWarp = 32 + 32 + 2 * kGBNV;  // per-warp scratch: x, d, y window, e (floats)
 
 __host__ __device__ inline size_t post_gradB_blk_smem(int K, int CG) {
   return (size_t)CG * kGBSub * 2 * sizeof(float) + (size_t)CG * gbb_row(K) * 2 * sizeof(float) +
@@ -373,8 +378,8 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* xs = wsc + (size_t)warp * kGBBWarp;  // [32]
   float* ds = xs + 32;                        // [32]
-  float* yw = ds + 32;                        // [168] (16-byte aligned)
-  float* es = yw + 168;                       // [168]
+  float* yw = ds + 32;                        // [kGBNV] (16-byte aligned)
+  float* es = yw + kGBNV;                     // [kGBNV]
   const double Z2 = a.logZ[b] * kLog2e;
   const size_t rb0 = (size_t)b * (T + 1);
   const int W = a.w1 - a.w0;
@@ -383,11 +388,11 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
     B2[i] = k < K ? (float)(a.dur[(size_t)k * C + c0 + cl] * kLog2e) : -CUDART_INF_F;
   }
   const int nitems = Cn * npass;
-  double acc[2][4];
+  double acc[2][kGBD];
 #pragma unroll
   for (int w = 0; w < 2; ++w)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[w][j] = 0.0;
+    for (int j = 0; j < kGBD; ++j) acc[w][j] = 0.0;
   const int sbeg = a.w0 + sb * a.SCB;
   const int send = min(min(sbeg + a.SCB, a.w1), L);
   __syncthreads();
@@ -422,44 +427,72 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
     __syncthreads();
     for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
       const int cl = it / npass, pass = it % npass;
-      const int kb = pass * kGBPass + 1;  // durations kb .. kb + 127 (lane owns kb + 4 lane + j)
+      const int kb = pass * kGBPass + 1;  // durations kb .. kb + kGBPass - 1 (lane owns kb + kGBD lane + j)
       const float2* A = sa + (size_t)cl * kGBSub;
       const float2* Bv = sbv + (size_t)cl * rowU;
       const float* b2 = B2 + (size_t)cl * KP;
-      float bk[4];
+      float bk[kGBD];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bk[j] = b2[kb - 1 + 4 * lane + j];
+      for (int j = 0; j < kGBD; ++j) bk[j] = b2[kb - 1 + kGBD * lane + j];
       for (int jb = 0; jb * 32 < ns; ++jb) {
         // sources of the block, detrended
         const float2 r = A[jb * 32 + lane];
         const bool fin = r.x != -CUDART_INF_F;
         const unsigned fm = __ballot_sync(0xffffffffu, fin);
         if (!fm) continue;
-        const int f0 = __ffs(fm) - 1, f1 = 31 - __clz(fm);
+        const int f0 = __ffs(fm) - 1;
         const float r0x = __shfl_sync(0xffffffffu, r.x, f0), r0y = __shfl_sync(0xffffffffu, r.y, f0);
-        const float r1x = __shfl_sync(0xffffffffu, r.x, f1), r1y = __shfl_sync(0xffffffffu, r.y, f1);
-        const float lam = f1 > f0 ? ((r1x - r0x) + (r1y - r0y)) / (float)(f1 - f0) : 0.f;
+        // targets u = s0 + 32 jb + kb + v, v in [0, kGBPass + 31): e'_v = rb + r0
+        float ev[kGBNV / 32];
+        int vlo = 1 << 30, vhi = -1;
+        float elo = 0.f, ehi = 0.f;
+#pragma unroll
+        for (int m = 0; m < kGBNV / 32; ++m) {
+          const int v = lane + 32 * m;
+          ev[m] = -CUDART_INF_F;
+          if (v < kGBPass + 31) {
+            const float2 q = Bv[gb_skew(jb * 32 + kb - 1 + v)];
+            if (q.x != -CUDART_INF_F) {
+              ev[m] = (q.x + r0x) + (q.y + r0y);
+              if (v < vlo) {
+                vlo = v;
+                elo = ev[m];
+              }
+              vhi = v;
+              ehi = ev[m];
+            }
+          }
+        }
+        // slope of the window (beta falls as alpha grows): detrend both sides with it
+        for (int o = 16; o > 0; o >>= 1) {
+          const int vl2 = __shfl_xor_sync(0xffffffffu, vlo, o), vh2 = __shfl_xor_sync(0xffffffffu, vhi, o);
+          const float el2 = __shfl_xor_sync(0xffffffffu, elo, o), eh2 = __shfl_xor_sync(0xffffffffu, ehi, o);
+          if (vl2 < vlo) {
+            vlo = vl2;
+            elo = el2;
+          }
+          if (vh2 > vhi) {
+            vhi = vh2;
+            ehi = eh2;
+          }
+        }
+        if (vhi < 0) continue;  // every target of this pass is past L
+        const float lam = vhi > vlo ? -(ehi - elo) / (float)(vhi - vlo) : 0.f;
         const float d = fin ? ((r.x - r0x) + (r.y - r0y)) - lam * (float)lane : -CUDART_INF_F;
         float gd = d, dmin = fin ? d : CUDART_INF_F;
         for (int o = 16; o > 0; o >>= 1) {
           gd = fmaxf(gd, __shfl_xor_sync(0xffffffffu, gd, o));
           dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         }
-        xs[lane] = fin ? Mth<float>::ex2(d - gd) : 0.f;
+        xs[lane] = fin ? Mth<float>::ex2((d - gd) + kGBLift) : 0.f;
         ds[lane] = d;
-        // targets u = s0 + 32 jb + kb + v, v in [0, 159): e_v = (rb + r0) + lam v
+        // detrended targets e_v = e'_v + lam v
         float ge = -CUDART_INF_F, emin = CUDART_INF_F;
-        float ev[5];
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const int v = lane + 32 * m;
-          ev[m] = -CUDART_INF_F;
-          if (v < 159) {
-            const float2 q = Bv[gb_skew(jb * 32 + kb - 1 + v)];
-            if (q.x != -CUDART_INF_F) {
-              ev[m] = ((q.x + r0x) + (q.y + r0y)) + lam * (float)v;
-              emin = fminf(emin, ev[m]);
-            }
+        for (int m = 0; m < kGBNV / 32; ++m) {
+          if (ev[m] != -CUDART_INF_F) {
+            ev[m] += lam * (float)(lane + 32 * m);
+            emin = fminf(emin, ev[m]);
           }
           ge = fmaxf(ge, ev[m]);
         }
@@ -469,22 +502,22 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
         }
         if (ge == -CUDART_INF_F) continue;  // every target of this pass is past L
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
+        for (int m = 0; m < kGBNV / 32; ++m) {
           const int v = lane + 32 * m;
-          if (v < 168) {
-            yw[v] = ev[m] != -CUDART_INF_F ? Mth<float>::ex2(ev[m] - ge) : 0.f;
-            es[v] = ev[m];
-          }
+          yw[v] = ev[m] != -CUDART_INF_F ? Mth<float>::ex2((ev[m] - ge) + kGBLift) : 0.f;
+          es[v] = ev[m];
         }
         __syncwarp();
-        const bool exact = (gd - dmin > kGBRange) || (ge - emin > kGBRange);
-        float out[4] = {0.f, 0.f, 0.f, 0.f};
-        if (!exact) {
-          // lane: durations kb + 4 lane + j, sum_i x_i y_{i + 4 lane + j}
-          float y[36];
-          const float4* y4 = (const float4*)(yw + 4 * lane);
+        const bool exact = (gd - dmin > a.gb_range) || (ge - emin > a.gb_range);
+        float out[kGBD];
 #pragma unroll
-          for (int q = 0; q < 9; ++q) {
+        for (int j = 0; j < kGBD; ++j) out[j] = 0.f;
+        if (!exact) {
+          // lane: durations kb + kGBD lane + j, sum_i x_i y_{i + kGBD lane + j}
+          float y[32 + kGBD];
+          const float4* y4 = (const float4*)(yw + kGBD * lane);
+#pragma unroll
+          for (int q = 0; q < (32 + kGBD) / 4; ++q) {
             const float4 t4 = y4[q];
             y[4 * q] = t4.x;
             y[4 * q + 1] = t4.y;
@@ -495,12 +528,14 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
           for (int i = 0; i < 32; ++i) {
             const float xi = xs[i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) out[j] = fmaf(xi, y[i + j], out[j]);
+            for (int j = 0; j < kGBD; ++j) out[j] = fmaf(xi, y[i + j], out[j]);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float E = (gd + ge) - lam * (float)(4 * lane + j) + bk[j];
-            if (out[j] > 0.f && E != -CUDART_INF_F) acc[slot & 1][j] += (double)(out[j] * Mth<float>::ex2(E));
+          for (int j = 0; j < kGBD; ++j) {
+            // the 2^-120 of the lift is applied in fp64 (the fp32 product could flush)
+            const float E = (gd + ge) - lam * (float)(kGBD * lane + j) + bk[j];
+            if (out[j] > 0.f && E != -CUDART_INF_F)
+              acc[slot & 1][j] += (double)out[j] * (double)Mth<float>::ex2(E) * 0x1p-120;
           }
         } else {
 #pragma unroll 4
@@ -508,13 +543,13 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
             const float di = ds[i];
             if (di == -CUDART_INF_F) continue;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float e = es[i + 4 * lane + j];
-              if (e != -CUDART_INF_F) out[j] += Mth<float>::ex2((di + e) - lam * (float)(4 * lane + j) + bk[j]);
+            for (int j = 0; j < kGBD; ++j) {
+              const float e = es[i + kGBD * lane + j];
+              if (e != -CUDART_INF_F) out[j] += Mth<float>::ex2((di + e) - lam * (float)(kGBD * lane + j) + bk[j]);
             }
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[slot & 1][j] += (double)out[j];
+          for (int j = 0; j < kGBD; ++j) acc[slot & 1][j] += (double)out[j];
         }
         __syncwarp();
       }
@@ -523,8 +558,8 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
   for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
     const int cl = it / npass, pass = it % npass;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int k = pass * kGBPass + 4 * lane + j;  // duration k + 1
+    for (int j = 0; j < kGBD; ++j) {
+      const int k = pass * kGBPass + kGBD * lane + j;  // duration k + 1
       if (k < K) a.gBp[(((size_t)b * a.nchB + sb) * K + k) * C + c0 + cl] = acc[slot & 1][j];
     }
   }
