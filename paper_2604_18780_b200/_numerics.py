@@ -11,6 +11,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import numpy as np
+
 NEG_INF = -1.0e9
 """Reference sentinel for log(0) (`_numerics.py:18`)."""
 
@@ -56,3 +58,17 @@ class RunStats:
 
 class ClampSemanticsError(ValueError):
     """Raised when the reference would have clipped an intermediate to +-CLAMP_LIMIT."""
+
+
+def logsumexp(a, axis, keepdims: bool = False):
+    """Guarded host log-sum-exp with the reference's sentinel semantics (_numerics.py:59-75):
+    a slice whose maximum is at or below NEG_INF + 1 reduces to NEG_INF. Host utility for
+    callers of the numpy API (gold-path scoring, tests); the kernels never call it."""
+    x = np.asarray(a, dtype=np.float64)
+    top = np.max(x, axis=axis, keepdims=True)
+    live = top > NEG_INF + 1.0
+    ref = np.where(live, top, 0.0)
+    with np.errstate(under="ignore", divide="ignore"):
+        tot = np.sum(np.exp(x - ref), axis=axis, keepdims=True)
+        val = np.where(live, ref + np.log(np.maximum(tot, 1e-300)), NEG_INF)
+    return val if keepdims else np.squeeze(val, axis=axis)

@@ -1,0 +1,74 @@
+"""Parity at FULL BASELINE lengths against the real reference.
+
+Fixtures from tests/golden/make_golden_full.py, which ran the reference
+(pkg/src/streamcrf: streaming_forward / streaming_backward / streaming_viterbi) for hours on
+the CPU: config 4 at T = 100 000 (one sequence), config 5 at T = 20 000 (one sequence),
+config 3 exactly (B = 32, T = 4000). Per-position arrays are stored on a fixed row sample
+(first and last 512 rows and every 64th); log Z, N, grad_T, grad_B, the segment count and
+the complete Viterbi segmentations are stored in full.
+
+Bars (tests/parity.py): fp32 log Z 1e-5 relative, gradients / marginals 1e-5 in the
+reference's max|d| / max(1, |ref|) metric; fp64 1e-9 / 1e-8; Viterbi bit-identical.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import golden_io  # noqa: E402
+import parity  # noqa: E402
+import paper_2604_18780_b200 as scrf  # noqa: E402
+from paper_2604_18780_b200 import streaming as S  # noqa: E402
+from paper_2604_18780_b200.potentials import CenteringMode  # noqa: E402
+
+
+def _case(name):
+    z = golden_io.load(name)
+    if z is None:
+        pytest.skip(f"golden_{name}.npz not generated")
+    _, params, cum = scrf.equivalence_instance(int(z["seed"]), T=int(z["T"]), K=int(z["K"]), C=int(z["C"]),
+                                               B=int(z["B"]), mode=CenteringMode(str(z["mode"])))
+    assert golden_io.digest(cum.S) == str(z["S_digest"]), "input stage drifted"
+    return z, params, cum
+
+
+@pytest.mark.parametrize("memory", ["full", "sublinear"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", ["c4f", "c5f", "c3f"])
+def test_full_length_posterior_matches_reference(name, precision, memory):
+    z, params, cum = _case(name)
+    kb = int(z["keep_b"])
+    S.set_precision(precision)
+    try:
+        logZ, grads, marg = scrf.posterior(cum, params, memory=memory)
+    finally:
+        S.set_precision("fp32")
+    tol = parity.TOL[precision]
+    errs = {"logZ": parity.rel_err(logZ, z["logZ"]),
+            "grad_T": parity.scaled_err(grads.grad_T, z["grad_T"]),
+            "grad_B": parity.scaled_err(grads.grad_B, z["grad_B"]),
+            "expected_segment_count": parity.scaled_err(marg.expected_segment_count, z["expected_segment_count"]),
+            "grad_S": parity.scaled_err(grads.grad_S[:kb][:, z["rows_s"]], z["grad_S"]),
+            "position_marginals": parity.scaled_err(marg.position_marginals[:kb][:, z["rows_p"]],
+                                                    z["position_marginals"]),
+            "boundary_posterior": parity.scaled_err(marg.boundary_posterior[:kb][:, z["rows_p"]],
+                                                    z["boundary_posterior"])}
+    print(name, precision, memory, {k: f"{v:.1e}" for k, v in errs.items()})
+    bad = {k: v for k, v in errs.items() if v > (tol["logZ"] if k == "logZ" else tol["grad"])}
+    assert not bad, (bad, errs)
+    # whole-array checksums the fixture holds (every position, not just the sample)
+    np.testing.assert_allclose(marg.position_marginals.sum(axis=(1, 2)), z["pm_total"], rtol=tol["grad"])
+    np.testing.assert_allclose(marg.boundary_posterior.sum(axis=1), z["bp_total"], rtol=tol["grad"])
+
+
+@pytest.mark.parametrize("name", ["c4f", "c5f", "c3f"])
+def test_full_length_viterbi_bit_identical(name):
+    z, params, cum = _case(name)
+    segs, scores = scrf.decode(cum, params)
+    exp = golden_io._outputs(z)
+    assert np.array_equal(scores, z["vit_scores"])
+    assert [s.segments for s in segs] == exp["vit_segments"]
