@@ -50,7 +50,10 @@ def make_full(name, seed, T, K, C, B, mode, ragged=False, projections=False, kee
     ri = n_ck // 2
     t_lo = ri * ck.delta
     t_hi = min((ri + 1) * ck.delta, T)
-    block = recompute_alpha(ck.omega[:, ri], ck.N[:, ri], cum, params, t_lo, t_hi)
+    # a COPY of the snapshot: with B = 1 the reference's recompute_alpha restores its ring as a
+    # view of omega_i (np.ascontiguousarray of a size-1-axis transpose is a view) and would
+    # overwrite the checkpoint set that streaming_backward replays from next
+    block = recompute_alpha(ck.omega[:, ri].copy(), ck.N[:, ri], cum, params, t_lo, t_hi)
     print(f"{name}: replay {time.time() - t0:.0f}s", flush=True)
     grads, marg = streaming_backward(cum, params, logZ, ck)
     print(f"{name}: backward {time.time() - t0:.0f}s", flush=True)
