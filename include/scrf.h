@@ -175,6 +175,15 @@ int scrf_recompute_alpha_work_bytes(const scrf_problem* p, int64_t t_start, int6
 int scrf_recompute_alpha(const scrf_problem* p, int precision, const double* omega_i, int64_t t_start,
                          int64_t t_end, double* block, void* work, size_t work_bytes, void* stream);
 
+/* The fixed-order batch reduction of per-sequence partials: out[i] = sum over b = 0..B-1, in
+ * order, of upstream[b] * parts[b][i] (upstream NULL = ones), one rounding per multiply and per
+ * add. scrf_backward / scrf_posterior finish with exactly this reduction over their
+ * *_partials, so a batch sharded across ranks (all-gather the partials in batch order, then
+ * this call) reproduces the single-GPU grad_T / grad_B bit for bit (the reference reduces in a
+ * fixed order too, streaming.py:389-395). */
+int scrf_reduce_partials(int64_t B, int64_t n, const double* parts, const double* upstream, double* out,
+                         void* stream);
+
 /* Clamp-event count per sequence (B,) int32 after scrf_forward (ckpt) and optionally
  * scrf_backward / scrf_posterior (work, or NULL): positions whose max alpha message relative
  * to the checkpoint normaliser, or max (unnormalised) beta message, leaves +-1e6 -- where the

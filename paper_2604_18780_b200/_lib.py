@@ -79,6 +79,7 @@ _SIGS = {
     "scrf_export_checkpoints_sparse": (_int, [_P, _i64, _int, _vp, _vp, _vp, _vp]),
     "scrf_recompute_alpha_work_bytes": (_int, [_P, _i64, _i64, _int, _psz]),
     "scrf_recompute_alpha": (_int, [_P, _int, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
+    "scrf_reduce_partials": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
     "scrf_position_outputs_event": (None, [_vp]),

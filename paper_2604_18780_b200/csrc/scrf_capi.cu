@@ -311,11 +311,13 @@ PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   long long want = (blk ? 2LL : 4LL) * num_sms();
   long long per = blk ? want / ((long long)ngc * B) : (want + (long long)ngc * B - 1) / ((long long)ngc * B);
   if (per < 1) per = 1;
-  int scb = (int)((Wn + per - 1) / per);
-  scb = (scb + kGBSub - 1) / kGBSub * kGBSub;
-  if (scb < kGBSub) scb = kGBSub;
-  q.SCB = scb;
-  q.nchB = (Wn + scb - 1) / scb;
+  // CTA source ranges are whole micro-chunks; partials are kept per micro-chunk (the
+  // per-sequence grad_B sum order depends on T only, not on B: sharding stays bit-identical)
+  const int nmic = (Wn + kGBMicro - 1) / kGBMicro;
+  int mper = (int)((nmic + per - 1) / per);
+  if (mper < 1) mper = 1;
+  q.SCB = mper * kGBMicro;
+  q.nchB = nmic;
   return q;
 }
 
@@ -685,7 +687,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     e = cudaFuncSetAttribute(post_gradB_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    post_gradB_blk_kernel<<<dim3(q.nchB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(
+    post_gradB_blk_kernel<<<dim3((q.nchB * kGBMicro + q.SCB - 1) / q.SCB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(
         *reinterpret_cast<const PostArgs<float>*>(&a));
   } else {
     // one CTA holds every duration window of its label group (K <= kGBW * 512 * kGBJ = 4096)
@@ -694,7 +696,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     e = cudaFuncSetAttribute(post_gradB_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    post_gradB_kernel<R><<<dim3(q.nchB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(a);
+    post_gradB_kernel<R><<<dim3((q.nchB * kGBMicro + q.SCB - 1) / q.SCB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(a);
   }
   {
     const int nT = C * C, nB = K * C;
@@ -1617,6 +1619,16 @@ int scrf_recompute_alpha(const scrf_problem* p, int precision, const double* ome
     ra_block_kernel<float><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
         omega_i, p->lengths, B, K, C, t0, t1, tf0, RL.rows, (const float*)(wb + RL.oY), (const double*)(wb + RL.on),
         block);
+  return (int)cudaGetLastError();
+}
+
+int scrf_reduce_partials(int64_t B, int64_t n, const double* parts, const double* upstream, double* out,
+                         void* stream) {
+  if (B < 1 || n < 1) return SCRF_EDIM;
+  if (!parts || !out) return SCRF_ENULL;
+  ++g_launches;
+  post_reduce2_kernel<<<(unsigned)((n + 31) / 32), 256, 0, (cudaStream_t)stream>>>((int)B, (int)n, 1, parts, upstream,
+                                                                                     nullptr, out);
   return (int)cudaGetLastError();
 }
 

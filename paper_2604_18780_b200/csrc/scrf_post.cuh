@@ -221,6 +221,7 @@ __global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, i
 // one pair per 16 so lanes kGBJ pairs apart hit distinct banks); terms are
 // (ra_hi + rb_hi) + (ra_lo + rb_lo) + B2[k-1], one ex2 each.
 constexpr int kGBSub = 128;
+constexpr int kGBMicro = 4096;  // grad_B partial granularity (sources); a multiple of kGBSub
 constexpr int kGBJ = 4;
 constexpr int kGBW = 2;  // windows per thread (host keeps CG * ceil(K / kGBJ) <= kGBW * 512)
 __host__ __device__ inline int gb_skew(int ui) { return ui + (ui >> 4); }
@@ -254,10 +255,20 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
 #pragma unroll
     for (int j = 0; j < kGBJ; ++j) acc[w][j] = 0.0;
   const int sbeg = a.w0 + sb * a.SCB;
-  const int send = min(min(sbeg + a.SCB, a.w1), L);  // sources s < L in [w0, w1)
   const int W = a.w1 - a.w0;
+  const int nmic = a.SCB / kGBMicro;
   __syncthreads();
-  for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
+  // partials per micro-chunk of kGBMicro sources (a fixed grid, independent of the batch size
+  // and of how CTAs are laid out: per-sequence sums are bit-identical under batch sharding)
+  for (int mi = 0; mi < nmic; ++mi) {
+  const int slot_m = sb * nmic + mi;
+  if (slot_m >= a.nchB) break;
+  const int send = min(min(sbeg + (mi + 1) * kGBMicro, a.w1), L);  // sources s < L in [w0, w1)
+#pragma unroll
+  for (int w = 0; w < kGBW; ++w)
+#pragma unroll
+    for (int j = 0; j < kGBJ; ++j) acc[w][j] = 0.0;
+  for (int s0 = sbeg + mi * kGBMicro; s0 < send; s0 += kGBSub) {
     __syncthreads();
     const int ns = min(kGBSub, send - s0);
     for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
@@ -329,9 +340,10 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       const int cl = idx / nkb, k0 = (idx % nkb) * kGBJ;
 #pragma unroll
       for (int j = 0; j < kGBJ; ++j)
-        if (k0 + j < K) a.gBp[(((size_t)b * a.nchB + sb) * K + k0 + j) * C + c0 + cl] = acc[w][j];
+        if (k0 + j < K) a.gBp[(((size_t)b * a.nchB + slot_m) * K + k0 + j) * C + c0 + cl] = acc[w][j];
     }
   }
+  }  // micro-chunks
 }
 
 // grad_B partial in exp space (fp32 working type): CTA (b, source range, label group), one warp
@@ -394,9 +406,17 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
 #pragma unroll
     for (int j = 0; j < kGBD; ++j) acc[w][j] = 0.0;
   const int sbeg = a.w0 + sb * a.SCB;
-  const int send = min(min(sbeg + a.SCB, a.w1), L);
+  const int nmic = a.SCB / kGBMicro;
   __syncthreads();
-  for (int s0 = sbeg; s0 < send; s0 += kGBSub) {
+  for (int mi = 0; mi < nmic; ++mi) {  // micro-chunks (see post_gradB_kernel)
+  const int slot_m = sb * nmic + mi;
+  if (slot_m >= a.nchB) break;
+  const int send = min(min(sbeg + (mi + 1) * kGBMicro, a.w1), L);
+#pragma unroll
+  for (int w = 0; w < 2; ++w)
+#pragma unroll
+    for (int j = 0; j < kGBD; ++j) acc[w][j] = 0.0;
+  for (int s0 = sbeg + mi * kGBMicro; s0 < send; s0 += kGBSub) {
     __syncthreads();
     const int ns = min(kGBSub, send - s0);
     for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
@@ -560,9 +580,10 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
 #pragma unroll
     for (int j = 0; j < kGBD; ++j) {
       const int k = pass * kGBPass + kGBD * lane + j;  // duration k + 1
-      if (k < K) a.gBp[(((size_t)b * a.nchB + sb) * K + k) * C + c0 + cl] = acc[slot & 1][j];
+      if (k < K) a.gBp[(((size_t)b * a.nchB + slot_m) * K + k) * C + c0 + cl] = acc[slot & 1][j];
     }
   }
+  }  // micro-chunks
 }
 
 template <typename R>
@@ -613,7 +634,7 @@ __global__ void __launch_bounds__(256) post_reduce2_kernel(int B, int n, int npa
 #pragma unroll
       for (int v = 0; v < 8; ++v) sb += ws[v][lane];
       if (ok && per_seq) per_seq[(size_t)b * n + i] = sb;
-      tot += (upstream ? upstream[b] : 1.0) * sb;
+      tot = __dadd_rn(tot, __dmul_rn(upstream ? upstream[b] : 1.0, sb));
     }
     __syncthreads();
   }
