@@ -1,18 +1,21 @@
 """Benchmark: streaming semi-CRF forward+backward positions/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+                    [--scaling weak|strong] [--memory full|sublinear]
 
-One step = one full forward + backward (logZ, all gradients, all marginals) of the
-batch of BASELINE.json config 4 (B=8, T=100000, K=1000, C=24; synthetic instance
-`equivalence_instance(seed=rank, ..., mode=MEAN)`), followed — for N > 1 — by the
-only cross-GPU exchange of the path: the fixed-rank-order reduction of the shared
-transition / duration gradients over NCCL. Weak scaling: every rank owns its own
-B=8 batch. `value` = all ranks' positions / max-over-ranks device time.
+One step = one full forward + backward (logZ, all gradients, all marginals) of the batch of
+BASELINE.json config 4 (B=8, T=100000, K=1000, C=24; synthetic instance
+`equivalence_instance(seed, ..., mode=MEAN)`), followed -- for N > 1 -- by the path's only
+cross-GPU exchange: the per-sequence grad_T / grad_B partials all-gathered in batch order and
+reduced in a fixed order (bit-identical to one GPU). Weak scaling (default): every rank owns
+its own B=8 batch. Strong scaling: one B=8 batch split across the ranks. `value` = all
+ranks' positions / max-over-ranks device time.
 
-`e2e` = the same metric through the public numpy API (`posterior`) with host inputs
-and host outputs (H2D of S and parameters, D2H of logZ, gradients, marginals) inside
-the timed region. `--impl reference` times the CPU oracle port of the reference
-algorithm (oracle/streaming_oracle.py) on the host cores.
+`e2e` = the same metric through the public numpy API (`posterior`) with host inputs and host
+outputs (H2D of S and parameters, D2H of logZ, gradients, marginals) inside the timed region.
+`--impl reference` times the REAL reference (baseline/_ref, pip-installed from
+/root/reference) on the host cores (steady-state positions, all cores); when baseline/_ref
+is absent, the CPU oracle port of the reference algorithm.
 
 The inputs (S: 8 x 100001 x 24 fp64 = 154 MB) are larger than the 126 MB L2, so no
 explicit flush is done between steps.
@@ -50,6 +53,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the forward-only and Viterbi throughputs (reported beside the headline, SURVEY 8(d))")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--memory", default="full", choices=["full", "sublinear"],
+                    help="working-memory mode of the timed posterior (the other mode is reported in extras)")
     return ap.parse_args()
 
 
@@ -61,10 +67,36 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port of the reference algorithm, steady-state sample
+# CPU baseline: the reference on the host cores, steady-state sample
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def _cpu_worker(args):
+def have_reference() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "streamcrf"))
+
+
+def _ref_worker(args):
+    """Seconds per steady-state position of the REAL reference's streaming_forward +
+    streaming_backward (one sequence): two runs of lengths K + n1 and K + n2 differenced, which
+    cancels the t < K ramp (SURVEY §6.2 method)."""
+    K, C, seed, n1, n2 = args
+    sys.path.insert(0, REF_DIR)
+    from streamcrf.potentials import CenteringMode as RMode
+    from streamcrf.streaming import streaming_backward, streaming_forward
+    from streamcrf.validation import equivalence_instance as ref_instance
+
+    secs = []
+    for n in (n1, n2):
+        _, params, cum = ref_instance(seed, T=K + n, K=K, C=C, B=1, mode=RMode.MEAN)
+        t0 = time.perf_counter()
+        logZ, ck = streaming_forward(cum, params)
+        streaming_backward(cum, params, logZ, ck)
+        secs.append(time.perf_counter() - t0)
+    return (secs[1] - secs[0]) / (n2 - n1)
+
+
+def _port_worker(args):
     cfg, seed, n_steps = args
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import streaming_oracle as oracle
@@ -78,34 +110,38 @@ def _cpu_worker(args):
 
 
 def cpu_baseline(cfg: dict, budget_s: float) -> dict:
-    """positions/s of the reference algorithm (oracle port) on all host cores.
+    """positions/s of the reference's fwd+bwd on all host cores (one sequence per core).
 
-    Each core runs one sequence's steady-state forward + replay + backward
-    positions (t >= K, every duration live); per-position cost is constant there,
-    so rate = cores / seconds-per-position (SURVEY §6.2 method).
-    """
+    The real reference (baseline/_ref) when installed -- kind "reference" -- else the oracle
+    port (kind "port"). Per-position cost is constant once t >= K, so rate = cores / seconds
+    per steady-state position; the sample is a few dozen positions per core."""
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
-    workers = max(1, min(cores, cfg["B"] if cfg["B"] > 1 else cores))
-    # calibrate the number of sampled positions to the time budget
-    probe = _cpu_worker((cfg, 0, 2))
-    n_steps = int(max(2, min(200, budget_s / max(probe, 1e-6) / 1.5)))
-    with mp.get_context("spawn").Pool(workers) as pool:
-        t0 = time.perf_counter()
-        secs = pool.map(_cpu_worker, [(cfg, s, n_steps) for s in range(workers)])
-        wall = time.perf_counter() - t0
+    workers = max(1, min(cores, 8))
+    K, C = cfg["K"], cfg["C"]
+    t0 = time.perf_counter()
+    if have_reference():
+        n1, n2 = 8, 8 + max(16, min(64, int(budget_s)))
+        with mp.get_context("spawn").Pool(workers) as pool:
+            secs = pool.map(_ref_worker, [(K, C, s, n1, n2) for s in range(workers)])
+        kind = "reference"
+        sample = (f"baseline/_ref streamcrf 0.1.0 (the reference, pip-installed from /root/reference): "
+                  f"streaming_forward + streaming_backward of one sequence per process, lengths K+{n1} and "
+                  f"K+{n2} differenced (steady state t >= K), K={K}, C={C}, {workers} processes")
+    else:
+        probe = _port_worker((cfg, 0, 2))
+        n_steps = int(max(2, min(200, budget_s / max(probe, 1e-6) / 1.5)))
+        with mp.get_context("spawn").Pool(workers) as pool:
+            secs = pool.map(_port_worker, [(cfg, s, n_steps) for s in range(workers)])
+        kind = "port"
+        sample = (f"oracle/streaming_oracle.py (reference algorithm, fp64 numpy) steady-state fwd+replay+bwd, "
+                  f"{n_steps} positions per process, K={K}, C={C}, {workers} processes")
+    wall = time.perf_counter() - t0
     per_pos = float(np.mean(secs))
-    value = workers / per_pos
-    return {
-        "value": value,
-        "unit": UNIT,
-        "cores": workers,
-        "kind": "port",
-        "sample": (f"oracle/streaming_oracle.py (reference algorithm, fp64 numpy) steady-state fwd+replay+bwd "
-                   f"positions t>=K at K={cfg['K']}, C={cfg['C']}: {n_steps} positions per core on {workers} "
-                   f"processes x 1 sequence, {wall:.1f}s wall; value = cores / mean s-per-position"),
-    }
+    return {"value": workers / per_pos, "unit": UNIT, "cores": workers, "kind": kind,
+            "sample": sample + f"; {wall:.1f}s wall; value = processes / mean s-per-position",
+            "seconds_per_position": per_pos}
 
 
 # ---------------------------------------------------------------------------
@@ -190,6 +226,7 @@ def run_ours(args, rank, world, local):
     import paper_2604_18780_b200 as scrf
     from paper_2604_18780_b200 import _lib
     from paper_2604_18780_b200 import streaming as S
+    from paper_2604_18780_b200.dist import reduce_shared_grads_exact, shard_bounds
     from paper_2604_18780_b200.instances import CONFIGS
 
     torch.cuda.set_device(local)
@@ -203,59 +240,67 @@ def run_ours(args, rank, world, local):
 
         dist.init_process_group("nccl", device_id=dev)
 
-    # synthetic instance of the config's shape (per-rank seed: weak scaling)
-    _, params, cum = scrf.equivalence_instance(rank, T=T, K=K, C=C, B=B, mode=scrf.CenteringMode.MEAN)
+    # synthetic instance of the config's shape: weak scaling -> every rank its own B-sequence
+    # batch (seed = rank); strong scaling -> one B-sequence batch, this rank's contiguous shard
+    if args.scaling == "weak":
+        _, params, cum = scrf.equivalence_instance(rank, T=T, K=K, C=C, B=B, mode=scrf.CenteringMode.MEAN)
+        B_glob, lo = B * world, rank * B
+    else:
+        _, params, cum_all = scrf.equivalence_instance(0, T=T, K=K, C=C, B=B, mode=scrf.CenteringMode.MEAN)
+        lo, hi = shard_bounds(B, rank, world)
+        from dataclasses import replace
+
+        cum = replace(cum_all, S=cum_all.S[lo:hi], lengths=np.asarray(cum_all.lengths)[lo:hi])
+        B_glob = B
+    B_loc = cum.batch_size
     prob = scrf.DeviceProblem.from_host(cum, params, device=dev)
     torch.cuda.synchronize()
     lib = _lib.load()
 
-    ev_main = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for e in ev_main:  # torch creates the CUDA event lazily on first record
-        e.record()
-    torch.cuda.synchronize()
-    bwd_ms, fwd_ms = [], []
-    launches = [0]
+    def step():
+        fwd, bw = S.device_posterior(prob, memory=args.memory)
+        n = lib.scrf_last_launch_count()
+        if world > 1:
+            # the path's only collective: per-sequence grad_T / grad_B partials gathered in batch
+            # order, fixed-order reduction (bit-identical to the single-GPU result)
+            gT, gB = S.device_grad_partials(prob, fwd, bw)
+            reduce_shared_grads_exact(gT, gB, B_glob)
+            n += 3
+        return n
 
-    from paper_2604_18780_b200.dist import reduce_shared_grads
-
-    def exchange(fwd, bw):
-        # the path's only collective: fixed-rank-order sum of grad_T / grad_B partials
-        return reduce_shared_grads(bw.grad_T, bw.grad_B)
-
-    def step(record: bool):
-        fwd, bw = S.device_posterior(prob)
-        launches[0] += lib.scrf_last_launch_count()
-        exchange(fwd, bw)
-        return bw
-
-    # warmup
     for _ in range(args.warmup):
-        step(False)
+        step()
     torch.cuda.synchronize()
 
     # live kernel timing (events around the fused alpha/beta sweep launch, on the launching stream)
+    ev_main = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for e in ev_main + ev_step:  # torch creates the CUDA event lazily on first record
+        e.record()
+    torch.cuda.synchronize()
+    sweep_ms, step_ms = [], []
     for _ in range(min(2, args.steps)):
         lib.scrf_profile_events(ev_main[0].cuda_event, ev_main[1].cuda_event)
         ev_step[0].record()
-        S.device_posterior(prob)
+        S.device_posterior(prob, memory=args.memory)
         ev_step[1].record()
         lib.scrf_profile_events(None, None)
         torch.cuda.synchronize()
-        fwd_ms.append(ev_main[0].elapsed_time(ev_main[1]))
-        bwd_ms.append(ev_step[0].elapsed_time(ev_step[1]))
+        sweep_ms.append(ev_main[0].elapsed_time(ev_main[1]))
+        step_ms.append(ev_step[0].elapsed_time(ev_step[1]))
 
-    launches[0] = 0
     t_start = torch.cuda.Event(enable_timing=True)
     t_stop = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
+    launches = 0
+    torch.cuda.reset_peak_memory_stats(dev)
     with sampler:
         t_start.record()
         for _ in range(args.steps):
-            step(False)
+            launches += step()
         t_stop.record()
         torch.cuda.synchronize()
     if dist is not None:
@@ -265,28 +310,31 @@ def run_ours(args, rank, world, local):
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    positions = world * B * T
+    positions = B_glob * T
     value = positions / (ms / 1e3)
     clocks = sampler.summary()
     peak_mem = torch.cuda.max_memory_allocated(dev)
 
     out = None
     if rank == 0:
-        # dominant kernel: the fused alpha+beta sweep (one launch): (K*C + C^2) ex2 per position per
-        # direction (SFU-bound roofline); HBM figures beside it from ncu
+        # dominant kernel: the fused alpha+beta sweep (one launch per step): (K*C + C^2) exps per
+        # position per direction in the factored recursion; the blocked tails
+        # evaluate most of the K*C part as FMA against exp-space source blocks, so the MUFU pipe
+        # is far from saturated -- the sweep is bound by the latency of its per-position chain
+        # step (profiles/r02_sweep_summary.txt has the executed MUFU / FMA pipe rates)
         E_sweep = 2 * (K * C + C * C)
-        sweep_avg = float(np.mean(fwd_ms))
-        post_avg = float(np.mean(bwd_ms)) - sweep_avg
+        sweep_avg = float(np.mean(sweep_ms))
+        post_avg = float(np.mean(step_ms)) - sweep_avg
         peak, peak_note = mufu_peak_per_s(clocks["sm_mhz"])
-        achieved = B * T * E_sweep / (sweep_avg / 1e3)
-        # algorithmic HBM bytes of the sweep launch: S read by both sweeps, Y^/X^ fp32 messages and
-        # fp64 normaliser / max-shift rows written
-        alg_bytes = 2 * B * (T + 1) * C * 8 + 2 * 2 * B * (T + 1) * C * 4 + B * (T + 1) * (2 * 8 + 4)
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "r01_sweep_traffic.json")
-        if os.path.exists(tfile) and (B, T, K, C) == (8, 100000, 1000, 24):
+        achieved = B_loc * T * E_sweep / (sweep_avg / 1e3)
+        alg_bytes = 2 * B_loc * (T + 1) * C * 8 + 2 * 2 * B_loc * (T + 1) * C * 4 + B_loc * (T + 1) * 2 * 8
+        traffic, executed = None, None
+        tfile = os.path.join(ROOT, "profiles", "r02_sweep_traffic.json")
+        if os.path.exists(tfile) and (B_loc, T, K, C) == (8, 100000, 1000, 24):
             with open(tfile) as fh:
-                traffic = int(json.load(fh)["bytes_per_launch"])
+                tj = json.load(fh)
+            traffic = int(tj["bytes_per_launch"])
+            executed = tj.get("executed")
         hbm_peak, hbm_src = hbm_peak_gbs()
         out = {
             "metric": METRIC,
@@ -297,50 +345,58 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
-            "dtype": "f32 log-semiring (fp64 prefix sums / normalisers; fp64 outputs)" if args.precision == "fp32" else "f64",
-            "data": "synthetic: equivalence_instance(seed=rank, mode=MEAN) of config 4, per-rank batch",
+            "dtype": ("f32 log-semiring (fp64 prefix sums / normalisers / cut normalisers; fp64 outputs)"
+                      if args.precision == "fp32" else "f64"),
+            "data": f"synthetic: equivalence_instance(seed={'rank' if args.scaling == 'weak' else 0}, mode=MEAN) of "
+                    f"config {args.config[1:]}",
             "config": {
-                "workload": f"BASELINE config 4 fwd+bwd (logZ, grad_S/T/B, marginals), B={B} T={T} K={K} C={C} per GPU",
-                "B_per_gpu": B, "T": T, "K": K, "C": C, "delta": S.choose_checkpoint_interval(T, K),
-                "parallelism": f"batch-sharded dp{world}; grad_T/grad_B fixed-order all_gather-sum over NCCL",
-                "l2": "inputs larger than L2 (S = 154 MB fp64 per GPU); no flush",
+                "workload": f"BASELINE config {args.config[1:]} fwd+bwd (logZ, grad_S/T/B, marginals), "
+                            f"B={B_glob} T={T} K={K} C={C} in total ({B_loc} per GPU)",
+                "B_total": B_glob, "B_per_gpu": B_loc, "T": T, "K": K, "C": C,
+                "delta": S.choose_checkpoint_interval(T, K), "memory_mode": args.memory,
+                "parallelism": f"batch-sharded dp{world}; grad_T/grad_B: per-sequence partials all-gathered "
+                               f"in batch order + fixed-order reduce (bit-identical to 1 GPU)",
+                "l2": "inputs larger than L2 (S = 154 MB fp64 per 8 sequences); no flush",
             },
             "roofline": {
                 "bound": "sfu",
+                "limiter": "latency of the per-position chain step of the alpha/beta recursions "
+                           "(one dependent LSE + C x C GEMV per position); no pipe is saturated",
                 "kernel": "sweep_kernel (alpha and beta message sweeps, one cluster per sequence and direction)",
                 "achieved": achieved / 1e9,
                 "peak": peak / 1e9,
                 "unit": "Gexp2/s",
                 "frac": achieved / peak,
                 "traffic": traffic,
-                "traffic_source": "profiles/r01_sweep_traffic.json (dram__bytes_read+write of one ncu --set full capture)",
+                "traffic_source": "profiles/r02_sweep_traffic.json (dram__bytes_read+write, ncu --set full)",
+                "executed": executed,
                 "hbm": {"algorithmic_bytes": alg_bytes, "achieved": alg_bytes / (sweep_avg / 1e3) / 1e9,
                         "peak": hbm_peak, "unit": "GB/s", "frac": alg_bytes / (sweep_avg / 1e3) / 1e9 / hbm_peak,
-                        "peak_source": hbm_src,
-                        "note": "latency bound: one dependent recurrence step per position, so HBM is far from binding"},
-                "algorithm": "factored: (K*C + C^2) ex2 per position per direction",
-                "per_launch_exps": B * T * E_sweep,
+                        "peak_source": hbm_src},
+                "algorithm": "factored: (K*C + C^2) exps per position per direction (algorithmic count)",
+                "per_launch_exps": B_loc * T * E_sweep,
                 "kernel_ms": sweep_avg,
                 "post_ms": post_avg,
                 "peak_note": peak_note,
             },
             "clocks": clocks,
             "peak_hbm_bytes": int(peak_mem),
-            "gpu_launches": int(launches[0]),
+            "gpu_launches": int(launches),
         }
-    return out, (prob, cum, params, cfg, dev, lib, S, scrf, torch, dist)
+    return out, (prob, cum, params, cfg, dev, lib, S, scrf, torch, dist, B_glob)
 
 
 def e2e_measure(ctx, args):
     """The public numpy API end to end: host arrays in, host arrays out."""
-    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist = ctx
-    B, T, K, C = cfg["B"], cfg["T"], cfg["K"], cfg["C"]
+    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist, B_glob = ctx
+    T, K = cfg["T"], cfg["K"]
+    B = cum.batch_size
     # warm: two calls holding their results, as the timed loop does, so the pinned host blocks
     # of both live result sets are in torch's caching host allocator (steady state)
-    res = scrf.posterior(cum, params)
-    res = scrf.posterior(cum, params)
+    res = scrf.posterior(cum, params, memory=args.memory)
+    res = scrf.posterior(cum, params, memory=args.memory)
     del res
     torch.cuda.synchronize()
     n = max(1, min(3, args.steps))
@@ -348,38 +404,66 @@ def e2e_measure(ctx, args):
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(n):
-        logZ, grads, marg = scrf.posterior(cum, params)
+        logZ, grads, marg = scrf.posterior(cum, params, memory=args.memory)
     wall = (time.perf_counter() - t0) / n
-    world = 1
     if dist is not None:  # every rank runs its shard through the API; the job takes the slowest
         tw = torch.tensor([wall], device=dev, dtype=torch.float64)
         dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         wall = float(tw.item())
-        world = dist.get_world_size()
     h2d = cum.S.nbytes + np.asarray(cum.lengths).nbytes + params.transition.nbytes + params.duration_bias.nbytes
     d2h = (logZ.nbytes + grads.grad_S.nbytes + grads.grad_T.nbytes + grads.grad_B.nbytes
            + marg.position_marginals.nbytes + marg.boundary_posterior.nbytes + marg.expected_segment_count.nbytes
            + B * 4 + B * 8 * (-(-T // S.choose_checkpoint_interval(T, K))))
-    return {"value": world * B * T / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+    return {"value": B_glob * T / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "paper_2604_18780_b200.posterior (numpy in / numpy out, host wall clock, max over ranks)",
             "steps": n}
 
 
-def extras_measure(ctx, args):
-    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist = ctx
-    B, T = cfg["B"], cfg["T"]
-    res = {}
-    for name, fn in (("forward", lambda: S.device_forward(prob)), ("viterbi", lambda: S.device_viterbi(prob))):
+def _time_device(torch, fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
         fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def extras_measure(ctx, args):
+    """Beside the headline: forward only, Viterbi, the other memory mode (throughput and peak
+    device memory of both), and the other BASELINE configs (fwd+bwd and Viterbi)."""
+    prob, cum, params, cfg, dev, lib, S, scrf, torch, dist, B_glob = ctx
+    B, T = prob.B, prob.T
+    res = {}
+    res["forward_positions_per_s"] = B * T / (_time_device(torch, lambda: S.device_forward(prob, sparse=True)) / 1e3)
+    res["viterbi_positions_per_s"] = B * T / (_time_device(torch, lambda: S.device_viterbi(prob)) / 1e3)
+    modes = {}
+    for mode in ("full", "sublinear"):
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        reps = 2
-        for _ in range(reps):
-            fn()
-        b.record()
-        torch.cuda.synchronize()
-        res[name + "_positions_per_s"] = B * T / (a.elapsed_time(b) / reps / 1e3)
+        base = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        ms = _time_device(torch, lambda: S.device_posterior(prob, memory=mode))
+        modes[mode] = {"positions_per_s": B * T / (ms / 1e3), "ms": ms,
+                       "peak_working_bytes": int(torch.cuda.max_memory_allocated(dev) - base),
+                       "input_bytes": int(prob.S.numel() * 8)}
+    res["memory_modes"] = modes
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    others = {}
+    for name in ("c1", "c2", "c3", "c5"):
+        c = CONFIGS[name]
+        _, p2, cum2 = scrf.equivalence_instance(0, T=c["T"], K=c["K"], C=c["C"], B=c["B"], mode=scrf.CenteringMode.MEAN)
+        pr = scrf.DeviceProblem.from_host(cum2, p2, device=dev)
+        n = c["B"] * c["T"]
+        others[name] = {
+            "workload": f"B={c['B']} T={c['T']} K={c['K']} C={c['C']}",
+            "fwd_bwd_positions_per_s": n / (_time_device(torch, lambda: S.device_posterior(pr)) / 1e3),
+            "viterbi_positions_per_s": n / (_time_device(torch, lambda: S.device_viterbi(pr)) / 1e3),
+        }
+        del pr
+    res["other_configs"] = others
     return res
 
 
@@ -393,12 +477,15 @@ def main():
         if rank != 0:
             return 0
         cb = cpu_baseline(cfg, args.cpu_seconds)
+        B_glob = cfg["B"] * (world if args.scaling == "weak" else 1)
         line = {
-            "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": cfg["B"] * cfg["T"] / cb["value"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config 4 fwd+bwd, B={cfg['B']} T={cfg['T']} K={cfg['K']} C={cfg['C']}",
-                       "note": "CPU time per position measured in steady state and scaled to the config"},
+            "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world, "steps": 1,
+            "warmup": 0, "ms_per_step": B_glob * cfg["T"] / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config[1:]} fwd+bwd, B={B_glob} T={cfg['T']} "
+                                   f"K={cfg['K']} C={cfg['C']}",
+                       "note": (f"one steady-state sample (requested --steps {args.steps} --warmup {args.warmup}): "
+                                "CPU seconds per position measured on the host cores and scaled to the config")},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
@@ -415,7 +502,7 @@ def main():
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
         print(json.dumps(out), flush=True)
-    dist = ctx[-1]
+    dist = ctx[-2]
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

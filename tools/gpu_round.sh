@@ -1,0 +1,10 @@
+#!/bin/bash
+# one GPU session: tests, bench, launch list, ncu full capture of the sweep (outputs in gpurun_out/)
+set -x
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+tail -n 5 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 3000 gpurun_out/bench.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-extras --no-cpu > gpurun_out/b_ncu.log 2>&1
+timeout 900 ncu --set full --import-source on -k regex:sweep_kernel -c 1 -o gpurun_out/ncu_sweep python tools/one_posterior.py c4 full > gpurun_out/ncu_sweep.log 2>&1
+ls -la gpurun_out/
