@@ -122,7 +122,7 @@ def cpu_baseline(cfg: dict, budget_s: float) -> dict:
     K, C = cfg["K"], cfg["C"]
     t0 = time.perf_counter()
     if have_reference():
-        n1, n2 = 8, 8 + max(16, min(64, int(budget_s)))
+        n1, n2 = 8, 8 + max(64, min(256, int(16 * budget_s)))
         with mp.get_context("spawn").Pool(workers) as pool:
             secs = pool.map(_ref_worker, [(K, C, s, n1, n2) for s in range(workers)])
         kind = "reference"

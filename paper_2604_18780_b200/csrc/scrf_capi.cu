@@ -221,7 +221,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
 
 // full-mode forward state ("checkpoint buffer"): per-position alpha-side messages
 struct FLayout {
-  size_t Y, X, n, clamp, total;
+  size_t Y, X, n, amx, clamp, total;
 };
 FLayout f_layout(const scrf_problem* p, int prec) {
   FLayout L;
@@ -231,6 +231,7 @@ FLayout f_layout(const scrf_problem* p, int prec) {
   L.Y = o;     o += al(npos * p->C * rs);
   L.X = o;     o += al(npos * p->C * rs);
   L.n = o;     o += al(npos * 8);
+  L.amx = o;   o += al(npos * rs);
   L.clamp = o; o += al(p->B * 4);
   L.total = o;
   return L;
@@ -458,6 +459,7 @@ struct SweepIO {
   double* N;
   int32_t* dead_at;
   int32_t* clamp;
+  void* amx;                 // full-mode alpha: per-position max shift (book_kernel input)
   bool record;               // profiling events around this launch
 };
 
@@ -500,7 +502,8 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
   a.logZb = io.logZb;
   a.dead_at = io.dead_at;
   a.N = io.N;
-  a.clamp = io.clamp;
+  a.clamp = io.store == 1 ? io.clamp : nullptr;
+  a.amx = (R*)io.amx;
   a.delta = (int)delta;
   a.n_ckpt = (int)n_ckpt_of(p->T, delta);
   a.store = io.store;
@@ -524,24 +527,21 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
   cudaError_t e;
-  if (io.tasks) {
-    if (tails && cw1)
-      e = launch_cl(sweep_kernel<R, true, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else if (tails)
-      e = launch_cl(sweep_kernel<R, true, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else if (cw1)
-      e = launch_cl(sweep_kernel<R, false, true, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else
-      e = launch_cl(sweep_kernel<R, false, false, true>, g.G, ncl, g.NT, smem, st, a, io.record);
-  } else {
-    if (tails && cw1)
-      e = launch_cl(sweep_kernel<R, true, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else if (tails)
-      e = launch_cl(sweep_kernel<R, true, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else if (cw1)
-      e = launch_cl(sweep_kernel<R, false, true, false>, g.G, ncl, g.NT, smem, st, a, io.record);
-    else
-      e = launch_cl(sweep_kernel<R, false, false, false>, g.G, ncl, g.NT, smem, st, a, io.record);
+  const int mode = io.tasks ? 2 : (io.store ? 1 : 0);
+#define SCRF_LAUNCH_SWEEP(M)                                                                              \
+  (tails && cw1 ? launch_cl(sweep_kernel<R, true, true, M>, g.G, ncl, g.NT, smem, st, a, io.record)      \
+   : tails    ? launch_cl(sweep_kernel<R, true, false, M>, g.G, ncl, g.NT, smem, st, a, io.record)     \
+   : cw1      ? launch_cl(sweep_kernel<R, false, true, M>, g.G, ncl, g.NT, smem, st, a, io.record)     \
+              : launch_cl(sweep_kernel<R, false, false, M>, g.G, ncl, g.NT, smem, st, a, io.record))
+  e = mode == 2 ? SCRF_LAUNCH_SWEEP(2) : mode == 1 ? SCRF_LAUNCH_SWEEP(1) : SCRF_LAUNCH_SWEEP(0);
+#undef SCRF_LAUNCH_SWEEP
+  if (e != cudaSuccess) return (int)e;
+  if (!io.tasks && io.store == 0 && (io.dirs & 1)) {
+    // full mode: the reference bookkeeping of the alpha sweep from the stored rows
+    ++g_launches;
+    book_kernel<R><<<a.B, 1024, 0, st>>>(a.Y[0], a.n[0], a.amx, p->lengths, a.T, a.C, a.delta, a.n_ckpt, a.N,
+                                        a.dead_at, a.logZ, io.clamp);
+    e = cudaGetLastError();
   }
   return (int)e;
 }
@@ -1089,6 +1089,7 @@ int scrf_forward(const scrf_problem* p, int64_t delta, int precision, double* lo
   io.Y[0] = fb + F.Y;
   io.X[0] = fb + F.X;
   io.n[0] = (double*)(fb + F.n);
+  io.amx = fb + F.amx;
   io.clamp = (int32_t*)(fb + F.clamp);
   io.logZ = logZ;
   io.N = N;
@@ -1145,6 +1146,7 @@ static int full_sweeps(const scrf_problem* p, int64_t delta, int precision, int 
     io.Y[0] = fb + F.Y;
     io.X[0] = fb + F.X;
     io.n[0] = (double*)(fb + F.n);
+    io.amx = fb + F.amx;
     io.clamp = (int32_t*)(fb + F.clamp);
     io.logZ = logZ;
     io.N = N;

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       R2 v;
       v.x = Mth<R>::ninf();
       v.y = 0;
-      if (u <= L && ui < kGBSub + K) {
+      if (u <= L && u < a.w1 + K && ui < kGBSub + K) {  // (beta rows of a window end at w1 + K - 1)
         const size_t o = (rb0 + u) * C + c;
         const size_t ob = rowB(a, b, u);
         const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
     for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
       const int cl = i / nU, ui = i % nU, u = s0 + 1 + ui, c = c0 + cl;
       float2 v = make_float2(-CUDART_INF_F, 0.f);
-      if (u <= L && ui < kGBSub + K) {
+      if (u <= L && u < a.w1 + K && ui < kGBSub + K) {  // (beta rows of a window end at w1 + K - 1)
         const size_t o = (rb0 + u) * C + c;
         const size_t ob = rowB(a, b, u);
         const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +

@@ -163,6 +163,7 @@ struct SweepArgs {
   double* logZb;     // [B] nats (beta: LSE_c beta[0,c], consistency value)
   int32_t* dead_at;  // [B]
   int32_t* clamp;    // [B] alpha positions whose max message leaves the reference's +-CLAMP_LIMIT (or null)
+  R* amx;            // [B][T+1] full mode, alpha: per-position max shift (-inf: dead position), or null
   double* N;         // [B][n_ckpt] reference checkpoint normalisers
   int delta, n_ckpt;
   // storage mode of the per-position outputs Y^, X^, n:
@@ -642,8 +643,20 @@ __device__ __forceinline__ long long out_row(const SweepArgs<R>& a, const SweepC
 
 template <typename R>
 __device__ __forceinline__ void put_out(const SweepArgs<R>& a, const SweepCtx& x, int t, int c, bool act, R y, R xv,
-                                        double n) {
+                                        double n, R am) {
   const int C = a.C;
+  if (!x.task && a.store == 0) {  // full mode: every position, row b*(T+1)+t
+    const long long row = (long long)x.b * (a.T + 1) + t;
+    if (act) {
+      a.Y[x.dir][row * C + c] = y;
+      a.X[x.dir][row * C + c] = xv;
+    }
+    if (c == 0) {
+      a.n[x.dir][row] = n;
+      if (x.dir == 0 && a.amx) a.amx[row] = am;
+    }
+    return;
+  }
   const long long row = out_row(a, x, t);
   if (row >= 0) {
     if (act) {
@@ -703,7 +716,7 @@ __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx&
   }
   const int sl = q & pm;
   const int cs = act ? c : 0;
-  put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[q & (kNring - 1)]);
+  put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[q & (kNring - 1)], h.pubA[sl]);
 }
 
 // per-position outputs (Y^, X^, n, max shift) of positions q-3 .. q from the published rings
@@ -717,7 +730,8 @@ __device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepC
     const int pos = q - 3 + i;
     if (pos >= 0) {
       const int sl = pos & 15;
-      put_out<R>(a, x, x.tpos(pos), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[pos & (kNring - 1)]);
+      put_out<R>(a, x, x.tpos(pos), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[pos & (kNring - 1)],
+                 h.pubA[sl]);
     }
   }
 }
@@ -811,7 +825,7 @@ __device__ __noinline__ R gemv_exact(const double* trans, int dir, int C, int NC
 // chain syncs; count NB. Every id is used with one count only.
 
 // ======================= chain warps =======================
-template <typename R, bool CW1, bool REPLAY>
+template <typename R, bool CW1, int MODE>
 __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int NB) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
@@ -899,23 +913,23 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   // computed ones; X^ (the transition GEMV) and everything downstream are recomputed, so the
   // replay reproduces the sweep that stored them (same positions mod 32, same arithmetic).
   // Forced rows are prefetched one position ahead.
-  const SweepTask* tk = REPLAY ? x.task : nullptr;
-  const int nforce = REPLAY ? tk->nforce : 0;
+  const SweepTask* tk = (MODE == 2) ? x.task : nullptr;
+  const int nforce = (MODE == 2) ? tk->nforce : 0;
   const int cs = act ? c : 0;
-  const R* fY = REPLAY ? a.fY[x.dir] + (long long)tk->frow * C + cs : nullptr;
-  const double* fN = REPLAY ? a.fN[x.dir] + tk->frow : nullptr;
-  const long long fsC = REPLAY ? (long long)tk->fstep * C : 0;
-  const int fs1 = REPLAY ? tk->fstep : 0;
+  const R* fY = (MODE == 2) ? a.fY[x.dir] + (long long)tk->frow * C + cs : nullptr;
+  const double* fN = (MODE == 2) ? a.fN[x.dir] + tk->frow : nullptr;
+  const long long fsC = (MODE == 2) ? (long long)tk->fstep * C : 0;
+  const int fs1 = (MODE == 2) ? tk->fstep : 0;
   R fq = Mth<R>::ninf();
   double nq = 0.0;
-  if (REPLAY && nforce > 0) {
+  if ((MODE == 2) && nforce > 0) {
     fq = act ? fY[0] : Mth<R>::ninf();
     nq = fN[0];
   }
   // position 0: alpha[0] = 0 (virtual source) / beta[L] = 0, or the first forced position
   const R yh0 = nforce > 0 ? fq : (x.dir == 0 ? (R)0 : Mth<R>::ninf());
   const double n0 = nforce > 0 ? nq : 0.0;
-  if (REPLAY && nforce > 1) {
+  if ((MODE == 2) && nforce > 1) {
     fq = act ? fY[fsC] : Mth<R>::ninf();
     nq = fN[fs1];
   }
@@ -936,18 +950,14 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   double n_prev = n0;
   // alpha: checkpoint normaliser in effect (log2) and the position counter since the last
   // checkpoint (streaming.py:205-214); beta: 0 (absolute frame)
-  double n_ref = REPLAY ? tk->n_ref : 0.0;
-  int ck_cnt = REPLAY ? tk->ck_phase : 0;
-  // reference bookkeeping of a full alpha sweep (checkpoint normalisers N_i, first dead
-  // position, clamp events): rare events, so the state lives in shared memory (h.wmax
-  // words 8..10), not in registers of this latency-bound loop
-  const bool book = !REPLAY && x.dir == 0 && tid == 0;
-  int* bk = (int*)(h.wmax + 8);  // [0] first dead position, [1] clamp events
-  if (book) {
-    bk[0] = -1;
-    bk[1] = 0;
-    if (a.N) a.N[(size_t)x.b * a.n_ckpt] = 0.0;
-  }
+  double n_ref = (MODE == 2) ? tk->n_ref : 0.0;
+  int ck_cnt = (MODE == 2) ? tk->ck_phase : 0;
+  // reference bookkeeping of the alpha sweep (streaming.py:194-229): in the full mode a
+  // post-pass reads it off the stored per-position messages (book_kernel); the checkpoint-row
+  // (sublinear) sweep stores too few positions for that, so its chain keeps it
+  const bool sbook = MODE == 1 && x.dir == 0;
+  int dmin = -1, n_clamp = 0;
+  if (sbook && tid == 0 && a.N) a.N[(size_t)x.b * a.n_ckpt] = 0.0;
   const R2* partc = h.part + cs;
   const typename Vec4<R>::T* hhc = h.hh + cs;
   const int pubm = g.PubS - 1;
@@ -958,15 +968,12 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     constexpr long long* tr = nullptr;
 #endif
     if (tr) tr[0] = clock64();
-    // guard threshold of this position in the chain's frame, computed before the wait (the
-    // guard is 1e9 wide: fp32 is exact enough for it)
-    const R thr = (R)(n_ref + kGuardL2 - n_prev);
     nbar_sync(BAR_B + (p & 3), NB);
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(4, p);
     bool dead;
     R yh, am;
     double n_p;
-    if (REPLAY && p < nforce) {
+    if ((MODE == 2) && p < nforce) {
       yh = fq;
       n_p = nq;
       am = (R)(n_p - n_prev);  // the stored sweep's shift (exact: n_p = n_prev + (double)am there)
@@ -988,7 +995,9 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       // the reference's guard (_numerics.py:59-75): a position whose every message is at or below
       // NEG_INF + 1 in the reference frame (alpha: relative to the checkpoint normaliser in effect,
       // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
-      dead = (am == Mth<R>::ninf()) || am <= thr;
+      dead = (am == Mth<R>::ninf());
+      // (a max shift below -1e8 is the only way to reach the 1e9-wide guard: exact test only then)
+      if (am < (R)-1e8) dead = dead || (n_prev + (double)am) - n_ref <= kGuardL2;
       yh = dead ? Mth<R>::ninf() : y - am;
       n_p = dead ? n_prev : n_prev + (double)am;
     }
@@ -1004,17 +1013,14 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     nbar_arrive(BAR_A + (p & 3), NA + ((p & 3) == 0 ? NAE : 0));
     if (blockIdx.x == 0 && tid == 0) SCRF_GT(5, p);
     if (tr) tr[3] = clock64();
-    // bookkeeping after the hand-off (off the critical path)
-    if (book) {
-      if (dead && bk[0] < 0) bk[0] = p;
-      // the reference clamps finite messages to +-1e6 relative to the checkpoint normaliser
-      // (_numerics.py:41-56, streaming.py:150-152): count the positions where that would fire
-      if (!dead && fabs(n_p - n_ref) > kClampLimit * kLog2e) ++bk[1];
+    if (sbook) {  // sparse alpha sweep: reference bookkeeping in registers (see below)
+      dmin = (dead && dmin < 0) ? p : dmin;
+      n_clamp += (!dead && fabs(n_p - n_ref) > kClampLimit * kLog2e) ? 1 : 0;
     }
     if (x.dir == 0 && ++ck_cnt == a.delta) {  // checkpoint shift at t % delta == 0 (live, alive only)
       ck_cnt = 0;
       if (!dead) n_ref = n_p;
-      if (book && a.N && p / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + p / a.delta] = n_ref * kLn2;
+      if (sbook && tid == 0 && a.N && p / a.delta < a.n_ckpt) a.N[(size_t)x.b * a.n_ckpt + p / a.delta] = n_ref * kLn2;
     }
     x4h = x3h;
     x3h = x2h;
@@ -1025,9 +1031,9 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     a1 = dead ? (R)0 : am;
     n_prev = n_p;
   }
-  if (!REPLAY && x.dir == 0) {
-    // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats), streaming.py:216-229; the reference raises only
-    // when the final log-partition is at or below the guard, naming the first dead position
+  if (sbook) {
+    // logZ = n_L + log2 sum_c 2^(Y^[L,c]) (nats); the reference raises only when the final
+    // log-partition is at or below the guard, naming the first dead position (streaming.py:216-229)
     R sm = act ? Mth<R>::ex2(h.pubY[(L & pubm) * C + c]) : (R)0;
     for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
     if (g.NCW > 1) {
@@ -1041,8 +1047,8 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       if (a.logZ) a.logZ[x.b] = lz;
       if (a.N)
         for (int i = L / a.delta + 1; i < a.n_ckpt; ++i) a.N[(size_t)x.b * a.n_ckpt + i] = n_ref * kLn2;  // frozen past L
-      if (a.dead_at) a.dead_at[x.b] = (lz - n_ref * kLn2 > kGuard) ? -1 : (bk[0] >= 0 ? bk[0] : L);
-      if (a.clamp) a.clamp[x.b] = bk[1];
+      if (a.dead_at) a.dead_at[x.b] = (lz - n_ref * kLn2 > kGuard) ? -1 : (dmin >= 0 ? dmin : L);
+      if (a.clamp) a.clamp[x.b] = n_clamp;
     }
   }
 }
@@ -1233,7 +1239,8 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
                    t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
     if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
     if (!do_edge && q > Lq)  // outputs of the positions after the last edge batch
-      put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q);
+      put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q, h.pubA[sl]);
+
     if (x.dir == 1 && q == L && c == 0 && !x.task) {
       const R* pX = h.pubX + sl * C;
       R mx = Mth<R>::ninf();
@@ -1279,7 +1286,7 @@ __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<
   }
 }
 
-template <typename R, bool TAILS, bool CW1, bool REPLAY>
+template <typename R, bool TAILS, bool CW1, int MODE>
 __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                           const TailLayout& TL) {
   using R2 = typename Vec2<R>::T;
@@ -1350,7 +1357,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   if (TAILS) cluster_sync_all();
 
   if (warp < g.NCW)
-    head_chain<R, CW1, REPLAY>(a, x, h, NA, NAE, NB);
+    head_chain<R, CW1, MODE>(a, x, h, NA, NAE, NB);
   else if (warp < g.NCW + g.NNW)
     head_near<R, TAILS>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
@@ -1772,14 +1779,16 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
 
 // ----------------------------------------------------------------------------
 
-template <typename R, bool TAILS, bool CW1, bool REPLAY>
+// MODE: 0 = full sweep (every position stored), 1 = checkpoint-row sweep (sublinear pass 1,
+// bookkeeping in the chain), 2 = window replay (SweepTask per cluster, forced start)
+template <typename R, bool TAILS, bool CW1, int MODE>
 __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SweepGeo& g = a.geo;
   const int ci = blockIdx.x / g.G;
   SweepCtx x;
   x.task = nullptr;
-  if (REPLAY) {
+  if (MODE == 2) {
     x.task = a.tasks + ci;
     x.b = x.task->b;
     x.dir = x.task->dir;
@@ -1827,10 +1836,66 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   }
 #endif
   if (x.rank == 0)
-    head_main<R, TAILS, CW1, REPLAY>(a, x, smem, HL, TL);
+    head_main<R, TAILS, CW1, MODE>(a, x, smem, HL, TL);
   else if (TAILS)
     tail_main<R>(a, x, smem, HL, TL);
   if (TAILS) cluster_sync_all();
+}
+
+// ----------------------------------------------------------------------------
+// Reference bookkeeping of a full-mode alpha sweep (streaming.py:194-229) from the stored
+// per-position normalisers n_t and max shifts (off the latency-bound chain): checkpoint
+// normalisers N_i (shift = max_c alpha at i*delta, applied only while the sequence is alive,
+// frozen past L), the first dead position (the chain marks it with a max shift of -inf), the
+// positions where the reference would clamp the max message to +-1e6 relative to the
+// normaliser in effect (_numerics.py:41-56), and logZ = LSE_c alpha[L,c]; the reference raises
+// only when the final log-partition is dead. One block per sequence.
+template <typename R>
+__global__ void __launch_bounds__(1024) book_kernel(const R* Ya, const double* na, const R* amx, const int64_t* lengths,
+                                                   int T, int C, int delta, int n_ckpt, double* N, int32_t* dead_at,
+                                                   double* logZ, int32_t* clamp) {
+  const int b = blockIdx.x;
+  const int L = (int)lengths[b];
+  const size_t rb = (size_t)b * (T + 1);
+  double* Nb = N + (size_t)b * n_ckpt;  // N in effect from checkpoint i on
+  __shared__ int dmin, ncl;
+  if (threadIdx.x == 0) {
+    double N_cur = 0.0;
+    Nb[0] = 0.0;
+    for (int i = 1; i < n_ckpt; ++i) {
+      const long long q = (long long)i * delta;
+      if (q <= L && amx[rb + q] != Mth<R>::ninf()) N_cur = na[rb + q] * kLn2;
+      Nb[i] = N_cur;
+    }
+    dmin = 0x7fffffff;
+    ncl = 0;
+  }
+  __syncthreads();
+  int best = 0x7fffffff, cl = 0;
+  for (int q = 1 + threadIdx.x; q <= L; q += blockDim.x) {
+    if (amx[rb + q] == Mth<R>::ninf()) {
+      best = min(best, q);
+    } else {
+      int i = (q - 1) / delta;  // normaliser in effect before the shift at q
+      if (i >= n_ckpt) i = n_ckpt - 1;
+      if (fabs(na[rb + q] * kLn2 - Nb[i]) > kClampLimit) ++cl;
+    }
+  }
+  atomicMin(&dmin, best);
+  atomicAdd(&ncl, cl);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    R s = 0;
+    for (int c = threadIdx.x; c < C; c += 32) s += Mth<R>::ex2(Ya[(rb + L) * C + c]);
+    s = group_sum(s, 32);
+    if (threadIdx.x == 0) {
+      const double lz = (s > (R)0) ? (na[rb + L] + (double)Mth<R>::lg2(s)) * kLn2 : -CUDART_INF;
+      logZ[b] = lz;
+      const double Nfin = Nb[n_ckpt - 1 < (L / delta) ? n_ckpt - 1 : (L / delta)];
+      dead_at[b] = (lz - Nfin > kGuard) ? -1 : (dmin == 0x7fffffff ? L : dmin);
+      if (clamp) clamp[b] = ncl;
+    }
+  }
 }
 
 }  // namespace scrf
