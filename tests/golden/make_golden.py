@@ -193,9 +193,27 @@ def make_train():
     save("train", **arrays)
 
 
+def make_io():
+    """The reference's serialisers (potentials.py:467-552) on a ragged instance with
+    projections: emissions CSV / JSON, params JSON, segmentation JSON (for byte-level checks of
+    this package's writers and readers)."""
+    import json as _json
+
+    batch, params, cum = equivalence_instance(3, T=13, K=4, C=3, B=3, ragged=True, projections=True)
+    P.save_emissions_csv(batch, os.path.join(HERE, "io_emissions.csv"))
+    P.save_emissions_json(batch, os.path.join(HERE, "io_emissions.json"))
+    params = P.SemiCRFParams(params.transition, params.duration_bias, np.arange(3) * 0.25, -np.arange(3) * 0.5)
+    P.save_params_json(params, os.path.join(HERE, "io_params.json"))
+    segs = [P.Segmentation(((0, 2, 1), (2, 3, 0))), P.Segmentation(((0, 1, 2),))]
+    with open(os.path.join(HERE, "io_segments.json"), "w") as fh:
+        _json.dump(P.segmentations_to_json(segs), fh)
+    print("wrote io_* fixtures")
+
+
 M = P.CenteringMode
 JOBS = {
     "masked": make_masked,
+    "io": make_io,
     "train": make_train,
     "small": lambda: make_small(),
     # c1 exactly as BASELINE.json config 1 (MEAN centering, SURVEY §8d), plus ragged+projections.
