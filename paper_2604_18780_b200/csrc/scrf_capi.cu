@@ -325,12 +325,27 @@ PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
 // cut-normaliser spacing (scrf_cut.cuh): 0 disables the correction (SCRF_CUT_D=0, debugging)
 int cut_spacing() { return env_int("SCRF_CUT_D", 512); }
 
+// Full-mode posterior passes (see run_full_post_win): SCRF_OVERLAP 1 = windows concurrent with
+// the sweeps (default), 0 = the same windows after the sweeps, -1 = one pass after the sweeps.
+int ovl_ws() { return env_int("SCRF_OVL_WS", 8192); }
+int ovl_mode(const scrf_problem* p) {
+  const int m = env_int("SCRF_OVERLAP", 1);
+  const int ws = ovl_ws();
+  if (m < 0 || cut_spacing() <= 0 || ws <= 0 || ws % kGBMicro || ws % cut_spacing()) return -1;
+  if ((long long)p->T + 1 < 4LL * ws) return -1;  // too short to gain from windows
+  if ((long long)p->T + 1 > 4096LL * ws) return -1;
+  return m > 0 ? 1 : 0;
+}
+
 // per-pass partials and the running per-sequence accumulators
 struct PLayout {
-  size_t logZb, tot, cntp, gTp, gBp, cutU, corr, carry, clamp, accT, accB, accN, total;
+  size_t logZb, tot, cntp, gTp, gBp, cutU, corr, carry, clamp, accT, accB, accN, Zt, tcut, prog, status, RA, RB, Wt,
+      Bmax, total;
+  int prepNR;  // rows of RA / RB per (sequence, label): the longest pass + 2K - 1
 };
-PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o) {
+PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o, int passWn = 0) {
   PLayout L;
+  if (passWn <= 0) passWn = Wn;
   const size_t B = p->B, C = p->C, K = p->K;
   const PostGeo q = post_geo(p, prec, Wn);
   const int d = cut_spacing();
@@ -346,6 +361,15 @@ PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o) {
   L.accT = o;  o += al(B * C * C * 8);
   L.accB = o;  o += al(B * K * C * 8);
   L.accN = o;  o += al(B * 8);
+  L.Zt = o;    o += al(B * 8);
+  L.tcut = o;  o += al(B * 4);
+  L.prog = o;  o += al(B * 2 * kProgSlots * 4);
+  L.status = o; o += al(4);
+  L.prepNR = passWn + 2 * (int)K - 1;
+  L.RA = o;    o += al(B * C * (size_t)L.prepNR * 8);
+  L.RB = o;    o += al(B * C * (size_t)L.prepNR * 8);
+  L.Wt = o;    o += al(C * (2 * K + 2 * kCutEC) * 8);
+  L.Bmax = o;  o += al(C * 8);
   L.total = o;
   return L;
 }
@@ -364,7 +388,8 @@ BLayout b_layout(const scrf_problem* p, int prec) {
   L.Y = o; o += al(npos * C * rs);
   L.X = o; o += al(npos * C * rs);
   L.n = o; o += al(npos * 8);
-  L.P = p_layout(p, prec, (int)p->T + 1, o);
+  // windowed passes (ovl_mode >= 0) need pass rows for one window only
+  L.P = p_layout(p, prec, (int)p->T + 1, o, ovl_mode(p) >= 0 ? ovl_ws() : (int)p->T + 1);
   L.total = L.P.total;
   return L;
 }
@@ -460,6 +485,7 @@ struct SweepIO {
   int32_t* dead_at;
   int32_t* clamp;
   void* amx;                 // full-mode alpha: per-position max shift (book_kernel input)
+  int* prog;                 // full mode: row progress for the overlapped passes (or null)
   bool record;               // profiling events around this launch
 };
 
@@ -514,6 +540,7 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
     a.nW = sg.nW;
   }
   a.tasks = io.tasks;
+  a.prog = io.prog;
   a.trace = g_trace;
   a.trace_from = env_int("SCRF_TRACE_FROM", 64);
   if (env_int("SCRF_WATCHDOG", 0)) {
@@ -572,9 +599,19 @@ __global__ void acc_kernel(int B, int n, int nparts, const double* parts, double
 // One posterior pass over positions [w0, w1): cut normalisers, frame correction, masses /
 // grad_S / grad_P / boundary / coverage (re-anchored at the cuts), grad_T, grad_B, and the
 // accumulation of the pass's transition / duration / count partials.
+// How a pass places its partials. Default (sublinear windows, single full pass): pass-local
+// partial arrays summed into the running accumulators at the end of the pass. Sequence-wide
+// (full-mode windows): the pass writes its chunks of sequence-wide partial arrays and the sums
+// run once after the last window (acc_parts), in the same order as one single pass.
+struct PassOpt {
+  const double* Z = nullptr;  // log Z reference of the masses (null: PostOut::logZ)
+  bool seqwide = false;
+  int pnch = 0, pnchB = 0;    // sequence-wide chunk / micro-chunk counts
+};
+
 template <typename R>
 int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const PostOut& out, unsigned char* wb,
-             const PLayout& PL, bool last, cudaStream_t st) {
+             const PLayout& PL, bool last, cudaStream_t st, const PassOpt& opt = PassOpt()) {
   const int Wn = w1 - w0;
   const PostGeo q = post_geo(p, sizeof(R) == 8, Wn);
   PostArgs<R> a;
@@ -586,7 +623,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   a.ps = p->proj_start;
   a.pe = p->proj_end;
   a.upstream = out.upstream;
-  a.logZ = out.logZ;
+  a.logZ = opt.Z ? opt.Z : out.logZ;
   a.B = (int)p->B;
   a.T = (int)p->T;
   a.K = (int)p->K;
@@ -617,12 +654,39 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   a.nchB = q.nchB;
   a.CGB = q.CGB;
   a.gBp = (double*)(wb + PL.gBp);
+  if (opt.seqwide) {
+    if (w0 % q.CH || w0 % kGBMicro) return SCRF_ECONFIG;
+    a.pq0 = w0 / q.CH;
+    a.pnch = opt.pnch;
+    a.pm0 = w0 / kGBMicro;
+    a.pnchB = opt.pnchB;
+  } else {
+    a.pq0 = 0;
+    a.pnch = q.nch;
+    a.pm0 = 0;
+    a.pnchB = q.nchB;
+  }
   a.gb_range = (float)env_int("SCRF_GB_RANGE", (int)kGBRange);
   const int B = a.B, C = a.C, K = a.K;
   cudaError_t e;
+  // the pass's source / target values, once (shared by the cut and grad_B kernels)
+  a.t_lo = w0 - K + 1;
+  a.NR = Wn + 2 * K - 1;
+  if (a.NR > PL.prepNR) return SCRF_EWORK;
+  a.RA = (double*)(wb + PL.RA);
+  a.RB = (double*)(wb + PL.RB);
+  {
+    const size_t sm = post_prep_smem(C);
+    e = cudaFuncSetAttribute(post_prep_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
+    ++g_launches;
+    post_prep_kernel<R><<<dim3((a.NR + kPrepRows - 1) / kPrepRows, B), 256, sm, st>>>(a);
+  }
   const int cd = cut_spacing();
   const int ncut = cut_slots(w0, w1, cd);
   if (cd > 0) {
+    ++g_launches;
+    cut_w_kernel<R><<<C, 256, 0, st>>>(p->duration_bias, K, C, (R*)(wb + PL.Wt), (double*)(wb + PL.Bmax));
     CutArgs<R> ca;
     memset(&ca, 0, sizeof(ca));
     ca.S = p->S;
@@ -630,7 +694,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ca.dur = p->duration_bias;
     ca.ps = p->proj_start;
     ca.pe = p->proj_end;
-    ca.logZ = out.logZ;
+    ca.logZ = a.logZ;
     ca.B = B;
     ca.T = a.T;
     ca.K = K;
@@ -650,6 +714,12 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ca.d = cd;
     ca.ncut = ncut;
     ca.U = (double*)(wb + PL.cutU);
+    ca.RA = a.RA;
+    ca.RB = a.RB;
+    ca.t_lo = a.t_lo;
+    ca.NR = a.NR;
+    ca.Wt = (const R*)(wb + PL.Wt);
+    ca.Bmax = (const double*)(wb + PL.Bmax);
     const size_t sm = cut_smem<R>(K);
     e = cudaFuncSetAttribute(cut_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;
@@ -672,8 +742,8 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     if (cd > 0 && cd % q.CH == 0)
       cut_prefix_kernel<<<(B * C + 127) / 128, 128, 0, st>>>(p->lengths, B, C, q.nch, q.CH, w0, w1, cd, ncut,
                                                            (const double*)(wb + PL.cutU), a.tot,
-                                                           (double*)(wb + PL.carry));
-    else if (w0 == 0)
+                                                           opt.seqwide ? nullptr : (double*)(wb + PL.carry));
+    else if (w0 == 0 && !opt.seqwide)
       post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
     else
       return SCRF_ECONFIG;  // windowed passes need the cut normalisers
@@ -698,7 +768,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ++g_launches;
     post_gradB_kernel<R><<<dim3((q.nchB * kGBMicro + q.SCB - 1) / q.SCB, (C + q.CGB - 1) / q.CGB, B), 512, sm, st>>>(a);
   }
-  {
+  if (!opt.seqwide) {
     const int nT = C * C, nB = K * C;
     ++g_launches;
     acc_kernel<<<(B * nT + 255) / 256, 256, 0, st>>>(B, nT, q.nch, a.gTp, (double*)(wb + PL.accT));
@@ -755,6 +825,236 @@ int run_full_post(const scrf_problem* p, const void* fstate, void* work, const P
   if (rc) return rc;
   rc = run_pass<R>(p, m, 0, (int)p->T + 1, out, wb, W.P, true, st);
   if (rc) return rc;
+  return pass_finish(p, wb, W.P, out, st);
+}
+
+// ---------------------------------------------------------------------------
+// Full mode, windowed posterior passes overlapped with the sweeps.
+//
+// Position t has both of its messages once the alpha sweep has passed t and the beta sweep has
+// come down to t, so a window [w0, w1) can run its pass once alpha is through w1 and beta
+// through w0 -- for windows around the middle, while the sweeps are still working on the rest
+// of the sequence. The sweep clusters occupy one CTA on 4 B SMs; the passes run on a second
+// (low-priority) stream on the remaining SMs, each window behind prog_wait_kernel, which spins
+// on the row progress the sweeps' writer warps publish (SweepArgs::prog). The final log Z is not
+// known until the sweeps end, so the masses use a provisional log Z from one cut normaliser at
+// the middle of each sequence (probe_finish_kernel); the cut normalisers divide it out again
+// (scrf_cut.cuh). Windows are aligned to 4096 positions, so every chunk / micro-chunk / cut is
+// the one a single pass over [0, T] uses, and the transition / duration / count partials are
+// kept sequence-wide and summed once at the end in the single-pass order: the result does not
+// depend on the window size or on whether the windows ran concurrently (SCRF_OVERLAP=0 runs the
+// same windows after the sweeps, for the bit-identity test).
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// one CTA: returns once every swept direction of every sequence has published its rows through
+// alpha t <= tA / beta t >= tB (probe: the probe cut of each sequence). Gives up after 20 s
+// (sets *status), so a broken sweep cannot hang the stream.
+__global__ void prog_wait_kernel(const int* prog, const int64_t* lengths, int B, int nw, int dirs, int tA, int tB,
+                                 int probe_d, int* status) {
+  for (int i = threadIdx.x; i < 2 * B; i += blockDim.x) {
+    const int b = i >> 1, dir = i & 1;
+    if (!((dirs >> dir) & 1)) continue;
+    const int L = (int)lengths[b];
+    int a0 = tA, b0 = tB;
+    if (probe_d > 0) a0 = b0 = probe_pos(L, probe_d);
+    const int need = dir == 0 ? min(L, max(a0, 0)) + 1 : L - min(L, max(b0, 0)) + 1;
+    const int* sl = prog + (size_t)i * kProgSlots;
+    const long long t0 = gtimer();
+    for (;;) {
+      int mn = 0x7fffffff;
+      for (int w = 0; w < nw; ++w) mn = min(mn, ld_acquire_gpu(sl + w));
+      if (mn >= need) break;
+      if (gtimer() - t0 > 20000000000LL) {
+        atomicExch(status, 1);
+        break;
+      }
+      __nanosleep(500);
+    }
+  }
+}
+
+struct OvlWin {
+  int w0, w1;
+  long long ready;
+};
+
+// windows of [0, T] in the order the sweeps complete them
+int ovl_windows(const scrf_problem* p, OvlWin* w, int cap) {
+  const int ws = ovl_ws();
+  const int T = (int)p->T;
+  int n = 0;
+  for (int w0 = 0; w0 <= T && n < cap; w0 += ws) {
+    const int w1 = w0 + ws < T + 1 ? w0 + ws : T + 1;
+    w[n].w0 = w0;
+    w[n].w1 = w1;
+    w[n].ready = (long long)(w1 > T - w0 ? w1 : T - w0) * 2 + (w0 > T / 2 ? 1 : 0);
+    ++n;
+  }
+  for (int i = 1; i < n; ++i)  // insertion sort by completion step
+    for (int j = i; j > 0 && w[j].ready < w[j - 1].ready; --j) {
+      const OvlWin t = w[j];
+      w[j] = w[j - 1];
+      w[j - 1] = t;
+    }
+  return n;
+}
+
+// writer warps per sweep cluster (SweepArgs::prog slots): output + source warp, or the source warps
+int prog_writers(int C) { return C <= 32 ? 2 : (C + 31) / 32; }
+
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static SideStream ss[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& x = ss[dev & 63];
+  if (!x.s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, lo);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return x;
+}
+
+// before the sweeps: zero the accumulators and the progress slots, fork the side stream
+int ovl_begin(const scrf_problem* p, unsigned char* wb, const PLayout& PL, int mode, cudaStream_t st) {
+  int rc = pass_begin(p, wb, PL, st);
+  if (rc) return rc;
+  cudaError_t e = cudaMemsetAsync(wb + PL.prog, 0, (size_t)p->B * 2 * kProgSlots * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.status, 0, 4, st);
+  if (e == cudaSuccess && mode == 1) {
+    SideStream& ss = side_stream();
+    if (!ss.s) return (int)cudaErrorUnknown;
+    e = cudaEventRecord(ss.fork, st);
+  }
+  return (int)e;
+}
+
+template <typename R>
+int fill_cut_args(const scrf_problem* p, const MsgView& m, const double* Z, CutArgs<R>* ca) {
+  memset(ca, 0, sizeof(*ca));
+  ca->S = p->S;
+  ca->lengths = p->lengths;
+  ca->dur = p->duration_bias;
+  ca->ps = p->proj_start;
+  ca->pe = p->proj_end;
+  ca->logZ = Z;
+  ca->B = (int)p->B;
+  ca->T = (int)p->T;
+  ca->K = (int)p->K;
+  ca->C = (int)p->C;
+  ca->Ya = (const R*)m.Ya;
+  ca->Xa = (const R*)m.Xa;
+  ca->Yb = (const R*)m.Yb;
+  ca->Xb = (const R*)m.Xb;
+  ca->na = m.na;
+  ca->nb = m.nb;
+  ca->rowsA = m.rowsA;
+  ca->tA0 = m.tA0;
+  ca->rowsB = m.rowsB;
+  ca->tB0 = m.tB0;
+  return 0;
+}
+
+// the windowed passes (after ovl_begin and the sweep launch on st); dirs = the directions the
+// sweep in flight computes (their progress is waited on in mode 1)
+template <typename R>
+int run_full_post_win(const scrf_problem* p, const void* fstate, void* work, const PostOut& out, int mode, int dirs,
+                      cudaStream_t st) {
+  const FLayout F = f_layout(p, sizeof(R) == 8);
+  const BLayout W = b_layout(p, sizeof(R) == 8);
+  const unsigned char* fb = (const unsigned char*)fstate;
+  unsigned char* wb = (unsigned char*)work;
+  MsgView m;
+  m.Ya = fb + F.Y;
+  m.Xa = fb + F.X;
+  m.na = (const double*)(fb + F.n);
+  m.Yb = wb + W.Y;
+  m.Xb = wb + W.X;
+  m.nb = (const double*)(wb + W.n);
+  m.rowsA = m.rowsB = (int)p->T + 1;
+  m.tA0 = m.tB0 = 0;
+  const int B = (int)p->B, C = (int)p->C;
+  const int d = cut_spacing();
+  const PostGeo qall = post_geo(p, sizeof(R) == 8, (int)p->T + 1);
+  cudaStream_t sw = st;
+  SideStream* ss = nullptr;
+  if (mode == 1) {
+    ss = &side_stream();
+    sw = ss->s;
+    cudaError_t e = cudaStreamWaitEvent(sw, ss->fork, 0);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int nw = prog_writers(C);
+  int* status = (int*)(wb + W.P.status);
+  // provisional log Z from the middle cut of each sequence
+  if (mode == 1) {
+    ++g_launches;
+    prog_wait_kernel<<<1, 256, 0, sw>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, 0, 0, d, status);
+  }
+  ++g_launches;
+  probe_pos_kernel<<<(B + 127) / 128, 128, 0, sw>>>(p->lengths, B, d, (int*)(wb + W.P.tcut));
+  {
+    CutArgs<R> ca;
+    fill_cut_args<R>(p, m, nullptr, &ca);
+    ca.d = d;
+    ca.ncut = 1;
+    ca.U = (double*)(wb + W.P.cutU);
+    ca.tcut = (const int*)(wb + W.P.tcut);
+    const size_t sm = cut_smem<R>((int)p->K);
+    cudaError_t e = cudaFuncSetAttribute(cut_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return (int)e;
+    ++g_launches;
+    cut_kernel<R><<<dim3(1, (C + kCutCG - 1) / kCutCG, B), 256, sm, sw>>>(ca);
+  }
+  ++g_launches;
+  probe_finish_kernel<R><<<(B + 127) / 128, 128, 0, sw>>>(p->lengths, B, C, (const int*)(wb + W.P.tcut), m.na, m.nb,
+                                                        m.rowsA, m.tA0, m.rowsB, m.tB0,
+                                                        (const double*)(wb + W.P.cutU), (double*)(wb + W.P.Zt));
+  OvlWin win[4096];
+  const int nwin = ovl_windows(p, win, 4096);
+  PassOpt opt;
+  opt.Z = (const double*)(wb + W.P.Zt);
+  opt.seqwide = true;
+  opt.pnch = qall.nch;
+  opt.pnchB = qall.nchB;
+  for (int i = 0; i < nwin; ++i) {
+    if (mode == 1) {
+      ++g_launches;
+      prog_wait_kernel<<<1, 256, 0, sw>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, win[i].w1 + 1,
+                                          win[i].w0 - 1, 0, status);
+    }
+    int rc = run_pass<R>(p, m, win[i].w0, win[i].w1, out, wb, W.P, i == nwin - 1, sw, opt);
+    if (rc) return rc;
+  }
+  if (mode == 1) {
+    cudaError_t e = cudaEventRecord(ss->join, sw);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ss->join, 0);
+    if (e != cudaSuccess) return (int)e;
+  }
+  // the sequence-wide sums, in the single-pass order
+  const int nT = C * C, nB = (int)p->K * C;
+  ++g_launches;
+  acc_kernel<<<(B * nT + 255) / 256, 256, 0, st>>>(B, nT, qall.nch, (const double*)(wb + W.P.gTp),
+                                                   (double*)(wb + W.P.accT));
+  ++g_launches;
+  acc_kernel<<<(B * nB + 255) / 256, 256, 0, st>>>(B, nB, qall.nchB, (const double*)(wb + W.P.gBp),
+                                                   (double*)(wb + W.P.accB));
+  ++g_launches;
+  acc_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, 1, qall.nch, (const double*)(wb + W.P.cntp),
+                                              (double*)(wb + W.P.accN));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
   return pass_finish(p, wb, W.P, out, st);
 }
 
@@ -1133,7 +1433,7 @@ static PostOut post_out(const double* logZ, const double* upstream, double* grad
 
 // full-mode beta sweep into the backward work buffer (dirs 2) or both sweeps (dirs 3)
 static int full_sweeps(const scrf_problem* p, int64_t delta, int precision, int dirs, void* ckpt, void* work,
-                       double* logZ, double* N, int32_t* dead_at, cudaStream_t st) {
+                       double* logZ, double* N, int32_t* dead_at, cudaStream_t st, bool progress = false) {
   const FLayout F = f_layout(p, precision);
   const BLayout W = b_layout(p, precision);
   unsigned char* fb = (unsigned char*)ckpt;
@@ -1156,6 +1456,7 @@ static int full_sweeps(const scrf_problem* p, int64_t delta, int precision, int 
   io.X[1] = wb + W.X;
   io.n[1] = (double*)(wb + W.n);
   io.logZb = (double*)(wb + W.P.logZb);
+  io.prog = progress ? (int*)(wb + W.P.prog) : nullptr;
   return SCRF_DISPATCH(precision, run_sweep)(p, delta, io, st);
 }
 
@@ -1169,10 +1470,16 @@ int scrf_backward(const scrf_problem* p, int64_t delta, int precision, const dou
   if (rc) return rc;
   if (work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  rc = full_sweeps(p, delta, precision, 2, (void*)ckpt, work, nullptr, nullptr, nullptr, st);
-  if (rc) return rc;
   const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
                              boundary_posterior, expected_segment_count);
+  const int om = ovl_mode(p);
+  if (om >= 0) {
+    rc = ovl_begin(p, (unsigned char*)work, b_layout(p, precision).P, om, st);
+    if (rc) return rc;
+  }
+  rc = full_sweeps(p, delta, precision, 2, (void*)ckpt, work, nullptr, nullptr, nullptr, st, om == 1);
+  if (rc) return rc;
+  if (om >= 0) return SCRF_DISPATCH(precision, run_full_post_win)(p, ckpt, work, o, om, 2, st);
   return SCRF_DISPATCH(precision, run_full_post)(p, ckpt, work, o, st);
 }
 
@@ -1187,10 +1494,16 @@ int scrf_posterior(const scrf_problem* p, int64_t delta, int precision, const do
   if (!N || !dead_at) return SCRF_ENULL;
   if (ckpt_bytes < f_layout(p, precision).total || work_bytes < b_layout(p, precision).total) return SCRF_EWORK;
   cudaStream_t st = (cudaStream_t)stream;
-  rc = full_sweeps(p, delta, precision, 3, ckpt, work, logZ, N, dead_at, st);
-  if (rc) return rc;
   const PostOut o = post_out(logZ, upstream, grad_S, grad_T, grad_B, grad_P_start, grad_P_end, position_marginals,
                              boundary_posterior, expected_segment_count);
+  const int om = ovl_mode(p);
+  if (om >= 0) {
+    rc = ovl_begin(p, (unsigned char*)work, b_layout(p, precision).P, om, st);
+    if (rc) return rc;
+  }
+  rc = full_sweeps(p, delta, precision, 3, ckpt, work, logZ, N, dead_at, st, om == 1);
+  if (rc) return rc;
+  if (om >= 0) return SCRF_DISPATCH(precision, run_full_post_win)(p, ckpt, work, o, om, 3, st);
   return SCRF_DISPATCH(precision, run_full_post)(p, ckpt, work, o, st);
 }
 

@@ -47,7 +47,36 @@ struct CutArgs {
   int d;                       // cut spacing
   int ncut;                    // cut slots per sequence: w0, w0 + d, ..., and min(w1, L) (last used slot)
   double* U;                   // [B][ncut][C] per-label contributions to U_t
+  const int* tcut;             // probe mode: one cut per sequence at tcut[b] (slot 0), or null
+  // pass mode: the pass's transposed source / target values (PostArgs::RA / RB, post_prep_kernel)
+  // and the duration weights w[c][i] = 2^(B[i - kCutEC - 1, c] - Bmax[c]) (cut_w_kernel)
+  const double *RA, *RB;
+  int t_lo, NR;
+  const R* Wt;
+  const double* Bmax;
 };
+
+// per-label duration weights of the cut kernel (independent of the cut): Wt[c][i], i in [0, 2K +
+// 2 kCutEC), k = i - kCutEC, w = 2^(B[k-1,c] - Bmax[c]) for k in 1..K, else 0
+template <typename R>
+__global__ void cut_w_kernel(const double* dur, int K, int C, R* Wt, double* Bmax) {
+  __shared__ double red[8];
+  const int c = blockIdx.x;
+  double bm = -CUDART_INF;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) bm = fmax(bm, dur[(size_t)k * C + c] * kLog2e);
+  for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = bm;
+  __syncthreads();
+  bm = -CUDART_INF;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) bm = fmax(bm, red[i]);
+  const int NW = 2 * K + 2 * kCutEC;
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+    const int k = i - kCutEC;
+    Wt[(size_t)c * NW + i] =
+        (bm > -CUDART_INF && k >= 1 && k <= K) ? Mth<R>::ex2((R)(dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
+  }
+  if (threadIdx.x == 0) Bmax[c] = bm;
+}
 
 // cut slots of a pass [w0, w1) for a sequence of length L: t_j = w0 + j d for j <= J =
 // (tend - 1 - w0) / d, t_{J+1} = tend = min(w1, L)
@@ -93,22 +122,29 @@ __device__ __forceinline__ double block_max_d(double v, double* red) {
 
 // grid (cut slot j, label group, b), 256 threads
 template <typename R>
-__global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
+__global__ void __launch_bounds__(256, 3) cut_kernel(CutArgs<R> a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[8];
   const int j = blockIdx.x, cg = blockIdx.y, b = blockIdx.z;
   const int C = a.C, T = a.T, K = a.K;
   const int L = (int)a.lengths[b];
-  if (L < a.w0) return;
-  const int tend = min(a.w1, L);
-  if (j >= cut_count(a.w0, tend, a.d)) return;
-  const int t = cut_pos(j, a.w0, tend, a.d);
+  int t;
+  if (a.tcut) {
+    if (j > 0) return;
+    t = a.tcut[b];
+  } else {
+    if (L < a.w0) return;
+    const int tend = min(a.w1, L);
+    if (j >= cut_count(a.w0, tend, a.d)) return;
+    t = cut_pos(j, a.w0, tend, a.d);
+  }
   const int c0 = cg * kCutCG;
   const int Cn = min(kCutCG, C - c0);
   const size_t rb0 = (size_t)b * (T + 1);
   const size_t ra0 = (size_t)b * a.rowsA - a.tA0;  // alpha row of t: ra0 + t
   const size_t rbb = (size_t)b * a.rowsB - a.tB0;  // beta row of t: rbb + t
-  const double Z2 = a.logZ[b] * kLog2e;
+  // log2 Z reference of the masses; without logZ (probe mode) the frames of the cut itself
+  const double Z2 = a.logZ ? a.logZ[b] * kLog2e : a.na[ra0 + t] + a.nb[rbb + t];
   const int NA = K + kCutSG, NBv = K + kCutEC, NW = 2 * K + 2 * kCutEC, NWp = cut_wphys(NW);
   R* sa = (R*)sm;                      // [CG][NA]   a[s], s = t-K+1+i
   R* sb = sa + (size_t)kCutCG * NA;    // [CG][NBv]  b[e], e = t+1+i
@@ -133,67 +169,64 @@ __global__ void __launch_bounds__(256) cut_kernel(CutArgs<R> a) {
     if (t > 0 && t < L && K >= 2) {
       // log2 source / target values (fp64), their maxima as references
       double ra_max = -CUDART_INF, rb_max = -CUDART_INF, bm = -CUDART_INF;
+      const double* rA = a.RA ? a.RA + ((size_t)b * C + c) * a.NR - a.t_lo : nullptr;  // index: position
+      const double* rB = a.RB ? a.RB + ((size_t)b * C + c) * a.NR - a.t_lo : nullptr;
+      auto src = [&](int s) -> double {  // ra[s] (-inf: no source)
+        if (s < 0) return -CUDART_INF;
+        if (rA) return rA[s];
+        const R xa = a.Xa[(ra0 + s) * C + c];
+        if (!(xa > Mth<R>::ninf())) return -CUDART_INF;
+        return a.na[ra0 + s] + (double)xa - a.S[(rb0 + s) * C + c] * kLog2e +
+               ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
+      };
+      auto tgt = [&](int e) -> double {  // rb[e] (-inf: no target)
+        if (e > L) return -CUDART_INF;
+        if (rB) return rB[e];
+        const R xb = a.Xb[(rbb + e) * C + c];
+        if (!(xb > Mth<R>::ninf())) return -CUDART_INF;
+        return a.nb[rbb + e] + (double)xb + a.S[(rb0 + e) * C + c] * kLog2e +
+               (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
+      };
       for (int i = threadIdx.x; i < K - 1; i += blockDim.x) {
-        const int s = s_lo + i;
-        if (s >= 0) {
-          const size_t o = (rb0 + s) * C + c;
-          const R xa = a.Xa[(ra0 + s) * C + c];
-          if (xa > Mth<R>::ninf()) {
-            const double ra = a.na[ra0 + s] + (double)xa - a.S[o] * kLog2e +
-                              ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
-            ra_max = fmax(ra_max, ra);
-          }
-        }
-        const int e = t + 1 + i;
-        if (e <= L) {
-          const size_t o = (rb0 + e) * C + c;
-          const R xb = a.Xb[(rbb + e) * C + c];
-          if (xb > Mth<R>::ninf()) {
-            const double rv = a.nb[rbb + e] + (double)xb + a.S[o] * kLog2e +
-                              (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
-            rb_max = fmax(rb_max, rv);
-          }
-        }
+        ra_max = fmax(ra_max, src(s_lo + i));
+        rb_max = fmax(rb_max, tgt(t + 1 + i));
       }
-      for (int k = threadIdx.x; k < K; k += blockDim.x) bm = fmax(bm, a.dur[(size_t)k * C + c] * kLog2e);
+      if (a.Bmax) {
+        bm = a.Bmax[c];
+      } else {
+        for (int k = threadIdx.x; k < K; k += blockDim.x) bm = fmax(bm, a.dur[(size_t)k * C + c] * kLog2e);
+      }
       ra_max = block_max_d(ra_max, red);
       rb_max = block_max_d(rb_max, red);
-      bm = block_max_d(bm, red);
+      if (!a.Bmax) bm = block_max_d(bm, red);
       R* A = sa + (size_t)cl * NA;
       R* Bv = sb + (size_t)cl * NBv;
       R* W = sw + (size_t)cl * NWp;
       const bool live = ra_max > -CUDART_INF && rb_max > -CUDART_INF && bm > -CUDART_INF;
       for (int i = threadIdx.x; i < NA; i += blockDim.x) {
-        const int s = s_lo + i;
         R v = 0;
-        if (live && i < K - 1 && s >= 0) {
-          const size_t o = (rb0 + s) * C + c;
-          const R xa = a.Xa[(ra0 + s) * C + c];
-          if (xa > Mth<R>::ninf()) {
-            const double ra = a.na[ra0 + s] + (double)xa - a.S[o] * kLog2e +
-                              ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0);
-            v = Mth<R>::ex2((R)(ra - ra_max));
-          }
+        if (live && i < K - 1) {
+          const double ra = src(s_lo + i);
+          if (ra > -CUDART_INF) v = Mth<R>::ex2((R)(ra - ra_max));
         }
         A[i] = v;
       }
       for (int i = threadIdx.x; i < NBv; i += blockDim.x) {
-        const int e = t + 1 + i;
         R v = 0;
-        if (live && i < K - 1 && e <= L) {
-          const size_t o = (rb0 + e) * C + c;
-          const R xb = a.Xb[(rbb + e) * C + c];
-          if (xb > Mth<R>::ninf()) {
-            const double rv = a.nb[rbb + e] + (double)xb + a.S[o] * kLog2e +
-                              (a.pe ? a.pe[((size_t)b * T + e - 1) * C + c] * kLog2e : 0.0) - Z2;
-            v = Mth<R>::ex2((R)(rv - rb_max));
-          }
+        if (live && i < K - 1) {
+          const double rv = tgt(t + 1 + i);
+          if (rv > -CUDART_INF) v = Mth<R>::ex2((R)(rv - rb_max));
         }
         Bv[i] = v;
       }
-      for (int i = threadIdx.x; i < NW; i += blockDim.x) {
-        const int k = i - kCutEC;
-        W[cut_wphys(i)] = (live && k >= 1 && k <= K) ? Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
+      if (a.Wt) {
+        const R* wg = a.Wt + (size_t)c * NW;
+        for (int i = threadIdx.x; i < NW; i += blockDim.x) W[cut_wphys(i)] = live ? wg[i] : (R)0;
+      } else {
+        for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+          const int k = i - kCutEC;
+          W[cut_wphys(i)] = (live && k >= 1 && k <= K) ? Mth<R>::ex2((R)(a.dur[(size_t)(k - 1) * C + c] * kLog2e - bm)) : (R)0;
+        }
       }
       __syncthreads();
       // sum_{s,e} a_s b_e w_{e-s}: item = (source group of kCutSG, target chunk of kCutEC).
@@ -345,6 +378,37 @@ __global__ void cut_prefix_kernel(const int64_t* lengths, int B, int C, int nch,
     }
   }
   if (carry) carry[(size_t)b * C + c] = run;
+}
+
+}  // namespace scrf
+
+namespace scrf {
+
+// Provisional log-partition of each sequence from one cut (the overlapped posterior passes run
+// before either sweep has finished, so the final log Z is not known yet). With the frame
+// reference Z_f = n_alpha[t] + n_beta[t] (log2) the cut total is U_t(Z_f) = 2^(Z - Z_f) exactly,
+// so Z~ = Z_f + log2 U_t(Z_f) is log Z up to the frame drift the cut normalisers measure and
+// remove anyway: every mass of a pass is divided by U interpolated between its cuts, which
+// makes the pass outputs independent of the Z reference up to rounding.
+//   probe position: the cut point nearest the middle of the sequence (both sweeps reach it first)
+__host__ __device__ inline int probe_pos(int L, int d) { return d * ((L / 2) / d); }
+
+__global__ void probe_pos_kernel(const int64_t* lengths, int B, int d, int* tcut) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) tcut[b] = probe_pos((int)lengths[b], d);
+}
+
+template <typename R>
+__global__ void probe_finish_kernel(const int64_t* lengths, int B, int C, const int* tcut, const double* na,
+                                    const double* nb, int rowsA, int tA0, int rowsB, int tB0, const double* U,
+                                    double* Zt) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int t = tcut[b];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s += U[(size_t)b * C + c];
+  const double zf = na[(size_t)b * rowsA + t - tA0] + nb[(size_t)b * rowsB + t - tB0];
+  Zt[b] = s > 0.0 ? (zf + log2(s)) * kLn2 : -CUDART_INF;
 }
 
 }  // namespace scrf

@@ -46,6 +46,16 @@ struct PostArgs {
   int SCB, nchB;      // grad_B: sources per CTA, CTAs per sequence (sources in [w0, w1))
   int CGB;            // labels per grad_B CTA
   double* gBp;        // [B][nchB][K][C]
+  // partial-array placement: cntp / gTp chunk ch of sequence b at b*pnch + pq0 + ch, gBp
+  // micro-chunk m at b*pnchB + pm0 + m (a window of a sequence-wide partial array; the final
+  // sums then run over the whole sequence in one fixed order whatever the windowing)
+  int pq0, pnch, pm0, pnchB;
+  // log2 source / target values of the pass (post_prep_kernel), transposed per label:
+  //   RA[b][c][s - t_lo] = na[s] + Xa[s,c] - S[s,c] + Ps[s,c]          (s in [w0 - K + 1, w1 - 1])
+  //   RB[b][c][u - t_lo] = nb[u] + Xb[u,c] + S[u,c] + Pe[u-1,c] - Z    (u in [w0 + 1, w1 + K - 1])
+  // (log2 units, -inf outside those ranges, past L or where the message is -inf)
+  double *RA, *RB;
+  int t_lo, NR;
   float gb_range;     // exp-space grad_B: detrended range above which a block takes the exact path
 };
 
@@ -62,6 +72,57 @@ __host__ __device__ inline int post_chunk(int C) {
 
 // pass 1: per (b, chunk) of CH positions: masses, grad_S / grad_P, local coverage scan,
 // boundary posterior, chunk totals, count and grad_T partials.
+// Transposed log2 source / target rows of a pass (PostArgs::RA / RB), shared by the cut and
+// grad_B kernels: each value is computed once, read row-major (coalesced over labels) and
+// written label-major (coalesced over positions) through a shared-memory tile. Grid
+// (ceil(NR / 32), B), 256 threads, smem 2 * C * 33 doubles.
+constexpr int kPrepRows = 32;
+template <typename R>
+__global__ void __launch_bounds__(256) post_prep_kernel(PostArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* tA = (double*)sm;                       // [C][kPrepRows + 1]
+  double* tB = tA + (size_t)a.C * (kPrepRows + 1);
+  const int b = blockIdx.y, C = a.C, T = a.T, K = a.K;
+  const int r0 = blockIdx.x * kPrepRows;
+  const int L = (int)a.lengths[b];
+  const double Z2 = a.logZ[b] * kLog2e;
+  const int aLo = a.w0 - K + 1, aHi = a.w1 - 1;  // source range
+  const int bLo = a.w0 + 1, bHi = a.w1 + K - 1;  // target range
+  const size_t rs0 = (size_t)b * (T + 1);
+  for (int i = threadIdx.x; i < kPrepRows * C; i += blockDim.x) {
+    const int r = i / C, c = i % C;
+    const int t = a.t_lo + r0 + r;
+    double va = -CUDART_INF, vb = -CUDART_INF;
+    if (r0 + r < a.NR && t >= 0 && t <= L) {
+      const double sv = a.S[(rs0 + t) * C + c] * kLog2e;
+      if (t >= aLo && t <= aHi) {
+        const size_t oa = rowA(a, b, t);
+        const R xa = a.Xa[oa * C + c];
+        if (xa > Mth<R>::ninf())
+          va = a.na[oa] + (double)xa - sv + ((a.ps && t < T) ? a.ps[((size_t)b * T + t) * C + c] * kLog2e : 0.0);
+      }
+      if (t >= bLo && t <= bHi && t >= 1) {
+        const size_t ob = rowB(a, b, t);
+        const R xb = a.Xb[ob * C + c];
+        if (xb > Mth<R>::ninf())
+          vb = a.nb[ob] + (double)xb + sv + (a.pe ? a.pe[((size_t)b * T + t - 1) * C + c] * kLog2e : 0.0) - Z2;
+      }
+    }
+    tA[(size_t)c * (kPrepRows + 1) + r] = va;
+    tB[(size_t)c * (kPrepRows + 1) + r] = vb;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPrepRows * C; i += blockDim.x) {
+    const int c = i / kPrepRows, r = i % kPrepRows;
+    if (r0 + r < a.NR) {
+      const size_t o = ((size_t)b * C + c) * a.NR + r0 + r;
+      a.RA[o] = tA[(size_t)c * (kPrepRows + 1) + r];
+      a.RB[o] = tB[(size_t)c * (kPrepRows + 1) + r];
+    }
+  }
+}
+__host__ __device__ inline size_t post_prep_smem(int C) { return (size_t)2 * C * (kPrepRows + 1) * sizeof(double); }
+
 template <typename R>
 __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -137,7 +198,7 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) a.cntp[(size_t)b * a.nch + ch] = red[0];
+  if (threadIdx.x == 0) a.cntp[(size_t)b * a.pnch + a.pq0 + ch] = red[0];
   // grad_T partial: sum over t < L of 2^(f_t + Ya[t,c'] + T2[c',c] + Yb[t,c])
   for (int pidx = threadIdx.x; pidx < C * C; pidx += blockDim.x) {
     const int cp = pidx / C, c = pidx % C;
@@ -149,7 +210,7 @@ __global__ void __launch_bounds__(256) post_pos_kernel(PostArgs<R> a) {
       acc1 += Mth<R>::ex2((R)sf[i + 1] + sYa[(size_t)(i + 1) * C + cp] + t2 + sYb[(size_t)(i + 1) * C + c]);
     }
     if (i < nt) acc0 += Mth<R>::ex2((R)sf[i] + sYa[(size_t)i * C + cp] + t2 + sYb[(size_t)i * C + c]);
-    a.gTp[((size_t)b * a.nch + ch) * C * C + pidx] = (double)(acc0 + acc1);
+    a.gTp[((size_t)b * a.pnch + a.pq0 + ch) * C * C + pidx] = (double)(acc0 + acc1);
   }
 }
 
@@ -241,8 +302,6 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
   R2* sa = (R2*)sm;                      // [CG][kGBSub]
   R2* sbv = sa + (size_t)CG * kGBSub;    // [CG][rowU] (skewed)
   R* B2 = (R*)(sbv + (size_t)CG * rowU); // [CG][K]
-  const double Z2 = a.logZ[b] * kLog2e;
-  const size_t rb0 = (size_t)b * (T + 1);
   for (int i = threadIdx.x; i < Cn * K; i += blockDim.x) {
     const int cl = i / K, k = i % K;
     B2[i] = (R)(a.dur[(size_t)k * C + c0 + cl] * kLog2e);
@@ -277,10 +336,7 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       v.x = Mth<R>::ninf();
       v.y = 0;
       if (si < ns) {
-        const size_t o = (rb0 + s) * C + c;
-        const size_t oa = rowA(a, b, s);
-        const double ra = a.na[oa] + (double)a.Xa[oa * C + c] - a.S[o] * kLog2e +
-                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0) +
+        const double ra = a.RA[((size_t)b * C + c) * a.NR + (s - a.t_lo)] +
                           (a.corr ? a.corr[(size_t)b * W + s - a.w0] : 0.0);
         split2(ra, v.x, v.y);
       }
@@ -291,13 +347,8 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       R2 v;
       v.x = Mth<R>::ninf();
       v.y = 0;
-      if (u <= L && u < a.w1 + K && ui < kGBSub + K) {  // (beta rows of a window end at w1 + K - 1)
-        const size_t o = (rb0 + u) * C + c;
-        const size_t ob = rowB(a, b, u);
-        const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +
-                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
-        split2(rv, v.x, v.y);
-      }
+      if (u <= L && u < a.w1 + K && ui < kGBSub + K)  // (beta rows of a window end at w1 + K - 1)
+        split2(a.RB[((size_t)b * C + c) * a.NR + (u - a.t_lo)], v.x, v.y);
       sbv[(size_t)cl * rowU + gb_skew(ui)] = v;
     }
     __syncthreads();
@@ -340,7 +391,7 @@ __global__ void __launch_bounds__(512) post_gradB_kernel(PostArgs<R> a) {
       const int cl = idx / nkb, k0 = (idx % nkb) * kGBJ;
 #pragma unroll
       for (int j = 0; j < kGBJ; ++j)
-        if (k0 + j < K) a.gBp[(((size_t)b * a.nchB + slot_m) * K + k0 + j) * C + c0 + cl] = acc[w][j];
+        if (k0 + j < K) a.gBp[(((size_t)b * a.pnchB + a.pm0 + slot_m) * K + k0 + j) * C + c0 + cl] = acc[w][j];
     }
   }
   }  // micro-chunks
@@ -372,7 +423,10 @@ __host__ __device__ inline size_t post_gradB_blk_smem(int K, int CG) {
          (size_t)CG * gbb_npass(K) * kGBPass * sizeof(float) + (size_t)16 * kGBBWarp * sizeof(float) + 64;
 }
 
-__global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) {
+#ifndef SCRF_GBB_MINB
+#define SCRF_GBB_MINB 2
+#endif
+__global__ void __launch_bounds__(512, SCRF_GBB_MINB) post_gradB_blk_kernel(PostArgs<float> a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int b = blockIdx.z, cg = blockIdx.y, sb = blockIdx.x;
   const int C = a.C, T = a.T, K = a.K, CG = a.CGB;
@@ -392,8 +446,6 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
   float* ds = xs + 32;                        // [32]
   float* yw = ds + 32;                        // [kGBNV] (16-byte aligned)
   float* es = yw + kGBNV;                     // [kGBNV]
-  const double Z2 = a.logZ[b] * kLog2e;
-  const size_t rb0 = (size_t)b * (T + 1);
   const int W = a.w1 - a.w0;
   for (int i = threadIdx.x; i < Cn * KP; i += blockDim.x) {
     const int cl = i / KP, k = i % KP;
@@ -423,10 +475,7 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
       const int cl = i / kGBSub, si = i % kGBSub, s = s0 + si, c = c0 + cl;
       float2 v = make_float2(-CUDART_INF_F, 0.f);
       if (si < ns) {
-        const size_t o = (rb0 + s) * C + c;
-        const size_t oa = rowA(a, b, s);
-        const double ra = a.na[oa] + (double)a.Xa[oa * C + c] - a.S[o] * kLog2e +
-                          ((a.ps && s < T) ? a.ps[((size_t)b * T + s) * C + c] * kLog2e : 0.0) +
+        const double ra = a.RA[((size_t)b * C + c) * a.NR + (s - a.t_lo)] +
                           (a.corr ? a.corr[(size_t)b * W + s - a.w0] : 0.0);
         split2(ra, v.x, v.y);
       }
@@ -435,17 +484,15 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
     for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
       const int cl = i / nU, ui = i % nU, u = s0 + 1 + ui, c = c0 + cl;
       float2 v = make_float2(-CUDART_INF_F, 0.f);
-      if (u <= L && u < a.w1 + K && ui < kGBSub + K) {  // (beta rows of a window end at w1 + K - 1)
-        const size_t o = (rb0 + u) * C + c;
-        const size_t ob = rowB(a, b, u);
-        const double rv = a.nb[ob] + (double)a.Xb[ob * C + c] + a.S[o] * kLog2e +
-                          (a.pe ? a.pe[((size_t)b * T + u - 1) * C + c] * kLog2e : 0.0) - Z2;
-        split2(rv, v.x, v.y);
-      }
+      if (u <= L && u < a.w1 + K && ui < kGBSub + K)  // (beta rows of a window end at w1 + K - 1)
+        split2(a.RB[((size_t)b * C + c) * a.NR + (u - a.t_lo)], v.x, v.y);
       sbv[(size_t)cl * rowU + gb_skew(ui)] = v;
     }
     __syncthreads();
-    for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
+#pragma unroll
+    for (int slot = 0; slot < 2; ++slot) {  // static slot index: acc stays in registers
+      const int it = warp + 16 * slot;
+      if (it >= nitems) break;
       const int cl = it / npass, pass = it % npass;
       const int kb = pass * kGBPass + 1;  // durations kb .. kb + kGBPass - 1 (lane owns kb + kGBD lane + j)
       const float2* A = sa + (size_t)cl * kGBSub;
@@ -555,7 +602,7 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
             // the 2^-120 of the lift is applied in fp64 (the fp32 product could flush)
             const float E = (gd + ge) - lam * (float)(kGBD * lane + j) + bk[j];
             if (out[j] > 0.f && E != -CUDART_INF_F)
-              acc[slot & 1][j] += (double)out[j] * (double)Mth<float>::ex2(E) * 0x1p-120;
+              acc[slot][j] += (double)out[j] * (double)Mth<float>::ex2(E) * 0x1p-120;
           }
         } else {
 #pragma unroll 4
@@ -569,18 +616,21 @@ __global__ void __launch_bounds__(512) post_gradB_blk_kernel(PostArgs<float> a) 
             }
           }
 #pragma unroll
-          for (int j = 0; j < kGBD; ++j) acc[slot & 1][j] += (double)out[j];
+          for (int j = 0; j < kGBD; ++j) acc[slot][j] += (double)out[j];
         }
         __syncwarp();
       }
     }
   }
-  for (int it = warp, slot = 0; it < nitems; it += 16, ++slot) {
+#pragma unroll
+  for (int slot = 0; slot < 2; ++slot) {
+    const int it = warp + 16 * slot;
+    if (it >= nitems) break;
     const int cl = it / npass, pass = it % npass;
 #pragma unroll
     for (int j = 0; j < kGBD; ++j) {
       const int k = pass * kGBPass + kGBD * lane + j;  // duration k + 1
-      if (k < K) a.gBp[(((size_t)b * a.nchB + slot_m) * K + k) * C + c0 + cl] = acc[slot & 1][j];
+      if (k < K) a.gBp[(((size_t)b * a.pnchB + a.pm0 + slot_m) * K + k) * C + c0 + cl] = acc[slot][j];
     }
   }
   }  // micro-chunks

@@ -179,7 +179,23 @@ struct SweepArgs {
   long long* trace;  // debug: [256][16] clock64 stamps of cluster 0 (chain lane 0: 0..7, near thread 0: 8..15)
   int trace_from;    // first traced position
   int* hang;         // debug: watchdog record {block, thread, site, index} (first writer wins), or null
+  // full mode: per-cluster progress of the stored rows, [B*2 + dir][kProgSlots] (or null). Slot w
+  // of writer warp w holds q + 1 once every row the warp writes for local positions <= q is
+  // globally visible (L + 1 when it is done); the overlapped posterior passes wait on the
+  // minimum over the writers (prog_wait_kernel, scrf_capi.cu).
+  int* prog;
 };
+
+constexpr int kProgSlots = 8;
+
+// publish "rows of local positions < v written by this warp are visible" (whole warp calls)
+__device__ __forceinline__ void prog_publish(int* slot, int v) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    *(volatile int*)slot = v;
+  }
+}
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -1199,6 +1215,11 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
   const R* b2c = h.B2 + (size_t)cs * b2_stride(g.kc);
   if (do_edge) edge_init(x, g, h.oq, T, C, L, cs, es);
   const int Lq = L & ~3;  // last position written by an edge batch
+  // progress slot: source warp w is writer 1 + w beside the output warp, or writer w
+  int* pslot = (a.prog && !x.task)
+                   ? a.prog + (size_t)(x.b * 2 + x.dir) * kProgSlots + (c >> 5) + (do_edge ? 0 : 1)
+                   : nullptr;
+  if (pslot && !do_edge) prog_publish(pslot, Lq + 1);  // only the positions after Lq are this warp's
   for (int q = 0; q <= L; ++q) {
 #ifdef SCRF_TRACE
     // source-warp phases (cluster 0, lane 0): [0] loop top, [1] after A(q), [2] ring written, [3] sends issued
@@ -1240,6 +1261,7 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
     if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
     if (!do_edge && q > Lq)  // outputs of the positions after the last edge batch
       put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q, h.pubA[sl]);
+    if (pslot && do_edge && (q & 255) == 255) prog_publish(pslot, q + 1);
 
     if (x.dir == 1 && q == L && c == 0 && !x.task) {
       const R* pX = h.pubX + sl * C;
@@ -1251,6 +1273,7 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
       a.logZb[x.b] = (mx == Mth<R>::ninf()) ? -CUDART_INF : (n_q + (double)mx + (double)Mth<R>::lg2(ssum)) * kLn2;
     }
   }
+  if (pslot) prog_publish(pslot, L + 1);
 }
 
 // ======================= edge warps (lane = label), NAS == 2 =======================
@@ -1280,10 +1303,13 @@ __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<
   const int C = a.C, L = x.L;
   const int c = threadIdx.x - wbase * 32;
   const bool act = c < C;
+  int* pslot = (a.prog && !x.task) ? a.prog + (size_t)(x.b * 2 + x.dir) * kProgSlots : nullptr;
   for (int q = 0; q <= L; q += 4) {
     nbar_sync(BAR_A + 0, NA + NAE);
     edge_outputs<R>(a, x, h, q, c, act);
+    if (pslot && (q & 255) == 252) prog_publish(pslot, q + 1);
   }
+  if (pslot) prog_publish(pslot, L + 1);
 }
 
 template <typename R, bool TAILS, bool CW1, int MODE>

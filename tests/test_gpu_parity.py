@@ -277,6 +277,39 @@ def test_full_config_fp32_matches_fp64(cfg):
         assert np.all(np.isfinite(out["logZ"])) and np.all(out["dead_at"] < 0)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_overlapped_windows_match_sequential_and_single_pass(monkeypatch, precision):
+    """Full-mode posterior passes run in 8192-position windows concurrently with the sweeps
+    (SCRF_OVERLAP=1, waiting on the sweeps' published row progress) give exactly the result of
+    the same windows run after the sweeps (0), and agree with one pass after the sweeps (-1, the
+    true log Z as mass reference instead of the cut-normalised provisional one) to rounding.
+    Ragged lengths and projections, so windows are ready at different times per sequence."""
+    _, params, cum = scrf.equivalence_instance(3, T=40000, K=300, C=12, B=3, mode=CenteringMode.MEAN, ragged=True,
+                                               projections=True)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    outs = {}
+    for mode in ("1", "0", "-1"):
+        monkeypatch.setenv("SCRF_OVERLAP", mode)
+        outs[mode] = _device_outputs(prob, precision)
+    for k in outs["1"]:
+        np.testing.assert_array_equal(outs["1"][k], outs["0"][k], err_msg=k)
+    tol = 1e-6 if precision == "fp32" else 1e-10
+    for k in ("grad_S", "grad_T", "grad_B", "position_marginals", "boundary_posterior", "expected_segment_count"):
+        assert parity.scaled_err(outs["1"][k], outs["-1"][k]) <= tol, k
+    np.testing.assert_array_equal(outs["1"]["logZ"], outs["-1"]["logZ"])
+    # the separate full-memory backward (beta sweep only, alpha rows complete) windows the same way
+    S.set_precision(precision)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SCRF_OVERLAP", mode)
+        fwd = S.device_forward(prob, sparse=False)
+        bw = S.device_backward(prob, fwd)
+        outs["b" + mode] = {k: getattr(bw, k).cpu().numpy() for k in ("grad_S", "grad_T", "grad_B")}
+    S.set_precision("fp32")
+    for k in ("grad_S", "grad_T", "grad_B"):
+        np.testing.assert_array_equal(outs["b1"][k], outs["b0"][k], err_msg=k)
+        assert parity.scaled_err(outs["b1"][k], outs["1"][k]) <= tol, k
+
+
 def test_alpha_beta_logz_agree_on_goldens():
     S.set_precision("fp32")
     for name in ["c1rp", "c2", "c3s", "c4s", "c5s"]:

@@ -89,14 +89,8 @@ def test_streaming_backward_replays_from_checkpoints(precision):
     parity.compare_posterior(logZ, grads, marg, exp, precision)
 
 
-def test_checkpoint_rows_are_sublinear():
-    """c4 (B=8, T=1e5, K=1000, C=24): the sparse checkpoint + backward work buffers are a small
-    fraction of the full-memory ones (O(sqrt(T K) C) vs O(T C))."""
-    from paper_2604_18780_b200.instances import CONFIGS
-
-    c = CONFIGS["c4"]
+def _mode_bytes(B, T, K, C):
     dev = torch.device("cuda", 0)
-    B, T, K, C = c["B"], c["T"], c["K"], c["C"]
     prob = scrf.DeviceProblem(torch.zeros((B, T + 1, C), dtype=torch.float64, device=dev),
                               torch.full((B,), T, dtype=torch.int64, device=dev),
                               torch.zeros((C, C), dtype=torch.float64, device=dev),
@@ -112,9 +106,24 @@ def test_checkpoint_rows_are_sublinear():
         sizes[name] = n.value
     full = sizes["scrf_checkpoint_bytes"] + sizes["scrf_backward_work_bytes"]
     sparse = sizes["scrf_sparse_checkpoint_bytes"] + sizes["scrf_sparse_backward_work_bytes"]
-    print(sizes, full / sparse)
+    return sizes, full, sparse
+
+
+def test_checkpoint_rows_are_sublinear():
+    """c4 (B=8, T=1e5, K=1000, C=24): the sparse checkpoint rows are a small fraction of the
+    full-memory message store, and the sparse working set grows like sqrt(T) (O(sqrt(T K) C):
+    checkpoint rows, one replay window and its pass buffers) while the full one grows like T."""
+    from paper_2604_18780_b200.instances import CONFIGS
+
+    c = CONFIGS["c4"]
+    B, T, K, C = c["B"], c["T"], c["K"], c["C"]
+    sizes, full, sparse = _mode_bytes(B, T, K, C)
+    _, full4, sparse4 = _mode_bytes(B, 4 * T, K, C)
+    print(sizes, full / sparse, full4 / full, sparse4 / sparse)
     assert sizes["scrf_sparse_checkpoint_bytes"] < 0.1 * sizes["scrf_checkpoint_bytes"]
-    assert sparse < 0.3 * full
+    assert sparse < 0.35 * full
+    assert full4 / full > 3.5
+    assert sparse4 / sparse < 2.5
 
 
 class TestRecomputeAlpha:
