@@ -209,6 +209,20 @@ void scrf_profile_events(void* start, void* stop);
  * remaining pass runs. */
 void scrf_position_outputs_event(void* event);
 
+/* Full-memory posterior / backward at long T run their posterior passes in windows of
+ * positions, concurrently with the sweeps (SCRF_OVERLAP, SCRF_OVL_WS). Writes the windows
+ * [w0[i], w1[i]) in the order the passes complete them and returns their number (0: one pass
+ * after the sweeps; -n: cap < n). Windows cover boundaries 0..T; a window's per-position
+ * outputs are grad_S rows [w0, w1) and grad_P*, position marginals, boundary posterior rows
+ * [w0, min(w1, T)). */
+int scrf_window_plan(const scrf_problem* p, int32_t* w0, int32_t* w1, int cap);
+
+/* events[i] (cudaEvent_t, or events = NULL to disable) is recorded, on the library's side
+ * stream, as soon as the per-position outputs of window i of every subsequent full-memory
+ * scrf_posterior / scrf_backward call on this thread are final -- for device-to-host copies
+ * of each window while the sweeps still run (the numpy posterior() facade does this). */
+void scrf_window_events(void** events, int n);
+
 /* Debug: if non-NULL, the next sweep writes clock64() phase stamps of cluster 0 for
  * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);

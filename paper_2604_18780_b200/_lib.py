@@ -83,6 +83,8 @@ _SIGS = {
     "scrf_last_launch_count": (_int, []),
     "scrf_profile_events": (None, [_vp, _vp]),
     "scrf_position_outputs_event": (None, [_vp]),
+    "scrf_window_plan": (_int, [_P, _vp, _vp, _int]),
+    "scrf_window_events": (None, [_vp, _int]),
     "scrf_debug_trace": (None, [_vp]),
     "scrf_debug_hang": (_int, [_vp]),
 }

@@ -23,6 +23,9 @@ thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev_start = nullptr;
 thread_local cudaEvent_t g_ev_stop = nullptr;
 thread_local cudaEvent_t g_ev_pos = nullptr;  // recorded once the per-position outputs are final
+// optional events recorded once the per-position outputs of window i (scrf_window_plan order) are final
+thread_local cudaEvent_t* g_win_ev = nullptr;
+thread_local int g_win_nev = 0;
 thread_local long long* g_trace = nullptr;  // debug: clock64 phase stamps of the next sweep
 int* g_hang = nullptr;                        // debug: watchdog record (SCRF_WATCHDOG=1)
 
@@ -607,6 +610,7 @@ struct PassOpt {
   const double* Z = nullptr;  // log Z reference of the masses (null: PostOut::logZ)
   bool seqwide = false;
   int pnch = 0, pnchB = 0;    // sequence-wide chunk / micro-chunk counts
+  cudaEvent_t pos_ev = nullptr;  // recorded once this pass's per-position outputs are final
 };
 
 template <typename R>
@@ -750,6 +754,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ++g_launches;
     post_carry_kernel<<<dim3(q.nch, B), 64, 0, st>>>(p->lengths, B, a.T, C, q.CH, q.nch, w0, w1, a.tot, out.pos);
     if (last && g_ev_pos) cudaEventRecord(g_ev_pos, st);
+    if (opt.pos_ev) cudaEventRecord(opt.pos_ev, st);
   }
   if (sizeof(R) == 4 && gradB_blocked()) {
     if ((long long)q.CGB * gbb_npass(K) > 32) return SCRF_ECONFIG;
@@ -1029,6 +1034,7 @@ int run_full_post_win(const scrf_problem* p, const void* fstate, void* work, con
   opt.pnch = qall.nch;
   opt.pnchB = qall.nchB;
   for (int i = 0; i < nwin; ++i) {
+    opt.pos_ev = i < g_win_nev ? g_win_ev[i] : nullptr;
     if (mode == 1) {
       ++g_launches;
       prog_wait_kernel<<<1, 256, 0, sw>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, win[i].w1 + 1,
@@ -1963,5 +1969,22 @@ void scrf_profile_events(void* start, void* stop) {
 }
 
 void scrf_position_outputs_event(void* event) { g_ev_pos = (cudaEvent_t)event; }
+
+void scrf_window_events(void** events, int n) {
+  g_win_ev = (cudaEvent_t*)events;
+  g_win_nev = events ? n : 0;
+}
+
+int scrf_window_plan(const scrf_problem* p, int32_t* w0, int32_t* w1, int cap) {
+  if (check_problem(p) || ovl_mode(p) < 0) return 0;
+  OvlWin win[4096];
+  const int n = ovl_windows(p, win, 4096);
+  if (n > cap) return -n;
+  for (int i = 0; i < n; ++i) {
+    w0[i] = win[i].w0;
+    w1[i] = win[i].w1;
+  }
+  return n;
+}
 
 }  // extern "C"

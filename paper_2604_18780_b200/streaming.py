@@ -617,6 +617,16 @@ def _to_host(*tensors):
 _SIDE = {}
 
 
+def _window_plan(prob: DeviceProblem) -> list[tuple[int, int]]:
+    """Posterior-pass windows of a full-memory call, in completion order ([] = one pass)."""
+    lib = _lib.load()
+    cap = 4096
+    w0 = (ctypes.c_int32 * cap)()
+    w1 = (ctypes.c_int32 * cap)()
+    n = lib.scrf_window_plan(prob.c_struct(), w0, w1, cap)
+    return [(int(w0[i]), int(w1[i])) for i in range(max(n, 0))]
+
+
 def _side_stream() -> torch.cuda.Stream:
     dev = torch.cuda.current_device()
     if dev not in _SIDE:
@@ -714,22 +724,46 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
             raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
         up_t = torch.as_tensor(up)
     prob = DeviceProblem.from_host(cum, params)
-    # the per-position outputs (the bulk of the device->host bytes) are copied on a side stream
-    # while the duration-gradient pass still runs
+    # The per-position outputs (the bulk of the device->host bytes) are copied on a side stream
+    # while the device still works: window by window as the posterior passes that overlap the
+    # sweeps finish them (full memory at long T, scrf_window_plan), else once they are final
+    # (before the duration-gradient pass).
     lib = _lib.load()
+    mem = choose_memory_mode(prob, delta, memory)
+    plan = _window_plan(prob) if mem == "full" else []
     ready = torch.cuda.Event()
     ready.record()  # torch creates the CUDA event lazily: make the handle real before passing it
+    win_ev = [torch.cuda.Event() for _ in plan]
+    for e in win_ev:
+        e.record()
+    handles = (ctypes.c_void_p * max(1, len(plan)))(*[e.cuda_event for e in win_ev])
     lib.scrf_position_outputs_event(ctypes.c_void_p(ready.cuda_event))
+    if plan:
+        lib.scrf_window_events(handles, len(plan))
     try:
-        fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device),
-                                   memory=choose_memory_mode(prob, delta, memory))
+        fwd, bw = device_posterior(prob, delta, None if up_t is None else up_t.to(prob.S.device), memory=mem)
     finally:
         lib.scrf_position_outputs_event(None)
+        lib.scrf_window_events(None, 0)
     side = _side_stream()
-    side.wait_event(ready)
-    with torch.cuda.stream(side):
-        early = _to_host_async(bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals,
-                               bw.boundary_posterior)
+    dev_outs = (bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals, bw.boundary_posterior)
+    if plan:
+        early = [None if t is None else torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev_outs]
+        with torch.cuda.stream(side):
+            for (w0, w1), ev in zip(plan, win_ev):
+                side.wait_event(ev)
+                for t, h in zip(dev_outs, early):
+                    if t is None:
+                        continue
+                    hi = min(w1, t.shape[1])  # grad_S has T + 1 rows, the others T
+                    if hi <= w0:
+                        continue
+                    for b in range(t.shape[0]):  # contiguous per sequence: one async memcpy each
+                        h[b, w0:hi].copy_(t[b, w0:hi], non_blocking=True)
+    else:
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            early = _to_host_async(*dev_outs)
     _raise_if_dead(fwd)
     _check_clamp(prob, fwd, bw, stats)
     if ledger is not None:

@@ -310,6 +310,25 @@ def test_overlapped_windows_match_sequential_and_single_pass(monkeypatch, precis
         assert parity.scaled_err(outs["b1"][k], outs["1"][k]) <= tol, k
 
 
+def test_numpy_posterior_window_copies_match_device_outputs():
+    """posterior() (numpy in / out) copies the per-position outputs window by window while the
+    sweeps still run (scrf_window_plan / scrf_window_events); the host arrays equal the device
+    outputs of the same call bit for bit."""
+    _, params, cum = scrf.equivalence_instance(5, T=40000, K=200, C=6, B=3, mode=CenteringMode.MEAN, ragged=True,
+                                               projections=True)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    assert len(S._window_plan(prob)) >= 4
+    logZ, grads, marg = scrf.posterior(cum, params, memory="full")
+    fwd, bw = S.device_posterior(prob, memory="full")
+    np.testing.assert_array_equal(logZ, fwd.logZ.cpu().numpy())
+    for name, host, dev in (("grad_S", grads.grad_S, bw.grad_S), ("grad_P_start", grads.grad_P_start, bw.grad_P_start),
+                            ("grad_P_end", grads.grad_P_end, bw.grad_P_end), ("grad_T", grads.grad_T, bw.grad_T),
+                            ("grad_B", grads.grad_B, bw.grad_B),
+                            ("position_marginals", marg.position_marginals, bw.position_marginals),
+                            ("boundary_posterior", marg.boundary_posterior, bw.boundary_posterior)):
+        np.testing.assert_array_equal(host, dev.cpu().numpy(), err_msg=name)
+
+
 def test_alpha_beta_logz_agree_on_goldens():
     S.set_precision("fp32")
     for name in ["c1rp", "c2", "c3s", "c4s", "c5s"]:
