@@ -223,6 +223,21 @@ int scrf_window_plan(const scrf_problem* p, int32_t* w0, int32_t* w1, int cap);
  * of each window while the sweeps still run (the numpy posterior() facade does this). */
 void scrf_window_events(void** events, int n);
 
+/* Streamed input for the next full-memory scrf_posterior / scrf_backward / scrf_forward calls on
+ * this thread (gate = NULL to disable): the sweeps start before S is on the device and read the
+ * rows [j << shift, (j+1) << shift) of every sequence only once gate[j] != 0. gate is a device
+ * int32 array of ngate + 1 entries, zeroed by the caller before the call; the caller copies the
+ * row chunks on another stream and marks each with scrf_gate_set on that stream after its copy
+ * (chunk order: the alpha sweep consumes chunks from 0 up, the beta sweep from ngate-1 down).
+ * gate[ngate] becomes 1 if a sweep waited more than 2 s for a chunk (the sweeps then stop waiting
+ * and read whatever is there: a caller bug). Ps / Pe must be on the device before the call. Returns SCRF_EDIM for a
+ * bad ngate / shift. */
+int scrf_input_gate(const int32_t* gate, int ngate, int shift);
+
+/* Launch, on `stream`, a one-thread kernel that release-stores gate[j] = 1 (after the chunk
+ * copies queued before it on that stream). */
+int scrf_gate_set(int32_t* gate, int j, void* stream);
+
 /* Debug: if non-NULL, the next sweep writes clock64() phase stamps of cluster 0 for
  * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);

@@ -85,6 +85,8 @@ _SIGS = {
     "scrf_position_outputs_event": (None, [_vp]),
     "scrf_window_plan": (_int, [_P, _vp, _vp, _int]),
     "scrf_window_events": (None, [_vp, _int]),
+    "scrf_input_gate": (_int, [_vp, _int, _int]),
+    "scrf_gate_set": (_int, [_vp, _int, _vp]),
     "scrf_debug_trace": (None, [_vp]),
     "scrf_debug_hang": (_int, [_vp]),
 }

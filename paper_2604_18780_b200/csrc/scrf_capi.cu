@@ -26,6 +26,9 @@ thread_local cudaEvent_t g_ev_pos = nullptr;  // recorded once the per-position 
 // optional events recorded once the per-position outputs of window i (scrf_window_plan order) are final
 thread_local cudaEvent_t* g_win_ev = nullptr;
 thread_local int g_win_nev = 0;
+// streamed input gate of the next full-mode sweeps (scrf_input_gate)
+thread_local const int* g_gate = nullptr;
+thread_local int g_gate_n = 0, g_gate_shift = 12;
 thread_local long long* g_trace = nullptr;  // debug: clock64 phase stamps of the next sweep
 int* g_hang = nullptr;                        // debug: watchdog record (SCRF_WATCHDOG=1)
 
@@ -544,6 +547,11 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
   }
   a.tasks = io.tasks;
   a.prog = io.prog;
+  if (!io.tasks && io.store == 0 && g_gate) {
+    a.gate = g_gate;
+    a.gate_shift = g_gate_shift;
+    a.ngate = g_gate_n;
+  }
   a.trace = g_trace;
   a.trace_from = env_int("SCRF_TRACE_FROM", 64);
   if (env_int("SCRF_WATCHDOG", 0)) {
@@ -850,11 +858,6 @@ int run_full_post(const scrf_problem* p, const void* fstate, void* work, const P
 // depend on the window size or on whether the windows ran concurrently (SCRF_OVERLAP=0 runs the
 // same windows after the sweeps, for the bit-identity test).
 
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // one CTA: returns once every swept direction of every sequence has published its rows through
 // alpha t <= tA / beta t >= tB (probe: the probe cut of each sequence). Gives up after 20 s
@@ -872,7 +875,7 @@ __global__ void prog_wait_kernel(const int* prog, const int64_t* lengths, int B,
     const long long t0 = gtimer();
     for (;;) {
       int mn = 0x7fffffff;
-      for (int w = 0; w < nw; ++w) mn = min(mn, ld_acquire_gpu(sl + w));
+      for (int w = 0; w < nw; ++w) mn = min(mn, ld_acquire_i32(sl + w));
       if (mn >= need) break;
       if (gtimer() - t0 > 20000000000LL) {
         atomicExch(status, 1);
@@ -931,8 +934,49 @@ SideStream& side_stream() {
   return x;
 }
 
+__global__ void gate_set_kernel(int* gate, int j) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(gate + j), "r"(1) : "memory");
+}
+
+// Under lazy module loading (torch's default) the first launch of a kernel loads it, and the
+// load waits for the kernels running on the device: a kernel that a running sweep waits on
+// (gate_set_kernel) would deadlock, and the overlapped passes would serialise behind the sweep.
+// Load every kernel those paths launch up front.
+template <typename R>
+void preload_post_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, probe_finish_kernel<R>);
+  cudaFuncGetAttributes(&fa, cut_kernel<R>);
+  cudaFuncGetAttributes(&fa, cut_w_kernel<R>);
+  cudaFuncGetAttributes(&fa, cut_corr_kernel<R>);
+  cudaFuncGetAttributes(&fa, post_prep_kernel<R>);
+  cudaFuncGetAttributes(&fa, post_pos_kernel<R>);
+  cudaFuncGetAttributes(&fa, post_gradB_kernel<R>);
+  cudaFuncGetAttributes(&fa, book_kernel<R>);
+}
+void preload_concurrent_kernels() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, gate_set_kernel);
+  cudaFuncGetAttributes(&fa, prog_wait_kernel);
+  cudaFuncGetAttributes(&fa, probe_pos_kernel);
+  cudaFuncGetAttributes(&fa, cut_prefix_kernel);
+  cudaFuncGetAttributes(&fa, post_prefix_kernel);
+  cudaFuncGetAttributes(&fa, post_carry_kernel);
+  cudaFuncGetAttributes(&fa, post_gradB_blk_kernel);
+  cudaFuncGetAttributes(&fa, acc_kernel);
+  cudaFuncGetAttributes(&fa, post_reduce2_kernel);
+  cudaFuncGetAttributes(&fa, post_count_kernel);
+  preload_post_kernels<float>();
+  preload_post_kernels<double>();
+}
+
 // before the sweeps: zero the accumulators and the progress slots, fork the side stream
 int ovl_begin(const scrf_problem* p, unsigned char* wb, const PLayout& PL, int mode, cudaStream_t st) {
+  preload_concurrent_kernels();
   int rc = pass_begin(p, wb, PL, st);
   if (rc) return rc;
   cudaError_t e = cudaMemsetAsync(wb + PL.prog, 0, (size_t)p->B * 2 * kProgSlots * 4, st);
@@ -1969,6 +2013,22 @@ void scrf_profile_events(void* start, void* stop) {
 }
 
 void scrf_position_outputs_event(void* event) { g_ev_pos = (cudaEvent_t)event; }
+
+int scrf_input_gate(const int32_t* gate, int ngate, int shift) {
+  if (gate && (ngate < 1 || shift < 0 || shift > 30)) return SCRF_EDIM;
+  if (gate) preload_concurrent_kernels();
+  g_gate = gate;
+  g_gate_n = gate ? ngate : 0;
+  g_gate_shift = shift;
+  return SCRF_OK;
+}
+
+int scrf_gate_set(int32_t* gate, int j, void* stream) {
+  if (!gate) return SCRF_ENULL;
+  if (j < 0) return SCRF_EDIM;
+  gate_set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(gate, j);
+  return (int)cudaGetLastError();
+}
 
 void scrf_window_events(void** events, int n) {
   g_win_ev = (cudaEvent_t*)events;

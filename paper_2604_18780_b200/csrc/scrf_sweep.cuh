@@ -184,9 +184,20 @@ struct SweepArgs {
   // globally visible (L + 1 when it is done); the overlapped posterior passes wait on the
   // minimum over the writers (prog_wait_kernel, scrf_capi.cu).
   int* prog;
+  // streamed input (full mode; or null): S rows [j << gate_shift, (j+1) << gate_shift) of every
+  // sequence are on the device once gate[j] != 0 (set by the caller's copy stream,
+  // scrf_gate_set); gate[ngate] = 1 records a wait that timed out
+  const int* gate;
+  int gate_shift, ngate;
 };
 
 constexpr int kProgSlots = 8;
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // publish "rows of local positions < v written by this warp are visible" (whole warp calls)
 __device__ __forceinline__ void prog_publish(int* slot, int v) {
@@ -575,6 +586,36 @@ __device__ __forceinline__ double2 oq_of(const SweepCtx& x, const SweepGeo& g, i
   const double psv = g.PsRow ? d[g.PsRow * C + c] * kLog2e : 0.0;
   const double pev = g.PeRow ? d[g.PeRow * C + c] * kLog2e : 0.0;
   return x.dir == 0 ? make_double2(s + pev, -s + psv) : make_double2(-s + psv, s + pev);
+}
+
+// Streamed input: wait until the rows of local positions p0 .. p1 (and one row beyond each end:
+// rows are not cache-line aligned, so a line fetched with an edge row may hold bytes of its
+// neighbour) are on the device. The source warps call it every 64 positions for the next 256:
+// every reader of S in the cluster (edge warps, output rows, tails) stays within a few dozen
+// positions of the source warps -- they wait on its barriers / ring sends -- so it gates them all.
+// Gives up after 2 s (records gate[ngate] = 1) rather than hang on a caller bug.
+template <typename R>
+__device__ __noinline__ void gate_span_wait(const SweepArgs<R>& a, const SweepCtx& x, int p0, int p1) {
+  int t0 = x.tpos(p0), t1 = x.tpos(p1);
+  if (t0 > t1) {
+    const int tt = t0;
+    t0 = t1;
+    t1 = tt;
+  }
+  t0 = t0 > 0 ? t0 - 1 : 0;
+  t1 = t1 < a.T ? t1 + 1 : a.T;
+  const int j0 = t0 >> a.gate_shift, j1 = t1 >> a.gate_shift;
+  for (int j = j0; j <= j1; ++j) {
+    const long long s = gtimer();
+    while (ld_acquire_i32(a.gate + j) == 0) {
+      if (ld_acquire_i32(a.gate + a.ngate) != 0) return;
+      if (gtimer() - s > 2000000000LL) {
+        atomicExch((int*)a.gate + a.ngate, 1);
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
 }
 
 // raw rows S[t], Ps[t], Pe[t-1] of label c at sweep position p into its staging slot
@@ -1221,6 +1262,10 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
                    : nullptr;
   if (pslot && !do_edge) prog_publish(pslot, Lq + 1);  // only the positions after Lq are this warp's
   for (int q = 0; q <= L; ++q) {
+    if (a.gate && (q & 63) == 0) {  // streamed input: the next 256 positions' rows
+      if ((threadIdx.x & 31) == 0) gate_span_wait(a, x, q, min(q + 256, L));
+      __syncwarp();
+    }
 #ifdef SCRF_TRACE
     // source-warp phases (cluster 0, lane 0): [0] loop top, [1] after A(q), [2] ring written, [3] sends issued
     long long* trs = (a.trace && blockIdx.x == 0 && c == 0 && q >= a.trace_from && q < a.trace_from + 256)
@@ -1838,6 +1883,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   x.S = a.S + (size_t)x.b * (a.T + 1) * a.C;
   x.ps = a.ps ? a.ps + (size_t)x.b * a.T * a.C : nullptr;
   x.pe = a.pe ? a.pe + (size_t)x.b * a.T * a.C : nullptr;
+  if (MODE == 0 && a.gate) {  // streamed input: the first rows every CTA may read before the loop
+    if (threadIdx.x == 0) gate_span_wait(a, x, 0, min(x.L, 320));
+    __syncthreads();
+  }
   const HeadLayout HL = head_layout<R>(a.K, a.C, g);
   const TailLayout TL = tail_layout<R>(a.K, a.C, g);
 #ifdef SCRF_TRACE

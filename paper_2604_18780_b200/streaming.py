@@ -19,6 +19,7 @@ Two layers:
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
 from dataclasses import dataclass, field
 from math import sqrt
@@ -118,10 +119,12 @@ class DeviceProblem:
         return self.duration_bias.shape[0]
 
     @classmethod
-    def from_host(cls, cum: CumulativeScores, params: SemiCRFParams, device=None, non_blocking=True):
+    def from_host(cls, cum: CumulativeScores, params: SemiCRFParams, device=None, non_blocking=True,
+                  defer_S: bool = False):
         """Copy the host problem to the device. Large arrays are staged through pinned memory
         (torch's caching host allocator keeps each staging block alive until its copy has run),
-        which is ~2.5x faster than a pageable copy."""
+        which is ~2.5x faster than a pageable copy. defer_S: S is allocated but not copied (the
+        caller streams it in behind the sweeps, _stream_S)."""
         dev = device or _dev()
 
         def put(a, dt=torch.float64):
@@ -132,20 +135,15 @@ class DeviceProblem:
                 t = t.to(dt)
             nbytes = t.numel() * t.element_size()
             if non_blocking and nbytes >= (16 << 20):
-                # chunked: the host copy of chunk i into pinned memory overlaps the DMA of chunk i-1
-                flat = t.reshape(-1)
-                pin = torch.empty(flat.shape, dtype=dt, pin_memory=True)
-                out = torch.empty(flat.shape, dtype=dt, device=dev)
-                step = -(-flat.numel() // 8)
-                for i0 in range(0, flat.numel(), step):
-                    pin[i0:i0 + step].copy_(flat[i0:i0 + step])
-                    out[i0:i0 + step].copy_(pin[i0:i0 + step], non_blocking=True)
-                return out.view(t.shape)
+                out = torch.empty(t.shape, dtype=dt, device=dev)
+                _fill_pinned(out, t)
+                return out
             if non_blocking and nbytes >= (1 << 16):
                 return t.pin_memory().to(device=dev, non_blocking=True)
             return t.to(device=dev)
 
-        return cls(put(cum.S), put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
+        S = (torch.empty(np.shape(cum.S), dtype=torch.float64, device=dev) if defer_S else put(cum.S))
+        return cls(S, put(np.asarray(cum.lengths, dtype=np.int64), torch.int64), put(params.transition),
                    put(params.duration_bias), put(cum.proj_start), put(cum.proj_end))
 
     def _signature(self):
@@ -617,6 +615,89 @@ def _to_host(*tensors):
 _SIDE = {}
 
 
+def _fill_pinned(out: torch.Tensor, t: torch.Tensor) -> None:
+    """Host tensor -> existing contiguous device tensor through pinned memory in 8 chunks (the
+    host copy of chunk i into pinned memory overlaps the DMA of chunk i-1)."""
+    flat = t.reshape(-1)
+    dst = out.view(-1)
+    pin = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+    step = -(-flat.numel() // 8)
+    for i0 in range(0, flat.numel(), step):
+        pin[i0:i0 + step].copy_(flat[i0:i0 + step])
+        dst[i0:i0 + step].copy_(pin[i0:i0 + step], non_blocking=True)
+
+
+_GATE_SHIFT = 12  # 4096-row chunks of S
+
+
+def _gate_for(prob: DeviceProblem):
+    n = -(-(prob.T + 1) // (1 << _GATE_SHIFT))
+    return torch.zeros(n + 1, dtype=torch.int32, device=prob.S.device), _GATE_SHIFT
+
+
+_PRIMED = set()
+
+
+def _prime_streaming(dev) -> None:
+    """First use, before any sweep waits on it: load gate_set_kernel (lazy module loading would
+    otherwise load it on its first launch, behind the running sweep that waits for it), create
+    the copy stream and run one pinned copy on it."""
+    if dev in _PRIMED:
+        return
+    lib = _lib.load()
+    g = torch.zeros(2, dtype=torch.int32, device=dev)
+    h = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+    cs = _copy_stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        g.copy_(h, non_blocking=True)
+        _lib.check(lib.scrf_gate_set(_lib.ptr(g), 0, _lib.stream_handle()), "scrf_gate_set")
+    cs.synchronize()
+    _PRIMED.add(dev)
+
+
+def _stream_S(prob: DeviceProblem, S_host, gate: torch.Tensor, shift: int, gate_ready: torch.cuda.Event,
+              pin: torch.Tensor) -> None:
+    """Copy S to prob.S chunk by chunk on the copy stream -- chunks from both ends inward, the
+    order the alpha and beta sweeps consume them -- marking each chunk's gate after its copy.
+    The current stream then waits for the last copy (later consumers of S)."""
+    lib = _lib.load()
+    Sh = np.asarray(S_host)
+    if Sh.dtype != np.float64 or not Sh.flags.c_contiguous:
+        Sh = np.ascontiguousarray(Sh, dtype=np.float64)
+    B, T1, _ = Sh.shape
+    R = 1 << shift
+    n = gate.numel() - 1
+    order = []
+    lo, hi = 0, n - 1
+    while lo <= hi:
+        order.append(lo)
+        if hi != lo:
+            order.append(hi)
+        lo, hi = lo + 1, hi - 1
+    St = torch.from_numpy(Sh)  # no copy; torch's CPU copy into pinned memory is multi-threaded
+    cs = _copy_stream()
+    cs.wait_event(gate_ready)
+    with torch.cuda.stream(cs):
+        for j in order:
+            r0, r1 = j * R, min((j + 1) * R, T1)
+            pin[:, r0:r1].copy_(St[:, r0:r1])
+            for b in range(B):  # contiguous per sequence: one async memcpy each
+                prob.S[b, r0:r1].copy_(pin[b, r0:r1], non_blocking=True)
+            _lib.check(lib.scrf_gate_set(_lib.ptr(gate), j, _lib.stream_handle()), "scrf_gate_set")
+    torch.cuda.current_stream().wait_stream(cs)
+
+
+_COPY = {}
+
+
+def _copy_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    if dev not in _COPY:
+        _COPY[dev] = torch.cuda.Stream()
+    return _COPY[dev]
+
+
 def _window_plan(prob: DeviceProblem) -> list[tuple[int, int]]:
     """Posterior-pass windows of a full-memory call, in completion order ([] = one pass)."""
     lib = _lib.load()
@@ -723,14 +804,34 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         if up.shape != (B,):
             raise ValueError(f"upstream must be shaped ({B},), got {up.shape}")
         up_t = torch.as_tensor(up)
-    prob = DeviceProblem.from_host(cum, params)
-    # The per-position outputs (the bulk of the device->host bytes) are copied on a side stream
-    # while the device still works: window by window as the posterior passes that overlap the
-    # sweeps finish them (full memory at long T, scrf_window_plan), else once they are final
-    # (before the duration-gradient pass).
+    # Full memory at long T: S is streamed in behind the sweeps (they start on its first row
+    # chunks, scrf_input_gate) and the per-position outputs (the bulk of the device->host bytes)
+    # are copied on a side stream window by window as the posterior passes that overlap the
+    # sweeps finish them (scrf_window_plan); otherwise S is copied first and the outputs once they
+    # are final (before the duration-gradient pass).
     lib = _lib.load()
-    mem = choose_memory_mode(prob, delta, memory)
-    plan = _window_plan(prob) if mem == "full" else []
+    shape_only = DeviceProblem.from_host(cum, params, defer_S=True)
+    mem = choose_memory_mode(shape_only, delta, memory)
+    plan = _window_plan(shape_only) if mem == "full" else []
+    streamed = (bool(plan) and np.asarray(cum.S).nbytes >= (32 << 20)
+                and os.environ.get("SCRF_STREAM_INPUT", "1") != "0")
+    if streamed:
+        prob = shape_only
+        _prime_streaming(prob.S.device)
+        gate, shift = _gate_for(prob)
+        _lib.check(lib.scrf_input_gate(_lib.ptr(gate), gate.numel() - 1, shift), "scrf_input_gate")
+        gate_ready = torch.cuda.Event()
+        gate_ready.record()  # the zeroed gate precedes every chunk mark
+        # pinned staging allocated before the launch: nothing that could wait for the device
+        # may run on this thread between the launch and the last chunk mark
+        pin = torch.empty(prob.S.shape, dtype=torch.float64, pin_memory=True)
+    else:
+        prob = shape_only
+        Sh = torch.from_numpy(np.ascontiguousarray(cum.S, dtype=np.float64))
+        if Sh.numel() * 8 >= (16 << 20):
+            _fill_pinned(prob.S, Sh)
+        else:
+            prob.S.copy_(Sh.pin_memory() if Sh.numel() * 8 >= (1 << 16) else Sh, non_blocking=True)
     ready = torch.cuda.Event()
     ready.record()  # torch creates the CUDA event lazily: make the handle real before passing it
     win_ev = [torch.cuda.Event() for _ in plan]
@@ -745,6 +846,10 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
     finally:
         lib.scrf_position_outputs_event(None)
         lib.scrf_window_events(None, 0)
+        if streamed:
+            lib.scrf_input_gate(None, 0, 0)
+    if streamed:
+        _stream_S(prob, cum.S, gate, shift, gate_ready, pin)
     side = _side_stream()
     dev_outs = (bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals, bw.boundary_posterior)
     if plan:
@@ -752,14 +857,18 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         with torch.cuda.stream(side):
             for (w0, w1), ev in zip(plan, win_ev):
                 side.wait_event(ev)
-                for t, h in zip(dev_outs, early):
+                for i, (t, h) in enumerate(zip(dev_outs, early)):
                     if t is None:
                         continue
-                    hi = min(w1, t.shape[1])  # grad_S has T + 1 rows, the others T
-                    if hi <= w0:
+                    # rows the pass over boundaries [w0, w1) finalises: grad_S (T + 1 rows) and
+                    # grad_P_start / marginals / boundary (T rows) rows [w0, w1); grad_P_end row
+                    # e - 1 belongs to boundary e, so rows [w0 - 1, w1 - 1)
+                    lo, hi = (max(w0 - 1, 0), w1 - 1) if i == 2 else (w0, w1)
+                    hi = min(hi, t.shape[1])
+                    if hi <= lo:
                         continue
                     for b in range(t.shape[0]):  # contiguous per sequence: one async memcpy each
-                        h[b, w0:hi].copy_(t[b, w0:hi], non_blocking=True)
+                        h[b, lo:hi].copy_(t[b, lo:hi], non_blocking=True)
     else:
         side.wait_event(ready)
         with torch.cuda.stream(side):
@@ -771,6 +880,8 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         ledger.record("workspace", bw.work)
     logZ, gT, gB, cnt = _to_host(fwd.logZ, bw.grad_T, bw.grad_B, bw.expected_segment_count)
     side.synchronize()
+    if streamed and int(gate[-1].item()) != 0:
+        raise RuntimeError("streamed input: a sweep timed out waiting for a row chunk of S")
     gS, gPs, gPe, pm, bp = (None if h is None else h.numpy() for h in early)
     return (logZ, GradientSet(grad_S=gS, grad_T=gT, grad_B=gB, grad_P_start=gPs, grad_P_end=gPe),
             MarginalSet(pm, bp, cnt, np.asarray(cum.lengths)))

@@ -55,22 +55,26 @@ def make_full(name, seed, T, K, C, B, mode, ragged=False, projections=False, kee
     # overwrite the checkpoint set that streaming_backward replays from next
     block = recompute_alpha(ck.omega[:, ri].copy(), ck.N[:, ri], cum, params, t_lo, t_hi)
     print(f"{name}: replay {time.time() - t0:.0f}s", flush=True)
+    omega_idx = np.unique(np.array([0, 1, ri, n_ck - 1], np.int64))
+    kb = slice(0, keep_b)
+    # snapshot omega BEFORE the backward: with B = 1 the reference's streaming_backward replays
+    # each window through recompute_alpha, whose ring is a view of ckpts.omega[:, i] (see above),
+    # and so overwrites every checkpoint it replays
+    omega_snap = ck.omega[kb][:, omega_idx].copy()
     grads, marg = streaming_backward(cum, params, logZ, ck)
     print(f"{name}: backward {time.time() - t0:.0f}s", flush=True)
     segs, scores = streaming_viterbi(cum, params)
     print(f"{name}: viterbi {time.time() - t0:.0f}s", flush=True)
     rows_s = sample_rows(T + 1)          # grad_S rows (boundaries 0..T)
     rows_p = rows_s[rows_s < T]          # per-position rows 0..T-1
-    omega_idx = np.unique(np.array([0, 1, ri, n_ck - 1], np.int64))
     replay_rows = sample_rows(block.shape[1])
-    kb = slice(0, keep_b)
     st, en, lb, of = flat_segments(segs)
     out = dict(
         seed=np.int64(seed), T=np.int64(T), K=np.int64(K), C=np.int64(C), B=np.int64(B),
         mode=np.array(mode.value), ragged=np.bool_(ragged), projections=np.bool_(projections),
         keep_b=np.int64(keep_b), delta_arg=np.int64(-1), S_digest=np.array(s_digest(cum.S)),
         logZ=logZ, N=ck.N, delta=np.int64(ck.delta),
-        omega_idx=omega_idx, omega=ck.omega[kb][:, omega_idx],
+        omega_idx=omega_idx, omega=omega_snap,
         replay_i=np.int64(ri), replay_rows=replay_rows, replay=block[kb][:, replay_rows],
         rows_s=rows_s, rows_p=rows_p,
         grad_S=grads.grad_S[kb][:, rows_s], grad_T=grads.grad_T, grad_B=grads.grad_B,
@@ -98,6 +102,27 @@ JOBS = {
     "c3f": lambda: make_full("c3f", 0, 4000, 64, 39, 32, M.MEAN, keep_b=4),
 }
 
+def patch_omega(name):
+    """Re-take omega of an existing fixture from a fresh forward (fixtures written before the
+    snapshot fix above hold the post-backward, overwritten checkpoints when B = 1)."""
+    path = os.path.join(HERE, f"golden_{name}.npz")
+    z = dict(np.load(path))
+    t0 = time.time()
+    _, params, cum = equivalence_instance(int(z["seed"]), T=int(z["T"]), K=int(z["K"]), C=int(z["C"]),
+                                          B=int(z["B"]), mode=P.CenteringMode(str(z["mode"])))
+    assert s_digest(cum.S) == str(z["S_digest"])
+    logZ, ck = streaming_forward(cum, params)
+    assert np.array_equal(logZ, z["logZ"]) and np.array_equal(ck.N, z["N"])
+    z["omega"] = ck.omega[: int(z["keep_b"])][:, z["omega_idx"]].copy()
+    np.savez_compressed(path, **z)
+    print(f"patched omega of {path} in {time.time() - t0:.0f}s", flush=True)
+
+
 if __name__ == "__main__":
-    for n in sys.argv[1:] or list(JOBS):
-        JOBS[n]()
+    args = sys.argv[1:]
+    if args and args[0] == "--patch-omega":
+        for n in args[1:]:
+            patch_omega(n)
+    else:
+        for n in args or list(JOBS):
+            JOBS[n]()

@@ -58,11 +58,17 @@ def test_full_length_posterior_matches_reference(name, precision, memory):
             "boundary_posterior": parity.scaled_err(marg.boundary_posterior[:kb][:, z["rows_p"]],
                                                     z["boundary_posterior"])}
     print(name, precision, memory, {k: f"{v:.1e}" for k, v in errs.items()})
-    bad = {k: v for k, v in errs.items() if v > (tol["logZ"] if k == "logZ" else tol["grad"])}
+    gtol = tol["grad"]
+    if precision == "fp64" and int(z["T"]) >= 50000:
+        # the reference's own fp64 posterior drifts by ~1e-8 at T = 1e5 (its beta recursion runs
+        # 1e5 unnormalised logsumexp steps on values up to ~4e4): the deviation peaks at t -> 0
+        # and decays toward t = T with or without our cut normalisers (profiles/r02_c4f_fp64_drift.txt)
+        gtol = 5e-8
+    bad = {k: v for k, v in errs.items() if v > (tol["logZ"] if k == "logZ" else gtol)}
     assert not bad, (bad, errs)
     # whole-array checksums the fixture holds (every position, not just the sample)
-    np.testing.assert_allclose(marg.position_marginals.sum(axis=(1, 2)), z["pm_total"], rtol=tol["grad"])
-    np.testing.assert_allclose(marg.boundary_posterior.sum(axis=1), z["bp_total"], rtol=tol["grad"])
+    np.testing.assert_allclose(marg.position_marginals.sum(axis=(1, 2)), z["pm_total"], rtol=gtol)
+    np.testing.assert_allclose(marg.boundary_posterior.sum(axis=1), z["bp_total"], rtol=gtol)
 
 
 @pytest.mark.parametrize("name", ["c4f", "c5f", "c3f"])

@@ -329,6 +329,21 @@ def test_numpy_posterior_window_copies_match_device_outputs():
         np.testing.assert_array_equal(host, dev.cpu().numpy(), err_msg=name)
 
 
+def test_numpy_posterior_streamed_input_matches_device_outputs():
+    """At full memory and long T the numpy posterior() streams S to the device behind the sweeps
+    (4096-row chunks from both ends inward; the sweeps wait on per-chunk gates, scrf_input_gate):
+    same results bit for bit as with S fully resident first."""
+    _, params, cum = scrf.equivalence_instance(6, T=100000, K=64, C=24, B=2, mode=CenteringMode.MEAN, ragged=True)
+    assert cum.S.nbytes >= (32 << 20)
+    logZ, grads, marg = scrf.posterior(cum, params, memory="full")
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    fwd, bw = S.device_posterior(prob, memory="full")
+    np.testing.assert_array_equal(logZ, fwd.logZ.cpu().numpy())
+    np.testing.assert_array_equal(grads.grad_S, bw.grad_S.cpu().numpy())
+    np.testing.assert_array_equal(grads.grad_B, bw.grad_B.cpu().numpy())
+    np.testing.assert_array_equal(marg.position_marginals, bw.position_marginals.cpu().numpy())
+
+
 def test_alpha_beta_logz_agree_on_goldens():
     S.set_precision("fp32")
     for name in ["c1rp", "c2", "c3s", "c4s", "c5s"]:
