@@ -565,13 +565,16 @@ int run_sweep(const scrf_problem* p, int64_t delta, const SweepIO& io, cudaStrea
   const size_t smem = sweep_smem_bytes<R>(a.K, a.C, g);
   const bool tails = g.G > 1, cw1 = g.NCW == 1;
   cudaError_t e;
-  const int mode = io.tasks ? 2 : (io.store ? 1 : 0);
+  const int mode = io.tasks ? 2 : (io.store ? 1 : (a.gate ? 3 : 0));  // 3: full mode, streamed input
 #define SCRF_LAUNCH_SWEEP(M)                                                                              \
   (tails && cw1 ? launch_cl(sweep_kernel<R, true, true, M>, g.G, ncl, g.NT, smem, st, a, io.record)      \
    : tails    ? launch_cl(sweep_kernel<R, true, false, M>, g.G, ncl, g.NT, smem, st, a, io.record)     \
    : cw1      ? launch_cl(sweep_kernel<R, false, true, M>, g.G, ncl, g.NT, smem, st, a, io.record)     \
               : launch_cl(sweep_kernel<R, false, false, M>, g.G, ncl, g.NT, smem, st, a, io.record))
-  e = mode == 2 ? SCRF_LAUNCH_SWEEP(2) : mode == 1 ? SCRF_LAUNCH_SWEEP(1) : SCRF_LAUNCH_SWEEP(0);
+  e = mode == 2   ? SCRF_LAUNCH_SWEEP(2)
+      : mode == 1 ? SCRF_LAUNCH_SWEEP(1)
+      : mode == 3 ? SCRF_LAUNCH_SWEEP(3)
+                  : SCRF_LAUNCH_SWEEP(0);
 #undef SCRF_LAUNCH_SWEEP
   if (e != cudaSuccess) return (int)e;
   if (!io.tasks && io.store == 0 && (io.dirs & 1)) {

@@ -698,11 +698,11 @@ __device__ __forceinline__ long long out_row(const SweepArgs<R>& a, const SweepC
   return (x.dir == 0 ? (long long)x.b * ck_rows_alpha(a.T, a.delta, a.mA) : (long long)x.b * a.nW * (a.K + 32)) + r;
 }
 
-template <typename R>
+template <typename R, int MODE>
 __device__ __forceinline__ void put_out(const SweepArgs<R>& a, const SweepCtx& x, int t, int c, bool act, R y, R xv,
                                         double n, R am) {
   const int C = a.C;
-  if (!x.task && a.store == 0) {  // full mode: every position, row b*(T+1)+t
+  if (MODE == 0 || MODE == 3) {  // full mode: every position, row b*(T+1)+t
     const long long row = (long long)x.b * (a.T + 1) + t;
     if (act) {
       a.Y[x.dir][row * C + c] = y;
@@ -747,7 +747,7 @@ __device__ __forceinline__ void edge_init(const SweepCtx& x, const SweepGeo& g, 
 
 // Per-step edge work at A(q) (PubS == 8) for label c: (O, Q) and edge terms of target q+5,
 // outputs of position q; rows of target q+9 prefetched into the register FIFO.
-template <typename R>
+template <typename R, int MODE>
 __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
                                           bool act, const R* b2c, EdgeState& e) {
   const SweepGeo& g = a.geo;
@@ -773,11 +773,11 @@ __device__ __forceinline__ void edge_step(const SweepArgs<R>& a, const SweepCtx&
   }
   const int sl = q & pm;
   const int cs = act ? c : 0;
-  put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[q & (kNring - 1)], h.pubA[sl]);
+  put_out<R, MODE>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[q & (kNring - 1)], h.pubA[sl]);
 }
 
 // per-position outputs (Y^, X^, n, max shift) of positions q-3 .. q from the published rings
-template <typename R>
+template <typename R, int MODE>
 __device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
                                              bool act) {
   const int C = a.C;
@@ -787,7 +787,7 @@ __device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepC
     const int pos = q - 3 + i;
     if (pos >= 0) {
       const int sl = pos & 15;
-      put_out<R>(a, x, x.tpos(pos), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[pos & (kNring - 1)],
+      put_out<R, MODE>(a, x, x.tpos(pos), c, act, h.pubY[sl * C + cs], h.pubX[sl * C + cs], h.nring[pos & (kNring - 1)],
                  h.pubA[sl]);
     }
   }
@@ -796,7 +796,7 @@ __device__ __forceinline__ void edge_outputs(const SweepArgs<R>& a, const SweepC
 // One edge batch at A(q) (q % 4 == 0) for label c: (O, Q) and edge terms hk = O[u] + Q[u-k] +
 // B[k-1] (k = 1..4) of targets u = q+kLead .. q+kLead+3, the outputs Y^, X^, n, max shift of
 // positions q-3 .. q, and the register prefetch of the next batch's rows.
-template <typename R>
+template <typename R, int MODE>
 __device__ __forceinline__ void edge_batch(const SweepArgs<R>& a, const SweepCtx& x, const HeadPtr<R>& h, int q, int c,
                                            bool act, const R* b2c, EdgeState& e, bool outputs) {
   const SweepGeo& g = a.geo;
@@ -832,7 +832,7 @@ __device__ __forceinline__ void edge_batch(const SweepArgs<R>& a, const SweepCtx
 #pragma unroll
     for (int i = 0; i < 4; ++i) e.qh[i] = qa[4 + i];
   }
-  if (outputs) edge_outputs<R>(a, x, h, q, c, act);
+  if (outputs) edge_outputs<R, MODE>(a, x, h, q, c, act);
 }
 
 // log2(2^m s + sum_k 2^xk), k = 1..4
@@ -1227,7 +1227,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& 
 // groups from iteration q+5 on) and to the tail owning the label; n_q to every tail. With
 // NAS == 1 also the edge batches; otherwise only the outputs of the last L % 4 positions
 // (the edge batches cover positions <= 4 floor(L/4)).
-template <typename R, bool TAILS>
+template <typename R, bool TAILS, int MODE>
 __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, HeadPtr<R>& h,
                          const TailLayout& TL, int NA, int NAE, int wbase, bool do_edge) {
   using R2 = typename Vec2<R>::T;
@@ -1262,7 +1262,7 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
                    : nullptr;
   if (pslot && !do_edge) prog_publish(pslot, Lq + 1);  // only the positions after Lq are this warp's
   for (int q = 0; q <= L; ++q) {
-    if (a.gate && (q & 63) == 0) {  // streamed input: the next 256 positions' rows
+    if (MODE == 3 && (q & 63) == 0) {  // streamed input: the next 256 positions' rows
       if ((threadIdx.x & 31) == 0) gate_span_wait(a, x, q, min(q + 256, L));
       __syncwarp();
     }
@@ -1303,9 +1303,9 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
     if (TAILS && nsender && q <= nsend_max)
       st_async_f64(t_nslot + (uint32_t)((q & (kSlots - 1)) * sizeof(double)), n_q,
                    t_nbar + (uint32_t)((q & (kSlots - 1)) * sizeof(uint64_t)));
-    if (do_edge) edge_step<R>(a, x, h, q, c, act, b2c, es);
+    if (do_edge) edge_step<R, MODE>(a, x, h, q, c, act, b2c, es);
     if (!do_edge && q > Lq)  // outputs of the positions after the last edge batch
-      put_out<R>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q, h.pubA[sl]);
+      put_out<R, MODE>(a, x, x.tpos(q), c, act, h.pubY[sl * C + cs], pXc[sl * C], n_q, h.pubA[sl]);
     if (pslot && do_edge && (q & 255) == 255) prog_publish(pslot, q + 1);
 
     if (x.dir == 1 && q == L && c == 0 && !x.task) {
@@ -1323,7 +1323,7 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
 
 // ======================= edge warps (lane = label), NAS == 2 =======================
 // Sync A(q) for q % 4 == 0 only (barrier id 1 counts the edge warps) and run the edge batch.
-template <typename R>
+template <typename R, int MODE>
 __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
   const SweepGeo& g = a.geo;
   const int C = a.C, T = a.T, L = x.L;
@@ -1335,7 +1335,7 @@ __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr
   edge_init(x, g, h.oq, T, C, L, cs, es);
   for (int q = 0; q <= L; q += 4) {
     nbar_sync(BAR_A + 0, NA + NAE);
-    edge_batch<R>(a, x, h, q, c, act, b2c, es, g.NOW == 0);
+    edge_batch<R, MODE>(a, x, h, q, c, act, b2c, es, g.NOW == 0);
     if (blockIdx.x == 0 && c == 0) SCRF_GT(7, q);
   }
 }
@@ -1343,7 +1343,7 @@ __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr
 // ======================= output warp (lane = label), NOW == 1 =======================
 // Joins A(q) for q % 4 == 0 like the edge warps and writes the outputs of positions q-3 .. q,
 // so the edge batch (on the critical path through that barrier) carries no HBM stores.
-template <typename R>
+template <typename R, int MODE>
 __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
   const int C = a.C, L = x.L;
   const int c = threadIdx.x - wbase * 32;
@@ -1351,7 +1351,7 @@ __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<
   int* pslot = (a.prog && !x.task) ? a.prog + (size_t)(x.b * 2 + x.dir) * kProgSlots : nullptr;
   for (int q = 0; q <= L; q += 4) {
     nbar_sync(BAR_A + 0, NA + NAE);
-    edge_outputs<R>(a, x, h, q, c, act);
+    edge_outputs<R, MODE>(a, x, h, q, c, act);
     if (pslot && (q & 255) == 252) prog_publish(pslot, q + 1);
   }
   if (pslot) prog_publish(pslot, L + 1);
@@ -1432,11 +1432,11 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   else if (warp < g.NCW + g.NNW)
     head_near<R, TAILS>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
-    head_src<R, TAILS>(a, x, smem, h, TL, NA, NAE, g.NCW + g.NNW, g.NAS == 1);
+    head_src<R, TAILS, MODE>(a, x, smem, h, TL, NA, NAE, g.NCW + g.NNW, g.NAS == 1);
   else if (g.NAS == 2 && warp < 3 * g.NCW + g.NNW)
-    head_edge_role<R>(a, x, h, NA, NAE, 2 * g.NCW + g.NNW);
+    head_edge_role<R, MODE>(a, x, h, NA, NAE, 2 * g.NCW + g.NNW);
   else if (g.NOW && warp < NH / 32)
-    head_out_role<R>(a, x, h, NA, NAE, 3 * g.NCW + g.NNW);
+    head_out_role<R, MODE>(a, x, h, NA, NAE, 3 * g.NCW + g.NNW);
 }
 
 // ----------------------------------------------------------------------------
@@ -1883,7 +1883,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   x.S = a.S + (size_t)x.b * (a.T + 1) * a.C;
   x.ps = a.ps ? a.ps + (size_t)x.b * a.T * a.C : nullptr;
   x.pe = a.pe ? a.pe + (size_t)x.b * a.T * a.C : nullptr;
-  if (MODE == 0 && a.gate) {  // streamed input: the first rows every CTA may read before the loop
+  if (MODE == 3) {  // streamed input: the first rows every CTA may read before the loop
     if (threadIdx.x == 0) gate_span_wait(a, x, 0, min(x.L, 320));
     __syncthreads();
   }
