@@ -313,9 +313,10 @@ PostGeo post_geo(const scrf_problem* p, int prec, int Wn) {
   }
   q.CGB = cg;
   const int ngc = (C + cg - 1) / cg;
-  // blocked grad_B: one full wave at 2 CTAs per SM; exact kernel: ~4 CTAs per SM
+  // blocked grad_B: one full wave at one CTA per SM (128 registers, no spills); exact kernel:
+  // ~4 CTAs per SM
   const bool blk = prec == 0 && gradB_blocked();
-  long long want = (blk ? 2LL : 4LL) * num_sms();
+  long long want = (blk ? 1LL : 4LL) * num_sms();
   long long per = blk ? want / ((long long)ngc * B) : (want + (long long)ngc * B - 1) / ((long long)ngc * B);
   if (per < 1) per = 1;
   // CTA source ranges are whole micro-chunks; partials are kept per micro-chunk (the

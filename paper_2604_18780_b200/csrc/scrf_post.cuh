@@ -424,7 +424,7 @@ __host__ __device__ inline size_t post_gradB_blk_smem(int K, int CG) {
 }
 
 #ifndef SCRF_GBB_MINB
-#define SCRF_GBB_MINB 2
+#define SCRF_GBB_MINB 1
 #endif
 __global__ void __launch_bounds__(512, SCRF_GBB_MINB) post_gradB_blk_kernel(PostArgs<float> a) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -471,8 +471,9 @@ __global__ void __launch_bounds__(512, SCRF_GBB_MINB) post_gradB_blk_kernel(Post
   for (int s0 = sbeg + mi * kGBMicro; s0 < send; s0 += kGBSub) {
     __syncthreads();
     const int ns = min(kGBSub, send - s0);
+    static_assert((kGBSub & (kGBSub - 1)) == 0, "kGBSub: power of two");
     for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
-      const int cl = i / kGBSub, si = i % kGBSub, s = s0 + si, c = c0 + cl;
+      const int cl = i / kGBSub, si = i & (kGBSub - 1), s = s0 + si, c = c0 + cl;
       float2 v = make_float2(-CUDART_INF_F, 0.f);
       if (si < ns) {
         const double ra = a.RA[((size_t)b * C + c) * a.NR + (s - a.t_lo)] +
@@ -481,12 +482,49 @@ __global__ void __launch_bounds__(512, SCRF_GBB_MINB) post_gradB_blk_kernel(Post
       }
       sa[(size_t)cl * kGBSub + si] = v;
     }
-    for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
-      const int cl = i / nU, ui = i % nU, u = s0 + 1 + ui, c = c0 + cl;
+    // targets u = s0 + 1 + ui of this sub-chunk: rb for ui < kGBSub + K - 1, -inf beyond (window
+    // over-read). Consecutive sub-chunks of a CTA overlap in all but kGBSub of them: after the
+    // first, the kept ones move down by kGBSub in place and only the new kGBSub are loaded.
+    auto tgt = [&](int cl, int ui) -> float2 {
+      const int u = s0 + 1 + ui;
       float2 v = make_float2(-CUDART_INF_F, 0.f);
-      if (u <= L && u < a.w1 + K && ui < kGBSub + K)  // (beta rows of a window end at w1 + K - 1)
-        split2(a.RB[((size_t)b * C + c) * a.NR + (u - a.t_lo)], v.x, v.y);
-      sbv[(size_t)cl * rowU + gb_skew(ui)] = v;
+      if (u <= L && u < a.w1 + K && ui < kGBSub + K - 1)  // (beta rows of a window end at w1 + K - 1)
+        split2(a.RB[((size_t)b * C + c0 + cl) * a.NR + (u - a.t_lo)], v.x, v.y);
+      return v;
+    };
+    if (s0 == sbeg) {
+      for (int i = threadIdx.x; i < Cn * nU; i += blockDim.x) {
+        const int cl = i / nU, ui = i % nU;
+        sbv[(size_t)cl * rowU + gb_skew(ui)] = tgt(cl, ui);
+      }
+    } else {
+      const int nk = K - 1;  // kept per label: ui in [0, K - 1) <- [kGBSub, kGBSub + K - 1)
+      constexpr int kR = 8;
+      for (int base = 0; base < Cn * nk; base += kR * 512) {
+        float2 keep[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const int i = base + r * 512 + (int)threadIdx.x;
+          if (i < Cn * nk) {
+            const int cl = i / nk, ui = i - cl * nk;
+            keep[r] = sbv[(size_t)cl * rowU + gb_skew(ui + kGBSub)];
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const int i = base + r * 512 + (int)threadIdx.x;
+          if (i < Cn * nk) {
+            const int cl = i / nk, ui = i - cl * nk;
+            sbv[(size_t)cl * rowU + gb_skew(ui)] = keep[r];
+          }
+        }
+        __syncthreads();
+      }
+      for (int i = threadIdx.x; i < Cn * kGBSub; i += blockDim.x) {
+        const int cl = i / kGBSub, ui = nk + (i & (kGBSub - 1));
+        sbv[(size_t)cl * rowU + gb_skew(ui)] = tgt(cl, ui);
+      }
     }
     __syncthreads();
 #pragma unroll
