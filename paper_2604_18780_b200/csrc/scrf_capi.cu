@@ -334,7 +334,7 @@ int cut_spacing() { return env_int("SCRF_CUT_D", 512); }
 
 // Full-mode posterior passes (see run_full_post_win): SCRF_OVERLAP 1 = windows concurrent with
 // the sweeps (default), 0 = the same windows after the sweeps, -1 = one pass after the sweeps.
-int ovl_ws() { return env_int("SCRF_OVL_WS", 8192); }
+int ovl_ws() { return env_int("SCRF_OVL_WS", 4096); }
 int ovl_mode(const scrf_problem* p) {
   const int m = env_int("SCRF_OVERLAP", 1);
   const int ws = ovl_ws();
@@ -349,6 +349,7 @@ struct PLayout {
   size_t logZb, tot, cntp, gTp, gBp, cutU, corr, carry, clamp, accT, accB, accN, Zt, tcut, prog, status, RA, RB, Wt,
       Bmax, total;
   int prepNR;  // rows of RA / RB per (sequence, label): the longest pass + 2K - 1
+  int nprep;   // RA / RB sets (2: concurrent windows on two side streams)
 };
 PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o, int passWn = 0) {
   PLayout L;
@@ -361,7 +362,9 @@ PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o, int passWn =
   L.cntp = o;  o += al(B * q.nch * 8);
   L.gTp = o;   o += al(B * q.nch * C * C * 8);
   L.gBp = o;   o += al(B * q.nchB * K * C * 8);
-  L.cutU = o;  o += d > 0 ? al(B * (size_t)cut_slots(0, Wn, d) * C * 8) : 0;
+  // (windowed full-mode passes keep each window's cut slots apart: 2 extra slots per window)
+  const size_t xslots = passWn < Wn ? 2 * ((size_t)Wn / kGBMicro + 2) : 0;
+  L.cutU = o;  o += d > 0 ? al(B * ((size_t)cut_slots(0, Wn, d) + xslots) * C * 8) : 0;
   L.corr = o;  o += d > 0 ? al(B * (size_t)Wn * 8) : 0;
   L.carry = o; o += al(B * C * 8);
   L.clamp = o; o += al(B * 4);
@@ -373,8 +376,9 @@ PLayout p_layout(const scrf_problem* p, int prec, int Wn, size_t o, int passWn =
   L.prog = o;  o += al(B * 2 * kProgSlots * 4);
   L.status = o; o += al(4);
   L.prepNR = passWn + 2 * (int)K - 1;
-  L.RA = o;    o += al(B * C * (size_t)L.prepNR * 8);
-  L.RB = o;    o += al(B * C * (size_t)L.prepNR * 8);
+  L.nprep = passWn < Wn ? 2 : 1;  // windowed: one set per side stream
+  L.RA = o;    o += al(B * C * (size_t)L.prepNR * 8 * L.nprep);
+  L.RB = o;    o += al(B * C * (size_t)L.prepNR * 8 * L.nprep);
   L.Wt = o;    o += al(C * (2 * K + 2 * kCutEC) * 8);
   L.Bmax = o;  o += al(C * 8);
   L.total = o;
@@ -623,6 +627,11 @@ struct PassOpt {
   bool seqwide = false;
   int pnch = 0, pnchB = 0;    // sequence-wide chunk / micro-chunk counts
   cudaEvent_t pos_ev = nullptr;  // recorded once this pass's per-position outputs are final
+  // scratch placement of concurrent windows (doubles): frame correction, chunk totals, cut
+  // slots; RA / RB set; duration weights of the cut kernel already in place (cut_w_kernel)
+  size_t corr_off = 0, tot_off = 0, cut_off = 0;
+  int prep_set = 0;
+  bool w_ready = false;
 };
 
 template <typename R>
@@ -663,7 +672,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   a.bnd = out.bnd;
   a.CH = q.CH;
   a.nch = q.nch;
-  a.tot = (double*)(wb + PL.tot);
+  a.tot = (double*)(wb + PL.tot) + opt.tot_off;
   a.cntp = (double*)(wb + PL.cntp);
   a.gTp = (double*)(wb + PL.gTp);
   a.SCB = q.SCB;
@@ -689,8 +698,9 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   a.t_lo = w0 - K + 1;
   a.NR = Wn + 2 * K - 1;
   if (a.NR > PL.prepNR) return SCRF_EWORK;
-  a.RA = (double*)(wb + PL.RA);
-  a.RB = (double*)(wb + PL.RB);
+  if (opt.prep_set >= PL.nprep) return SCRF_EWORK;
+  a.RA = (double*)(wb + PL.RA) + (size_t)opt.prep_set * B * C * PL.prepNR;
+  a.RB = (double*)(wb + PL.RB) + (size_t)opt.prep_set * B * C * PL.prepNR;
   {
     const size_t sm = post_prep_smem(C);
     e = cudaFuncSetAttribute(post_prep_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -701,8 +711,10 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
   const int cd = cut_spacing();
   const int ncut = cut_slots(w0, w1, cd);
   if (cd > 0) {
-    ++g_launches;
-    cut_w_kernel<R><<<C, 256, 0, st>>>(p->duration_bias, K, C, (R*)(wb + PL.Wt), (double*)(wb + PL.Bmax));
+    if (!opt.w_ready) {
+      ++g_launches;
+      cut_w_kernel<R><<<C, 256, 0, st>>>(p->duration_bias, K, C, (R*)(wb + PL.Wt), (double*)(wb + PL.Bmax));
+    }
     CutArgs<R> ca;
     memset(&ca, 0, sizeof(ca));
     ca.S = p->S;
@@ -729,7 +741,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ca.w1 = w1;
     ca.d = cd;
     ca.ncut = ncut;
-    ca.U = (double*)(wb + PL.cutU);
+    ca.U = (double*)(wb + PL.cutU) + opt.cut_off;
     ca.RA = a.RA;
     ca.RB = a.RB;
     ca.t_lo = a.t_lo;
@@ -741,13 +753,13 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
     cut_kernel<R><<<dim3(ncut, (C + kCutCG - 1) / kCutCG, B), 256, sm, st>>>(ca);
-    a.corr = (const double*)(wb + PL.corr);
+    a.corr = (const double*)(wb + PL.corr) + opt.corr_off;
   }
   // per-position frame correction (when enabled) and the beta-side clamp-event count
   ++g_launches;
   cut_corr_kernel<R><<<dim3((Wn + 255) / 256, B), 256, 0, st>>>(
-      p->lengths, C, w0, w1, cd, ncut, cd > 0 ? (const double*)(wb + PL.cutU) : nullptr,
-      cd > 0 ? (double*)(wb + PL.corr) : nullptr, a.Xb, a.nb, m.rowsB, m.tB0, (int32_t*)(wb + PL.clamp));
+      p->lengths, C, w0, w1, cd, ncut, cd > 0 ? (const double*)(wb + PL.cutU) + opt.cut_off : nullptr,
+      cd > 0 ? (double*)(wb + PL.corr) + opt.corr_off : nullptr, a.Xb, a.nb, m.rowsB, m.tB0, (int32_t*)(wb + PL.clamp));
   {
     const size_t sm = post_pos_smem<R>(C, q.CH);
     e = cudaFuncSetAttribute(post_pos_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -757,7 +769,7 @@ int run_pass(const scrf_problem* p, const MsgView& m, int w0, int w1, const Post
     ++g_launches;
     if (cd > 0 && cd % q.CH == 0)
       cut_prefix_kernel<<<(B * C + 127) / 128, 128, 0, st>>>(p->lengths, B, C, q.nch, q.CH, w0, w1, cd, ncut,
-                                                           (const double*)(wb + PL.cutU), a.tot,
+                                                           (const double*)(wb + PL.cutU) + opt.cut_off, a.tot,
                                                            opt.seqwide ? nullptr : (double*)(wb + PL.carry));
     else if (w0 == 0 && !opt.seqwide)
       post_prefix_kernel<<<(B * C + 7) / 8, 256, 0, st>>>(B, C, q.nch, a.tot);
@@ -919,21 +931,26 @@ int ovl_windows(const scrf_problem* p, OvlWin* w, int cap) {
 // writer warps per sweep cluster (SweepArgs::prog slots): output + source warp, or the source warps
 int prog_writers(int C) { return C <= 32 ? 2 : (C + 31) / 32; }
 
+// two low-priority side streams per device: the windows left and right of the middle run on
+// their own streams (independent scratch), so the passes of both flanks overlap each other too
 struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, probe = nullptr, join[2] = {nullptr, nullptr};
 };
 SideStream& side_stream() {
   static SideStream ss[64];
   int dev = 0;
   cudaGetDevice(&dev);
   SideStream& x = ss[dev & 63];
-  if (!x.s) {
+  if (!x.s[0]) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, lo);
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamCreateWithPriority(&x.s[i], cudaStreamNonBlocking, lo);
+      cudaEventCreateWithFlags(&x.join[i], cudaEventDisableTiming);
+    }
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.probe, cudaEventDisableTiming);
   }
   return x;
 }
@@ -987,7 +1004,7 @@ int ovl_begin(const scrf_problem* p, unsigned char* wb, const PLayout& PL, int m
   if (e == cudaSuccess) e = cudaMemsetAsync(wb + PL.status, 0, 4, st);
   if (e == cudaSuccess && mode == 1) {
     SideStream& ss = side_stream();
-    if (!ss.s) return (int)cudaErrorUnknown;
+    if (!ss.s[0] || !ss.s[1]) return (int)cudaErrorUnknown;
     e = cudaEventRecord(ss.fork, st);
   }
   return (int)e;
@@ -1040,23 +1057,26 @@ int run_full_post_win(const scrf_problem* p, const void* fstate, void* work, con
   const int B = (int)p->B, C = (int)p->C;
   const int d = cut_spacing();
   const PostGeo qall = post_geo(p, sizeof(R) == 8, (int)p->T + 1);
-  cudaStream_t sw = st;
+  // mode 1: windows left / right of the middle on side streams 0 / 1; mode 0: all on st
+  cudaStream_t sw[2] = {st, st};
   SideStream* ss = nullptr;
   if (mode == 1) {
     ss = &side_stream();
-    sw = ss->s;
-    cudaError_t e = cudaStreamWaitEvent(sw, ss->fork, 0);
+    sw[0] = ss->s[0];
+    sw[1] = ss->s[1];
+    cudaError_t e = cudaStreamWaitEvent(sw[0], ss->fork, 0);
     if (e != cudaSuccess) return (int)e;
   }
   const int nw = prog_writers(C);
   int* status = (int*)(wb + W.P.status);
-  // provisional log Z from the middle cut of each sequence
+  // provisional log Z from the middle cut of each sequence, and the cut kernel's duration
+  // weights, on side stream 0; side stream 1 starts after them
   if (mode == 1) {
     ++g_launches;
-    prog_wait_kernel<<<1, 256, 0, sw>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, 0, 0, d, status);
+    prog_wait_kernel<<<1, 256, 0, sw[0]>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, 0, 0, d, status);
   }
   ++g_launches;
-  probe_pos_kernel<<<(B + 127) / 128, 128, 0, sw>>>(p->lengths, B, d, (int*)(wb + W.P.tcut));
+  probe_pos_kernel<<<(B + 127) / 128, 128, 0, sw[0]>>>(p->lengths, B, d, (int*)(wb + W.P.tcut));
   {
     CutArgs<R> ca;
     fill_cut_args<R>(p, m, nullptr, &ca);
@@ -1068,34 +1088,53 @@ int run_full_post_win(const scrf_problem* p, const void* fstate, void* work, con
     cudaError_t e = cudaFuncSetAttribute(cut_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return (int)e;
     ++g_launches;
-    cut_kernel<R><<<dim3(1, (C + kCutCG - 1) / kCutCG, B), 256, sm, sw>>>(ca);
+    cut_kernel<R><<<dim3(1, (C + kCutCG - 1) / kCutCG, B), 256, sm, sw[0]>>>(ca);
   }
   ++g_launches;
-  probe_finish_kernel<R><<<(B + 127) / 128, 128, 0, sw>>>(p->lengths, B, C, (const int*)(wb + W.P.tcut), m.na, m.nb,
-                                                        m.rowsA, m.tA0, m.rowsB, m.tB0,
-                                                        (const double*)(wb + W.P.cutU), (double*)(wb + W.P.Zt));
+  probe_finish_kernel<R><<<(B + 127) / 128, 128, 0, sw[0]>>>(p->lengths, B, C, (const int*)(wb + W.P.tcut), m.na, m.nb,
+                                                           m.rowsA, m.tA0, m.rowsB, m.tB0,
+                                                           (const double*)(wb + W.P.cutU), (double*)(wb + W.P.Zt));
+  ++g_launches;
+  cut_w_kernel<R><<<C, 256, 0, sw[0]>>>(p->duration_bias, (int)p->K, C, (R*)(wb + W.P.Wt), (double*)(wb + W.P.Bmax));
+  if (mode == 1) {
+    cudaError_t e = cudaEventRecord(ss->probe, sw[0]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sw[1], ss->probe, 0);
+    if (e != cudaSuccess) return (int)e;
+  }
   OvlWin win[4096];
   const int nwin = ovl_windows(p, win, 4096);
+  const int ws = ovl_ws();
   PassOpt opt;
   opt.Z = (const double*)(wb + W.P.Zt);
   opt.seqwide = true;
   opt.pnch = qall.nch;
   opt.pnchB = qall.nchB;
+  opt.w_ready = true;
   for (int i = 0; i < nwin; ++i) {
+    const int w0 = win[i].w0, w1 = win[i].w1;
+    const int side = (long long)(w0 + w1) > (long long)p->T + 1 ? 1 : 0;
     opt.pos_ev = i < g_win_nev ? g_win_ev[i] : nullptr;
+    // disjoint scratch per window (positions, chunks and cut slots of the window itself)
+    opt.corr_off = (size_t)B * w0;
+    opt.tot_off = (size_t)(w0 / qall.CH) * B * C;
+    opt.cut_off = (size_t)(w0 / d + 2 * (w0 / ws)) * B * C;
+    opt.prep_set = side;
     if (mode == 1) {
       ++g_launches;
-      prog_wait_kernel<<<1, 256, 0, sw>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, win[i].w1 + 1,
-                                          win[i].w0 - 1, 0, status);
+      prog_wait_kernel<<<1, 256, 0, sw[side]>>>((const int*)(wb + W.P.prog), p->lengths, B, nw, dirs, w1 + 1,
+                                                w0 - 1, 0, status);
     }
-    int rc = run_pass<R>(p, m, win[i].w0, win[i].w1, out, wb, W.P, i == nwin - 1, sw, opt);
+    int rc = run_pass<R>(p, m, w0, w1, out, wb, W.P, false, sw[side], opt);
     if (rc) return rc;
   }
   if (mode == 1) {
-    cudaError_t e = cudaEventRecord(ss->join, sw);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ss->join, 0);
-    if (e != cudaSuccess) return (int)e;
+    for (int i = 0; i < 2; ++i) {
+      cudaError_t e = cudaEventRecord(ss->join[i], sw[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ss->join[i], 0);
+      if (e != cudaSuccess) return (int)e;
+    }
   }
+  if (g_ev_pos) cudaEventRecord(g_ev_pos, st);  // every window's per-position outputs are final
   // the sequence-wide sums, in the single-pass order
   const int nT = C * C, nB = (int)p->K * C;
   ++g_launches;
