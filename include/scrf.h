@@ -238,6 +238,12 @@ int scrf_input_gate(const int32_t* gate, int ngate, int shift);
  * copies queued before it on that stream). */
 int scrf_gate_set(int32_t* gate, int j, void* stream);
 
+/* Rows [r0, r1) of B row-major blocks of `rows` rows of row_bytes each (e.g. S: rows = T + 1,
+ * row_bytes = 8 C), host (pinned) -> device, as one 2-D copy on `stream`; then, if gate is not
+ * NULL, scrf_gate_set(gate, j). */
+int scrf_upload_rows(void* dst, const void* src, int64_t B, int64_t rows, int64_t row_bytes, int64_t r0, int64_t r1,
+                     int32_t* gate, int j, void* stream);
+
 /* Debug: if non-NULL, the next sweep writes clock64() phase stamps of cluster 0 for
  * positions 64..319 into buf (int64 [256][16]: chain lane 0 in 0..7, near thread 0 in 8..15). */
 void scrf_debug_trace(void* buf);

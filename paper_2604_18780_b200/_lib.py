@@ -87,6 +87,7 @@ _SIGS = {
     "scrf_window_events": (None, [_vp, _int]),
     "scrf_input_gate": (_int, [_vp, _int, _int]),
     "scrf_gate_set": (_int, [_vp, _int, _vp]),
+    "scrf_upload_rows": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _int, _vp]),
     "scrf_debug_trace": (None, [_vp]),
     "scrf_debug_hang": (_int, [_vp]),
 }

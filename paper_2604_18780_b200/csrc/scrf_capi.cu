@@ -2066,6 +2066,23 @@ int scrf_input_gate(const int32_t* gate, int ngate, int shift) {
   return SCRF_OK;
 }
 
+int scrf_upload_rows(void* dst, const void* src, int64_t B, int64_t rows, int64_t row_bytes, int64_t r0, int64_t r1,
+                     int32_t* gate, int j, void* stream) {
+  if (!dst || !src) return SCRF_ENULL;
+  if (B < 1 || rows < 1 || row_bytes < 1 || r0 < 0 || r1 > rows || r1 <= r0) return SCRF_EDIM;
+  const size_t pitch = (size_t)rows * row_bytes;
+  cudaError_t e = cudaMemcpy2DAsync((char*)dst + r0 * row_bytes, pitch, (const char*)src + r0 * row_bytes, pitch,
+                                    (size_t)(r1 - r0) * row_bytes, (size_t)B, cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return (int)e;
+  if (gate) {
+    if (j < 0) return SCRF_EDIM;
+    gate_set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(gate, j);
+    e = cudaGetLastError();
+  }
+  return (int)e;
+}
+
 int scrf_gate_set(int32_t* gate, int j, void* stream) {
   if (!gate) return SCRF_ENULL;
   if (j < 0) return SCRF_EDIM;

@@ -590,9 +590,9 @@ __device__ __forceinline__ double2 oq_of(const SweepCtx& x, const SweepGeo& g, i
 
 // Streamed input: wait until the rows of local positions p0 .. p1 (and one row beyond each end:
 // rows are not cache-line aligned, so a line fetched with an edge row may hold bytes of its
-// neighbour) are on the device. The source warps call it every 64 positions for the next 256:
-// every reader of S in the cluster (edge warps, output rows, tails) stays within a few dozen
-// positions of the source warps -- they wait on its barriers / ring sends -- so it gates them all.
+// neighbour) are on the device. The readers of S call it before they cross into rows not yet
+// checked, 512 rows at a time: the edge warps (or the source warps when they do the edge work)
+// every 256 positions, each tail thread when its next staged target passes its threshold.
 // Gives up after 2 s (records gate[ngate] = 1) rather than hang on a caller bug.
 template <typename R>
 __device__ __noinline__ void gate_span_wait(const SweepArgs<R>& a, const SweepCtx& x, int p0, int p1) {
@@ -1262,8 +1262,8 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
                    : nullptr;
   if (pslot && !do_edge) prog_publish(pslot, Lq + 1);  // only the positions after Lq are this warp's
   for (int q = 0; q <= L; ++q) {
-    if (MODE == 3 && (q & 63) == 0) {  // streamed input: the next 256 positions' rows
-      if ((threadIdx.x & 31) == 0) gate_span_wait(a, x, q, min(q + 256, L));
+    if (MODE == 3 && do_edge && (q & 255) == 0) {  // streamed input (edge work here): next 512 rows
+      if ((threadIdx.x & 31) == 0) gate_span_wait(a, x, q, min(q + 512, L));
       __syncwarp();
     }
 #ifdef SCRF_TRACE
@@ -1334,6 +1334,10 @@ __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr
   EdgeState es;
   edge_init(x, g, h.oq, T, C, L, cs, es);
   for (int q = 0; q <= L; q += 4) {
+    if (MODE == 3 && (q & 255) == 0) {  // streamed input: the rows of the next 512 positions
+      if ((threadIdx.x & 31) == 0) gate_span_wait(a, x, q, min(q + 512, L));
+      __syncwarp();
+    }
     nbar_sync(BAR_A + 0, NA + NAE);
     edge_batch<R, MODE>(a, x, h, q, c, act, b2c, es, g.NOW == 0);
     if (blockIdx.x == 0 && c == 0) SCRF_GT(7, q);
@@ -1458,7 +1462,12 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   // each warp stages its own copy (warps sharing a label run at different paces)
   const int NWs = tail_stage_slots(g), LPW = tail_lpw(g);
   const int WPL_ = g.WPL, lstep_ = g.NWt / WPL_, cl0_ = warp / WPL_;
+  int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
   auto stage = [&](int u, int cl) {
+    if (a.gate && u >= gnext) {
+      gate_span_wait(a, x, u, min(u + 512, x.L));
+      gnext = u + 256;
+    }
     const int t = x.tpos(u), c = lo + cl;
     double* d = stg + ((size_t)(u & (kStage - 1)) * NWs + warp * LPW + (cl - cl0_) / lstep_) * 2;
     cp_async8(d, x.S + (size_t)t * C + c);
@@ -1555,7 +1564,12 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   const R* wt = (const R*)(smem + TL.wtab) + (size_t)cl * 2 * WSZ;
   const R* bx = (const R*)(smem + TL.bx) + (size_t)cl * (kBlk + 1);
   const R bmax = bx[kBlk];
+  int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
   auto stage = [&](int u) {
+    if (a.gate && u >= gnext) {
+      gate_span_wait(a, x, u, min(u + 512, x.L));
+      gnext = u + 256;
+    }
     const int t = x.tpos(u), c = lo + cl;
     double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + cl) * 2;
     cp_async8(d, x.S + (size_t)t * C + c);

@@ -628,6 +628,7 @@ def _fill_pinned(out: torch.Tensor, t: torch.Tensor) -> None:
 
 
 _GATE_SHIFT = 12  # 4096-row chunks of S
+_PIN_KEEP = []    # pinned staging buffers of streamed uploads still in flight
 
 
 def _gate_for(prob: DeviceProblem):
@@ -678,13 +679,21 @@ def _stream_S(prob: DeviceProblem, S_host, gate: torch.Tensor, shift: int, gate_
     St = torch.from_numpy(Sh)  # no copy; torch's CPU copy into pinned memory is multi-threaded
     cs = _copy_stream()
     cs.wait_event(gate_ready)
+    row_bytes = Sh.shape[2] * 8
     with torch.cuda.stream(cs):
         for j in order:
             r0, r1 = j * R, min((j + 1) * R, T1)
             pin[:, r0:r1].copy_(St[:, r0:r1])
-            for b in range(B):  # contiguous per sequence: one async memcpy each
-                prob.S[b, r0:r1].copy_(pin[b, r0:r1], non_blocking=True)
-            _lib.check(lib.scrf_gate_set(_lib.ptr(gate), j, _lib.stream_handle()), "scrf_gate_set")
+            # one 2-D copy of the chunk's rows of every sequence, then its gate
+            _lib.check(lib.scrf_upload_rows(_lib.ptr(prob.S), _lib.ptr(pin), B, T1, row_bytes, r0, r1,
+                                            _lib.ptr(gate), j, _lib.stream_handle()), "scrf_upload_rows")
+    # keep the pinned staging alive until its copies have run (torch's host allocator only
+    # tracks copies it issued itself)
+    done = torch.cuda.Event()
+    done.record(cs)
+    _PIN_KEEP.append((pin, done))
+    while _PIN_KEEP and _PIN_KEEP[0][1].query():
+        _PIN_KEEP.pop(0)
     torch.cuda.current_stream().wait_stream(cs)
 
 
