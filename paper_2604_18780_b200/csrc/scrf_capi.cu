@@ -452,7 +452,7 @@ WLayout w_layout(const scrf_problem* p, int64_t delta, int prec, int G) {
 template <typename Kern, typename ArgT>
 cudaError_t launch_cl(Kern kern, int G, int nclusters, int NT, size_t smem, cudaStream_t st, ArgT arg, bool record) {
   const size_t half = (size_t)smem_optin() / 2 + 1024;
-  if (smem < half) smem = half;
+  if (smem < half && !env_int("SCRF_NO_PAD", 0)) smem = half;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (G > 8) {
