@@ -202,12 +202,20 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
       g.CgMax = (C + tails - 1) / tails;
       g.WPL = 1;
       g.TBlk = (blk && g.CgMax <= 16) ? 1 : 0;
-      g.TWb = (g.TBlk && g.CgMax * 2 <= 16) ? 2 : 1;  // two warps per label when they fit
+      if (blk && !g.TBlk && env_int("SCRF_TAIL_ML", 1)) {
+        // several labels per warp: LB lanes per label hold the <= LB live complete blocks
+        const int nblk = (K - kNear - 1) / 32 + 1;
+        int LB = 8;
+        while (LB < nblk) LB *= 2;
+        if (LB <= 16 && (g.CgMax + 32 / LB - 1) / (32 / LB) <= 16) g.TBlk = LB;
+      }
+      g.TWb = (g.TBlk == 1 && g.CgMax * 2 <= 16) ? 2 : 1;  // two warps per label when they fit
       g.KTm = g.TBlk ? 63 : pow2_ceil(K) - 1;
       if (!g.TBlk)
         while (g.WPL < 4 && g.CgMax * g.WPL * 2 <= 16) g.WPL *= 2;
       g.NWt = g.CgMax * g.WPL < 16 ? g.CgMax * g.WPL : 16 / g.WPL * g.WPL;
-      if (g.TBlk) g.NWt = g.CgMax * g.TWb;
+      if (g.TBlk == 1) g.NWt = g.CgMax * g.TWb;
+      if (g.TBlk > 1) g.NWt = (g.CgMax + 32 / g.TBlk - 1) / (32 / g.TBlk);
       const int head_nt = (g.NCW + g.NAS * g.NCW + g.NNW + g.NOW) * 32;
       g.NT = head_nt > g.NWt * 32 ? head_nt : g.NWt * 32;
       size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);

@@ -123,7 +123,8 @@ struct SweepGeo {
   int GWn;    // near threads per label (power of two <= 32)
   int NWt;    // tail warps
   int WPL;    // tail warps per label (each pushes its own partial)
-  int TBlk;   // 1: blocked tails (exp-space source blocks, FMA); 0: exact per-term tails
+  int TBlk;   // blocked tails (exp-space source blocks, FMA): 1 = one label per warp, 8 / 16 = that
+              // many lanes per label (32 / TBlk labels per warp: more labels per tail); 0 = exact
   int PsRow;  // staged row holding Ps[t] (0 = no proj_start)
   int PeRow;  // staged row holding Pe[t-1] (0 = no proj_end)
   int CgMax;  // max labels per tail
@@ -280,12 +281,13 @@ constexpr int kBlk = 32;
 // Input rows are prefetched into registers one batch (or four steps) ahead.
 constexpr int kLead = 8;
 __host__ __device__ inline int edge_lead(const SweepGeo& g) { return g.PubS == 16 ? kLead : 5; }
-__host__ __device__ inline int blk_wlen(int kc) { return (1024 + 64 + kc + 1) & ~1; }
+// w table length: windows read durations up to K + 35
+__host__ __device__ inline int blk_wlen(int kc, int K) { return ((K < 1024 + kc ? K : 1024 + kc) + 64 + 1) & ~1; }
 // w is stored in rows of 32 elements with a row stride of 34: lanes read windows that start
 // 32*j elements apart, which the skew spreads over all banks (pairs never straddle a row)
 __host__ __device__ inline int blk_wrow() { return 34; }
 __host__ __device__ inline int blk_wphys(int e) { return (e >> 5) * 34 + (e & 31); }
-__host__ __device__ inline int blk_wsize(int kc) { return (blk_wlen(kc) / 32 + 2) * 34; }
+__host__ __device__ inline int blk_wsize(int kc, int K) { return (blk_wlen(kc, K) / 32 + 2) * 34; }
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -335,7 +337,7 @@ __host__ __device__ inline TailLayout tail_layout(int K, int C, const SweepGeo& 
   L.nslot = o; o += a16(kSlots * sizeof(double));
   L.tbar = o;  o += a16(kSlots * sizeof(uint64_t));
   L.stg = o;   o += a16((size_t)kStage * 2 * tail_stage_slots(g) * sizeof(double));
-  L.wtab = o;  o += g.TBlk ? a16((size_t)g.CgMax * 2 * blk_wsize(g.kc) * sizeof(R)) : 0;
+  L.wtab = o;  o += g.TBlk ? a16((size_t)g.CgMax * 2 * blk_wsize(g.kc, K) * sizeof(R)) : 0;
   L.bx = o;    o += g.TBlk ? a16((size_t)g.CgMax * (kBlk + 1) * sizeof(R)) : 0;
   L.total = o;
   return L;
@@ -1560,7 +1562,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   const double* nslot = (const double*)(smem + TL.nslot);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
   double* stg = (double*)(smem + TL.stg);
-  const int WSZ = blk_wsize(kc);
+  const int WSZ = blk_wsize(kc, K);
   const R* wt = (const R*)(smem + TL.wtab) + (size_t)cl * 2 * WSZ;
   const R* bx = (const R*)(smem + TL.bx) + (size_t)cl * (kBlk + 1);
   const R bmax = bx[kBlk];
@@ -1806,6 +1808,253 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   cp_async_wait<0>();
 }
 
+// Blocked tail with several labels per warp (TBlk = LB lanes per label, 32 / LB labels per warp):
+// the arithmetic of tail_loop_blocked, for durations short enough that at most LB complete source
+// blocks are live (LB >= (K - kc - 1) / 32 + 1). A label's lane group holds one block per lane
+// (block j in sub-lane j % LB), and the newest, incomplete block's 32 sources are spread over
+// the group, 32 / LB per lane. Lets the exp-space tails serve 43-label slices (config 5: C = 128
+// over 3 tails, where one label per warp would need 43 warps).
+template <typename R, int LB>
+__device__ void tail_loop_blocked_ml(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem,
+                                     const HeadLayout& HL, const TailLayout& TL, int lo, int Cg) {
+  using R2 = typename Vec2<R>::T;
+  constexpr int P = 32 / LB;    // labels per warp
+  constexpr int Q = kBlk / LB;  // sources of a 32-block per sub-lane
+  const SweepGeo& g = a.geo;
+  const int C = a.C, T = a.T, L = x.L, kc = g.kc, KTm = g.KTm, K = a.K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pg = lane / LB, sl = lane % LB, gbase = pg * LB;
+  const int cl = warp * P + pg;
+  const bool lact = cl < Cg;  // groups past the tail's labels stay warp-synchronous but send nothing
+  const int clc = lact ? cl : 0;
+  const R2* rg = (const R2*)(smem + TL.ring) + (size_t)clc * (KTm + 1);
+  const double* nslot = (const double*)(smem + TL.nslot);
+  uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
+  double* stg = (double*)(smem + TL.stg);
+  const int WSZ = blk_wsize(kc, K);
+  const R* wt = (const R*)(smem + TL.wtab) + (size_t)clc * 2 * WSZ;
+  const R* bx = (const R*)(smem + TL.bx) + (size_t)clc * (kBlk + 1);
+  const R bmax = bx[kBlk];
+  int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
+  auto stage = [&](int u) {
+    if (a.gate && u >= gnext) {
+      gate_span_wait(a, x, u, min(u + 512, x.L));
+      gnext = u + 256;
+    }
+    const int t = x.tpos(u), c = lo + clc;
+    double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + clc) * 2;
+    cp_async8(d, x.S + (size_t)t * C + c);
+    if (x.dir == 0 && x.pe && t >= 1)
+      cp_async8(d + 1, x.pe + (size_t)(t - 1) * C + c);
+    else if (x.dir == 1 && x.ps && t < T)
+      cp_async8(d + 1, x.ps + (size_t)t * C + c);
+    else
+      d[1] = 0.0;
+  };
+  // sub-lanes 0..3 of each label group stage / compute / send targets ub + sl
+  const int u0 = kc + 1;
+  constexpr int nahead = 3;
+  for (int gq = 0; gq < nahead; ++gq) {
+    if (lact && sl < 4 && u0 + 4 * gq + sl <= L) stage(u0 + 4 * gq + sl);
+    cp_async_commit();
+  }
+  const uint32_t hbar = mapa_u32(smem_u32(smem + HL.tbar), 0);
+  const uint32_t hpart = mapa_u32(smem_u32(smem + HL.tpart), 0);
+  R zr[kBlk];
+#pragma unroll
+  for (int i = 0; i < kBlk; ++i) zr[i] = 0;
+  R Gh = Mth<R>::ninf(), Gl = 0;
+  int jown = -1, jlast = -1, snext = 0;
+  for (int ub = u0; ub <= L; ub += 4) {
+    const int sb = ub - kc - 1;         // newest source of target ub (a multiple of 4)
+    const int nt = min(4, L - ub + 1);  // targets in this group
+    cp_async_wait<2>();
+    __syncwarp();
+    const int s0 = snext;
+    for (int s = s0; s < sb + nt; ++s) sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
+    snext = sb + nt;
+    R eh[4], el[4];
+    {
+      R h = 0, l = 0;
+      if (lact && sl < nt) {
+        const int u = ub + sl;
+        const double F = nslot[(sb + sl) & (kSlots - 1)];
+        const double* d = stg + ((size_t)(u & (kStage - 1)) * g.CgMax + clc) * 2;
+        const double s2 = d[0] * kLog2e, o2 = d[1] * kLog2e;
+        split2((x.dir == 0 ? s2 + o2 : -s2 + o2) - F, h, l);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        eh[i] = __shfl_sync(0xffffffffu, h, gbase + i);
+        el[i] = __shfl_sync(0xffffffffu, l, gbase + i);
+      }
+    }
+    __syncwarp();
+    if (warp == 0 && lane < snext - s0) {
+      const int s = s0 + lane;
+      if (s + kSlots <= L - kc - 1)
+        mbar_expect(smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
+    }
+    // newest complete block: z = 2^(r - G) (G its largest source; first one in source order
+    // supplies the lo part) into the registers of its owner sub-lane jb % LB
+    if (sb >= kBlk && (sb >> 5) - 1 > jlast) {
+      const int jb = (sb >> 5) - 1;
+      R2 r[Q];
+      R gh = Mth<R>::ninf();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        r[q] = rg[(jb * kBlk + sl + LB * q) & KTm];
+        gh = fmax(gh, r[q].x);
+      }
+#pragma unroll
+      for (int o = LB / 2; o > 0; o >>= 1) gh = fmax(gh, __shfl_xor_sync(0xffffffffu, gh, o));
+      int ic = 1 << 30;
+      R glc = 0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (ic == (1 << 30) && r[q].x == gh) {
+          ic = sl + LB * q;
+          glc = r[q].y;
+        }
+#pragma unroll
+      for (int o = LB / 2; o > 0; o >>= 1) {
+        const int oi = __shfl_xor_sync(0xffffffffu, ic, o);
+        const R og = __shfl_xor_sync(0xffffffffu, glc, o);
+        if (oi < ic) {
+          ic = oi;
+          glc = og;
+        }
+      }
+      const R gl = glc;
+      R z[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        z[q] = (gh == Mth<R>::ninf() || r[q].x == Mth<R>::ninf()) ? (R)0 : Mth<R>::ex2((r[q].x - gh) + (r[q].y - gl));
+      const bool own = sl == (jb & (LB - 1));
+#pragma unroll
+      for (int i = 0; i < kBlk; ++i) {
+        const R v = __shfl_sync(0xffffffffu, z[i / LB], gbase + (i % LB));
+        if (own) zr[i] = v;
+      }
+      if (own) {
+        Gh = gh;
+        Gl = gl;
+        jown = jb;
+      }
+      jlast = jb;
+    }
+    // newest incomplete block: sources s = base + sl + LB q, term by term
+    const int base = sb & ~(kBlk - 1);
+    R xe[4][Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int s = base + sl + LB * q;
+      const R2 r = rg[s & KTm];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xe[i][q] = Mth<R>::ninf();
+        if (i < nt && s <= sb + i) xe[i][q] = (r.x + eh[i]) + (r.y + el[i]) + bx[ub + i - s - kc - 1];
+      }
+    }
+    // complete block owned by this sub-lane: 4 x 32 FMAs against one window of w
+    R pb[4] = {0, 0, 0, 0};
+    bool have = false;
+    if (jown >= 0 && Gh != Mth<R>::ninf()) {
+      const int d0 = ub - jown * kBlk;  // duration of the block's source 0 for target ub
+      const int wb = d0 - (kBlk - 1);   // window start: durations wb .. wb+34
+      if (wb <= K) {
+        have = true;
+        const int m = wb & 1;
+        const R* wc = wt + (size_t)m * WSZ;
+        const int e0 = wb + m;
+        const int r0 = e0 >> 5, c0 = e0 & 31;
+        R wv[kBlk + 4];
+#pragma unroll
+        for (int t2 = 0; t2 < (kBlk + 4) / 2; ++t2) {
+          const int cc = c0 + 2 * t2;
+          const int ph = r0 * 34 + cc + (cc >= 32 ? 2 : 0) + (cc >= 64 ? 2 : 0);
+          const auto w2 = *(const typename Vec2<R>::T*)(wc + ph);
+          wv[2 * t2] = w2.x;
+          wv[2 * t2 + 1] = w2.y;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kBlk; ++jj) {
+          const R zz = zr[jj];
+          pb[0] += zz * wv[31 - jj];
+          pb[1] += zz * wv[32 - jj];
+          pb[2] += zz * wv[33 - jj];
+          pb[3] += zz * wv[34 - jj];
+        }
+      }
+    }
+    // shared reference per target: the exact term of its newest source or the newest complete
+    // block's value, whichever is larger; exact group maximum when a term would overflow it
+    R Mv[4], Sv[4], xbv[4], xm[4];
+    const int jnew = (sb >> 5) - 1;
+    bool slow = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      xbv[i] = (have && pb[i] > (R)0) ? ((Gh + eh[i]) + (Gl + el[i])) + bmax : Mth<R>::ninf();
+      xm[i] = xbv[i];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) xm[i] = fmax(xm[i], xe[i][q]);
+      const int ii = (sb & (kBlk - 1)) + i;  // index of source sb + i in the incomplete block (<= 31)
+      R mine = Mth<R>::ninf();
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (ii / LB == q) mine = xe[i][q];
+      const R rx = __shfl_sync(0xffffffffu, mine, gbase + (ii % LB));
+      const R rb = __shfl_sync(0xffffffffu, xbv[i], gbase + (jnew & (LB - 1)));
+      const R M = fmax(rx, rb);
+      Mv[i] = M;
+      slow |= (xm[i] > M + (R)kSlack) || (M == Mth<R>::ninf() && xm[i] != Mth<R>::ninf());
+    }
+    if (__any_sync(0xffffffffu, slow)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        R v = xm[i];
+#pragma unroll
+        for (int o = LB / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        Mv[i] = v;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const R M = Mv[i];
+      R sm = 0;
+      if (M != Mth<R>::ninf()) {
+        if (xbv[i] != Mth<R>::ninf()) sm += pb[i] * Mth<R>::ex2(xbv[i] - M);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (xe[i][q] != Mth<R>::ninf()) sm += Mth<R>::ex2(xe[i][q] - M);
+      }
+      Sv[i] = sm;
+    }
+#pragma unroll
+    for (int o = LB / 2; o > 0; o >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Sv[i] += __shfl_xor_sync(0xffffffffu, Sv[i], o);
+    }
+    {
+      R mi = Mv[0], si = Sv[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i)
+        if (sl == i) {
+          mi = Mv[i];
+          si = Sv[i];
+        }
+      if (lact && sl < nt) {
+        const int slt = (sb + sl) & (kSlots - 1);
+        const uint32_t off = (uint32_t)(((size_t)slt * C + lo + cl) * 2 * sizeof(R));
+        st_async_pair<R>(hpart + off, mi, si, hbar + (uint32_t)(slt * sizeof(uint64_t)));
+      }
+      if (lact && sl < 4 && ub + 4 * nahead + sl <= L) stage(ub + 4 * nahead + sl);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+}
+
 template <typename R>
 __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                           const TailLayout& TL) {
@@ -1816,7 +2065,7 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   R* B2 = (R*)(smem + TL.B2);
   uint64_t* tbar = (uint64_t*)(smem + TL.tbar);
   if (g.TBlk) {
-    const int WLEN = blk_wlen(g.kc);
+    const int WLEN = blk_wlen(g.kc, K);
     R* bx = (R*)(smem + TL.bx);
     R* wt = (R*)(smem + TL.wtab);
     for (int cl = tid; cl < Cg; cl += blockDim.x) {  // per-label max duration bias and near-duration table
@@ -1829,7 +2078,7 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
       }
     }
     __syncthreads();
-    const int WSZ = blk_wsize(g.kc);
+    const int WSZ = blk_wsize(g.kc, K);
     for (int i = tid; i < Cg * 2 * WLEN; i += blockDim.x) {
       const int cl = i / (2 * WLEN), r = i % (2 * WLEN), m = r / WLEN, y = r % WLEN;
       const int k = y - m;  // copy m holds w[y - m]
@@ -1855,7 +2104,11 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   __syncthreads();
   cluster_sync_all();
   if ((tid >> 5) < g.NWt) {
-    if (g.TBlk)
+    if (g.TBlk == 8)
+      tail_loop_blocked_ml<R, 8>(a, x, smem, HL, TL, lo, Cg);
+    else if (g.TBlk == 16)
+      tail_loop_blocked_ml<R, 16>(a, x, smem, HL, TL, lo, Cg);
+    else if (g.TBlk)
       tail_loop_blocked<R>(a, x, smem, HL, TL, lo, Cg);
     else
       tail_loop<R>(a, x, smem, HL, TL, lo, Cg);
