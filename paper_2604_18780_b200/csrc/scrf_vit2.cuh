@@ -59,8 +59,14 @@ __host__ __device__ inline int v2_tail_lo(int rank, int C, int G) { return (int)
 __host__ __device__ inline size_t v2_a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct V2Head {
-  size_t hg, hs, hS, hP, ha, Tm, vsm, part, tbar, total;
+  size_t hg, hs, hP, hS, ha, Tm, vsm, part, tbar, gpb, gpa, total;
 };
+// warps sharing the head's gamma (every warp of the head CTA) and whether they are more than
+// the label warps
+__host__ __device__ inline int v2_gamma_warps(const V2Geo& g) { return g.NT / 32; }
+// (worth its two extra barriers per position only when each label scans many c': measured
+// c5 (C = 128) 188.8 -> 132.2 ms, c4 (C = 24) 192.4 -> 198.8 ms, c3 (C = 39) unchanged)
+__host__ __device__ inline bool v2_par_gamma(const V2Geo& g) { return g.G > 1 && g.NCW >= 3 && g.NT / 32 > g.NCW; }
 __host__ __device__ inline V2Head v2_head_layout(int C, const V2Geo& g, bool has_ps) {
   V2Head L;
   size_t o = 0;
@@ -74,6 +80,9 @@ __host__ __device__ inline V2Head v2_head_layout(int C, const V2Geo& g, bool has
   L.vsm = o;  o += v2_a16((size_t)2 * C * 8);
   L.part = o; o += g.G > 1 ? v2_a16((size_t)g.R * C * 16) : 0;
   L.tbar = o; o += v2_a16((size_t)g.R * 8);
+  const size_t NPG = v2_par_gamma(g) ? (size_t)v2_gamma_warps(g) * g.NCW * 32 : 0;
+  L.gpb = o;  o += v2_a16(NPG * 16);  // per (gamma warp, label): best and sec of its c' range
+  L.gpa = o;  o += v2_a16(NPG * 4);   // and its first argmax
   L.total = o;
   return L;
 }
@@ -160,7 +169,44 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
   }
   __syncthreads();
   if (tails) cluster_sync_all();
-  if (tid >= NH) return;
+  // gamma over c' split across every warp of the head CTA: warp w scans c' in its range for
+  // every label, then the label lanes join the ranges in order (the sequential scan's result
+  // exactly: a later range wins only with a strictly larger value; its sec is the larger of
+  // the earlier ranges' best and its own)
+  const bool par = v2_par_gamma(g);
+  const int GH = v2_gamma_warps(g), NPG = GH * 32;
+  double2* gpb = (double2*)(smem + HL.gpb);
+  int* gpa = (int*)(smem + HL.gpa);
+  auto gamma_part = [&](int t) {
+    const double* v = vsm + (t & 1) * C;
+    const int w = tid >> 5, lane = tid & 31;
+    const int CH = (C + GH - 1) / GH, c0 = w * CH, c1 = min(C, c0 + CH);
+    for (int cw = 0; cw < g.NCW; ++cw) {
+      const int lc = cw * 32 + lane;
+      const int lcs = lc < C ? lc : 0;
+      double best = -CUDART_INF, sec = -CUDART_INF;
+      int arg = c0;
+      for (int cp = c0; cp < c1; ++cp) {
+        const double x = __dadd_rn(v[cp], Tm[(size_t)cp * C + lcs]);
+        if (x > best) {
+          sec = best;
+          best = x;
+          arg = cp;
+        }
+      }
+      gpb[(size_t)w * NH + lc] = make_double2(best, sec);
+      gpa[(size_t)w * NH + lc] = arg;
+    }
+  };
+  if (tid >= NH) {
+    if (!par) return;
+    for (int t = 0; t <= L; ++t) {  // helper warps: the gamma ranges of every position
+      asm volatile("bar.sync 2, %0;" ::"r"(NPG) : "memory");
+      gamma_part(t);
+      asm volatile("bar.sync 3, %0;" ::"r"(NPG) : "memory");
+    }
+    return;
+  }
 
   const int c = tid;
   const bool act = c < C;
@@ -194,6 +240,22 @@ __device__ void v2_head(const V2Args& a, unsigned char* smem, const V2Tail& TL, 
     const double* v = vsm + (t & 1) * C;
     double best = -CUDART_INF, sec = -CUDART_INF;
     int arg = 0;
+    if (par) {
+      asm volatile("bar.sync 2, %0;" ::"r"(NPG) : "memory");
+      gamma_part(t);
+      asm volatile("bar.sync 3, %0;" ::"r"(NPG) : "memory");
+      best = gpb[c].x;
+      sec = gpb[c].y;
+      arg = gpa[c];
+      for (int w = 1; w < GH; ++w) {
+        const double2 pv = gpb[(size_t)w * NH + c];
+        if (pv.x > best) {
+          sec = best > pv.y ? best : pv.y;
+          best = pv.x;
+          arg = gpa[(size_t)w * NH + c];
+        }
+      }
+    } else
     for (int c0 = 0; c0 < C; c0 += 8) {  // 8 independent loads + adds, then the ordered scan
       double x[8];
 #pragma unroll
