@@ -282,7 +282,7 @@ __global__ void post_carry_kernel(const int64_t* lengths, int B, int T, int C, i
 // one pair per 16 so lanes kGBJ pairs apart hit distinct banks); terms are
 // (ra_hi + rb_hi) + (ra_lo + rb_lo) + B2[k-1], one ex2 each.
 constexpr int kGBSub = 128;
-constexpr int kGBMicro = 4096;  // grad_B partial granularity (sources); a multiple of kGBSub
+constexpr int kGBMicro = 1024;  // grad_B partial granularity (sources); a multiple of kGBSub
 constexpr int kGBJ = 4;
 constexpr int kGBW = 2;  // windows per thread (host keeps CG * ceil(K / kGBJ) <= kGBW * 512)
 __host__ __device__ inline int gb_skew(int ui) { return ui + (ui >> 4); }
