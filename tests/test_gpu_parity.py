@@ -344,6 +344,21 @@ def test_numpy_posterior_streamed_input_matches_device_outputs():
     np.testing.assert_array_equal(marg.position_marginals, bw.position_marginals.cpu().numpy())
 
 
+@pytest.mark.parametrize("C,K,B,T", [(64, 160, 16, 400), (96, 300, 12, 300)])
+def test_multi_label_blocked_tails_fp32_matches_fp64(C, K, B, T):
+    """More than 16 labels per tail CTA (many sequences, large C): the tails run the exp-space
+    blocks with 8 (K=160) or 16 (K=300) lanes per label; fp32 against the fp64 instantiation at
+    the north-star bar in the reference's metric."""
+    _, params, cum = scrf.equivalence_instance(7, T=T, K=K, C=C, B=B, mode=CenteringMode.MEAN, ragged=True,
+                                               projections=True)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    f32 = _device_outputs(prob, "fp32")
+    f64 = _device_outputs(prob, "fp64")
+    assert parity.rel_err(f32["logZ"], f64["logZ"]) <= 1e-5
+    for k in ("grad_S", "grad_T", "grad_B", "position_marginals", "boundary_posterior", "expected_segment_count"):
+        assert parity.scaled_err(f32[k], f64[k]) <= 1e-5, k
+
+
 def test_alpha_beta_logz_agree_on_goldens():
     S.set_precision("fp32")
     for name in ["c1rp", "c2", "c3s", "c4s", "c5s"]:
