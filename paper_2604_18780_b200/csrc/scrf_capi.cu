@@ -438,7 +438,9 @@ WLayout w_layout(const scrf_problem* p, int64_t delta, int prec, int G) {
   L.g = sparse_geo(p, delta);
   L.Pw = win_par(p, G, L.g.nWin);
   const size_t rb = B * (size_t)L.g.rowsBeta;
-  const size_t rw = (size_t)L.Pw * B * L.g.rowsWin;
+  // two sets of window rows: the posterior passes of one replay launch run on a side stream
+  // while the next launch replays into the other set (run_sparse_post)
+  const size_t rw = (size_t)2 * L.Pw * B * L.g.rowsWin;
   size_t o = 0;
   L.bY = o;    o += al((rb ? rb : 1) * C * rs);
   L.bn = o;    o += al((rb ? rb : 1) * 8);
@@ -944,6 +946,7 @@ int prog_writers(int C) { return C <= 32 ? 2 : (C + 31) / 32; }
 struct SideStream {
   cudaStream_t s[2] = {nullptr, nullptr};
   cudaEvent_t fork = nullptr, probe = nullptr, join[2] = {nullptr, nullptr};
+  cudaEvent_t sp_rep[2] = {nullptr, nullptr}, sp_pass[2] = {nullptr, nullptr};  // sublinear passes
 };
 SideStream& side_stream() {
   static SideStream ss[64];
@@ -956,6 +959,8 @@ SideStream& side_stream() {
     for (int i = 0; i < 2; ++i) {
       cudaStreamCreateWithPriority(&x.s[i], cudaStreamNonBlocking, lo);
       cudaEventCreateWithFlags(&x.join[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&x.sp_rep[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&x.sp_pass[i], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.probe, cudaEventDisableTiming);
@@ -1231,8 +1236,27 @@ int run_sparse_post(const scrf_problem* p, int64_t delta, const void* ckpt, cons
   SweepTask* tasks = (SweepTask*)(wb + WL.tasks);
   rc = pass_begin(p, wb, WL.P, st);
   if (rc) return rc;
-  for (int j0 = 0; j0 < g.nWin; j0 += WL.Pw) {
+  // replay launch i writes window-row set i & 1 on st; its passes run in order on side stream 0
+  // (after the launch) while launch i + 1 replays into the other set; launch i + 2 waits for
+  // the passes of launch i (set reuse). SCRF_SPARSE_OVL=0: everything on st.
+  const bool ovl = env_int("SCRF_SPARSE_OVL", 1) != 0;
+  if (ovl) preload_concurrent_kernels();
+  SideStream* ss = ovl ? &side_stream() : nullptr;
+  cudaStream_t sp = ovl ? ss->s[0] : st;
+  if (ovl) {
+    cudaError_t e = cudaEventRecord(ss->fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, ss->fork, 0);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const size_t setrows = (size_t)WL.Pw * wstride;  // rows of one window-row set
+  for (int j0 = 0, bi = 0; j0 < g.nWin; j0 += WL.Pw, ++bi) {
     const int P = g.nWin - j0 < WL.Pw ? g.nWin - j0 : WL.Pw;
+    const int set = bi & 1;
+    const size_t so = set * setrows;
+    if (ovl && bi >= 2) {
+      cudaError_t e = cudaStreamWaitEvent(st, ss->sp_pass[set], 0);
+      if (e != cudaSuccess) return (int)e;
+    }
     ++g_launches;
     build_tasks_kernel<<<(2 * B * P + 127) / 128, 128, 0, st>>>(p->lengths, N, B, T, K, (int)delta,
                                                                 (int)n_ckpt_of(p->T, delta), g.mA, g.W, g.nW,
@@ -1242,23 +1266,28 @@ int run_sparse_post(const scrf_problem* p, int64_t delta, const void* ckpt, cons
     io.dirs = 3;
     io.tasks = tasks;
     io.ntasks = 2 * B * P;
-    io.Y[0] = wb + WL.aY;
-    io.X[0] = wb + WL.aX;
-    io.n[0] = (double*)(wb + WL.an);
-    io.Y[1] = wb + WL.wY;
-    io.X[1] = wb + WL.wX;
-    io.n[1] = (double*)(wb + WL.wn);
+    io.Y[0] = wb + WL.aY + so * C * rs;
+    io.X[0] = wb + WL.aX + so * C * rs;
+    io.n[0] = (double*)(wb + WL.an) + so;
+    io.Y[1] = wb + WL.wY + so * C * rs;
+    io.X[1] = wb + WL.wX + so * C * rs;
+    io.n[1] = (double*)(wb + WL.wn) + so;
     io.fY[0] = cb + SL.Y;
     io.fN[0] = (const double*)(cb + SL.n);
     io.fY[1] = wb + WL.bY;
     io.fN[1] = (const double*)(wb + WL.bn);
     rc = run_sweep<R>(p, delta, io, st);
     if (rc) return rc;
+    if (ovl) {
+      cudaError_t e = cudaEventRecord(ss->sp_rep[set], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, ss->sp_rep[set], 0);
+      if (e != cudaSuccess) return (int)e;
+    }
     for (int wi = 0; wi < P; ++wi) {
       const int j = j0 + wi;
       const int w0 = j * g.W, w1 = (j + 1) * g.W < T + 1 ? (j + 1) * g.W : T + 1;
       MsgView m;
-      const size_t ro = (size_t)wi * wstride;
+      const size_t ro = so + (size_t)wi * wstride;
       m.Ya = wb + WL.aY + ro * C * rs;
       m.Xa = wb + WL.aX + ro * C * rs;
       m.na = (const double*)(wb + WL.an) + ro;
@@ -1268,9 +1297,18 @@ int run_sparse_post(const scrf_problem* p, int64_t delta, const void* ckpt, cons
       m.rowsA = m.rowsB = g.rowsWin;
       m.tA0 = j == 0 ? 0 : ((w0 - K + 1) & ~31);
       m.tB0 = w0;
-      rc = run_pass<R>(p, m, w0, w1, out, wb, WL.P, j == g.nWin - 1, st);
+      rc = run_pass<R>(p, m, w0, w1, out, wb, WL.P, j == g.nWin - 1, sp);
       if (rc) return rc;
     }
+    if (ovl) {
+      cudaError_t e = cudaEventRecord(ss->sp_pass[set], sp);
+      if (e != cudaSuccess) return (int)e;
+    }
+  }
+  if (ovl) {
+    cudaError_t e = cudaEventRecord(ss->join[0], sp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ss->join[0], 0);
+    if (e != cudaSuccess) return (int)e;
   }
   return pass_finish(p, wb, WL.P, out, st);
 }
