@@ -130,7 +130,16 @@ struct SweepGeo {
   int CgMax;  // max labels per tail
   int NT;     // block size (max over roles)
   int Msm;    // exp-space transition matrix staged in shared memory
+  unsigned long long wperm;  // head warp placement: 4 bits per physical warp = the role (logical
+                             // warp) it runs; 0 = identity (SMSP of a warp = its index mod 4)
 };
+
+// logical head thread index of this thread (role layout is defined on logical warps)
+__device__ __forceinline__ int head_ltid(const SweepGeo& g) {
+  const int w = threadIdx.x >> 5;
+  const int lw = g.wperm ? (int)((g.wperm >> (4 * w)) & 15) : w;
+  return (lw << 5) | (threadIdx.x & 31);
+}
 
 // One window replay (sublinear-memory mode, streaming.py:232-261 recompute_alpha and its beta
 // twin): a sweep over local positions p = 0 .. steps with absolute position t = t0 + p (alpha)
@@ -848,6 +857,10 @@ __device__ __forceinline__ R lse5(R m, R s, R x4, R x3, R x2, R x1) {
   return M + Mth<R>::lg2(sum);
 }
 
+// the reference's guard in the reference frame (rare: only reachable with a max shift below -1e8);
+// out of line so that its fp64 arithmetic is not if-converted onto the chain's critical path
+__device__ __noinline__ bool guard_dead(double n_prev, double am, double n_ref) { return (n_prev + am) - n_ref <= kGuardL2; }
+
 // exact log-space transition pass (rare: underflowing exp-space sums)
 template <typename R>
 __device__ __noinline__ R gemv_exact(const double* trans, int dir, int C, int NCW, R* ew, R yh, bool act, int c, bool slow,
@@ -1056,7 +1069,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
       // streaming.py:194-214; beta: absolute, streaming.py:316-355) is masked, i.e. -inf here
       dead = (am == Mth<R>::ninf());
       // (a max shift below -1e8 is the only way to reach the 1e9-wide guard: exact test only then)
-      if (am < (R)-1e8) dead = dead || (n_prev + (double)am) - n_ref <= kGuardL2;
+      if (am < (R)-1e8) dead = dead || guard_dead(n_prev, (double)am, n_ref);
       yh = dead ? Mth<R>::ninf() : y - am;
       n_p = dead ? n_prev : n_prev + (double)am;
     }
@@ -1123,7 +1136,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& 
   const SweepGeo& g = a.geo;
   const int C = a.C, L = x.L;
   const int kc = g.kc, KRm = g.KRm;
-  const int ntid = threadIdx.x - g.NCW * 32;
+  const int ntid = head_ltid(g) - g.NCW * 32;
   const int NG = g.NG;
   const int ngw = g.NNW / NG;          // warps per group
   const int gi = (ntid >> 5) / ngw;    // group
@@ -1236,7 +1249,7 @@ __device__ void head_src(const SweepArgs<R>& a, const SweepCtx& x, unsigned char
   const SweepGeo& g = a.geo;
   const int C = a.C, T = a.T, L = x.L;
   const int KRm = g.KRm, KTm = g.KTm;
-  const int c = threadIdx.x - wbase * 32;  // label
+  const int c = head_ltid(g) - wbase * 32;  // label
   const bool act = c < C;
   const int cs = act ? c : 0;
   const R* pXc = h.pubX + cs;
@@ -1329,7 +1342,7 @@ template <typename R, int MODE>
 __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
   const SweepGeo& g = a.geo;
   const int C = a.C, T = a.T, L = x.L;
-  const int c = threadIdx.x - wbase * 32;
+  const int c = head_ltid(g) - wbase * 32;
   const bool act = c < C;
   const int cs = act ? c : 0;
   const R* b2c = h.B2 + (size_t)cs * b2_stride(g.kc);
@@ -1352,7 +1365,7 @@ __device__ void head_edge_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr
 template <typename R, int MODE>
 __device__ void head_out_role(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int wbase) {
   const int C = a.C, L = x.L;
-  const int c = threadIdx.x - wbase * 32;
+  const int c = head_ltid(a.geo) - wbase * 32;
   const bool act = c < C;
   int* pslot = (a.prog && !x.task) ? a.prog + (size_t)(x.b * 2 + x.dir) * kProgSlots : nullptr;
   for (int q = 0; q <= L; q += 4) {
@@ -1369,7 +1382,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
   const int K = a.K, C = a.C, T = a.T, L = x.L;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = head_ltid(a.geo) >> 5;
   const int NAUX = g.NAS * g.NCW;                            // source (+ edge) warps
   const int NA = (2 * g.NCW + g.NNW / g.NG) * 32;            // chain + source + one near group
   const int NB = (g.NCW + g.NNW / g.NG) * 32;                // chain + one near group
