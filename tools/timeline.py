@@ -50,8 +50,8 @@ for e in ev:
     a[2] += ov
     a[3] = e.get("args", {}).get("stream")
     a[4] += 1 if e["ts"] < s1 else 0
-tot = sum(a[1] for a in agg.values())
-tov = sum(a[2] for a in agg.values())
+tot = sum(a[1] for k, a in agg.items() if k != "prog_wait_kernel")  # the spin-wait gates are not work
+tov = sum(a[2] for k, a in agg.items() if k != "prog_wait_kernel")
 lines.append(f"{'kernel':28s} {'launches':>8s} {'busy us':>10s} {'under sweep us':>15s} {'started under sweep':>20s}")
 for k, a in agg.items():
     lines.append(f"{k:28s} {a[0]:8d} {a[1]:10.1f} {a[2]:15.1f} {a[4]:20d}")
