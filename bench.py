@@ -438,7 +438,18 @@ def extras_measure(ctx, args):
     B, T = prob.B, prob.T
     res = {}
     res["forward_positions_per_s"] = B * T / (_time_device(torch, lambda: S.device_forward(prob, sparse=True)) / 1e3)
-    res["viterbi_positions_per_s"] = B * T / (_time_device(torch, lambda: S.device_viterbi(prob)) / 1e3)
+    vit_ms = _time_device(torch, lambda: S.device_viterbi(prob))
+    res["viterbi_positions_per_s"] = B * T / (vit_ms / 1e3)
+    # Viterbi against the fp64 add pipe: (K*C + C^2) max-plus candidates per position (one fp64
+    # add + one fp64 compare each, exact fp64 with the reference's tie rules); peak = measured
+    # add.f64 rate (profiles/r01_microbench.jsonl: 18.1 T/s at 1965 MHz)
+    K, C = prob.K, prob.C
+    cand = float(B * T) * (K * C + C * C)
+    res["viterbi_roofline"] = {"bound": "latency (one dependent max-plus step per position; head issue-bound)",
+                               "pipe": "fp64", "achieved": cand / (vit_ms / 1e3) / 1e9, "peak": 18100.0,
+                               "unit": "G fp64 add/s", "frac": cand / (vit_ms / 1e3) / 1e9 / 18100.0,
+                               "peak_source": "profiles/r01_microbench.jsonl (add.f64, measured)",
+                               "kernel_ms": vit_ms}
     modes = {}
     for mode in ("full", "sublinear"):
         torch.cuda.synchronize()

@@ -916,6 +916,18 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
 #pragma unroll
     for (int y = 0; y < 32; ++y) Mreg[y] = (act && y < C) ? Mval(y) : (R)0;
   }
+  // The exp-space GEMV sum of label x is >= M[y*][x] (the frame's maximal label y* has Y^ = 0
+  // exactly), so when every column's smallest factor is >= 2^-90 the sum can never fall below
+  // the 1e-30 fallback threshold (a dead position sums to 0 and gives -inf on both paths): the
+  // per-step vote for the exact path is then skipped (C <= 32; the outcome is unchanged).
+  bool may_underflow = true;
+  if (CW1) {
+    R mn = (R)1;
+#pragma unroll
+    for (int y = 0; y < 32; ++y)
+      if (y < C) mn = fmin(mn, Mreg[y]);
+    may_underflow = __any_sync(0xffffffffu, act && !(mn >= (R)8.077935669463161e-28));  // 2^-90
+  }
   const R xmax = act ? h.Xmax[c] : (R)0;
   // X^[x] = xmax[x] + log2 sum_y 2^(yh[y]) M[y][x]
   auto gemv = [&](R yh) -> R {
@@ -967,7 +979,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
     const R sum = (s0 + s1) + (s2 + s3);
     R out = xmax + Mth<R>::lg2(sum);
     const bool slow = act && !(sum >= (R)1e-30);
-    if (__any_sync(0xffffffffu, slow)) out = gemv_exact<R>(a.trans, x.dir, C, g.NCW, h.ew, yh, act, c, slow, out);
+    if (may_underflow && __any_sync(0xffffffffu, slow)) out = gemv_exact<R>(a.trans, x.dir, C, g.NCW, h.ew, yh, act, c, slow, out);
     return out;
   };
   auto chain_max = [&](R y) -> R {
