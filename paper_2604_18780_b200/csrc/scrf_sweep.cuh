@@ -902,7 +902,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
   const int C = a.C, L = x.L;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = head_ltid(g), warp = tid >> 5, lane = tid & 31;  // logical (placement-independent)
   const int c = warp * 32 + lane;
   const bool act = c < C;
   const int nch = g.NCW * 32;

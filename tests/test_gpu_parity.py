@@ -501,3 +501,19 @@ def test_batch_sharding_is_bit_identical(memory):
         assert torch.equal(torch.cat(gS), bw.grad_S), world
         assert torch.equal(rT, bw.grad_T), world
         assert torch.equal(rB, bw.grad_B), world
+
+
+@pytest.mark.parametrize("perm", ["01234567", "01236574", "76543210"])
+def test_head_warp_placement_is_bit_identical(monkeypatch, perm):
+    """The head CTA's roles may be placed on any physical warps (SCRF_WPERM; the default for the
+    8-warp head puts the output warp beside the chain): placement changes timing only, so the
+    posterior (both sweeps, tails, overlapped passes) is bit-identical to the default placement.
+    Config-4 shape (K = 1000, C = 24: head + tails clusters, 8-warp head)."""
+    _, params, cum = scrf.equivalence_instance(5, T=3000, K=1000, C=24, B=2, mode=CenteringMode.MEAN, ragged=True)
+    prob = scrf.DeviceProblem.from_host(cum, params)
+    monkeypatch.delenv("SCRF_WPERM", raising=False)
+    ref = _device_outputs(prob, "fp32")
+    monkeypatch.setenv("SCRF_WPERM", perm)
+    got = _device_outputs(prob, "fp32")
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
