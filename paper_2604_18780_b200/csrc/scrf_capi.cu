@@ -39,7 +39,7 @@ int env_int(const char* name, int dflt) {
 
 // SCRF_WPERM=<hex digits>: digit i = the head role (logical warp) physical warp i runs
 // (placement experiment: which roles share an SM sub-partition); must be a permutation
-unsigned long long head_wperm(int nwarps, bool one_chain) {
+unsigned long long head_wperm(int nwarps, int ncw, bool one_chain) {
   const char* v = getenv("SCRF_WPERM");
   // default for the 8-warp head (chain, 4 near groups, source, edge, output): the output warp on
   // the chain's sub-partition and the last near group beside the third (c4: sweep -2.5 %,
@@ -51,6 +51,7 @@ unsigned long long head_wperm(int nwarps, bool one_chain) {
   for (int i = 0; i < nwarps; ++i) {
     const int d = (v[i] >= 'a') ? v[i] - 'a' + 10 : v[i] - '0';
     if (d < 0 || d >= nwarps || (seen >> d) & 1) return 0;
+    if (i < ncw && d != i) return 0;  // the chain warps stay on warps 0 .. NCW-1
     seen |= 1 << d;
     m |= (unsigned long long)d << (4 * i);
   }
@@ -186,7 +187,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
     g.NT = (g.NCW + g.NAS * g.NCW + g.NNW + g.NOW) * 32;
     size_t sm = prec ? sweep_smem_bytes<double>(K, C, g) : sweep_smem_bytes<float>(K, C, g);
     if (g.NNW <= g.NG * maxg && sm <= limit) {
-      g.wperm = head_wperm(g.NCW + g.NAS * g.NCW + g.NNW + g.NOW, g.NCW == 1 && g.NOW == 1);
+      g.wperm = head_wperm(g.NCW + g.NAS * g.NCW + g.NNW + g.NOW, g.NCW, g.NCW == 1 && g.NOW == 1);
       *out = g;
       return SCRF_OK;
     }
@@ -248,7 +249,7 @@ int choose_sweep_geo(int B, int K, int C, int prec, int ndirs, bool has_ps, bool
     }
   }
   if (!found) return SCRF_ECONFIG;
-  g.wperm = head_wperm(g.NCW + g.NAS * g.NCW + g.NNW + g.NOW, g.NCW == 1 && g.NOW == 1);
+  g.wperm = head_wperm(g.NCW + g.NAS * g.NCW + g.NNW + g.NOW, g.NCW, g.NCW == 1 && g.NOW == 1);
   *out = g;
   return SCRF_OK;
 }

@@ -902,7 +902,9 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
   const int C = a.C, L = x.L;
-  const int tid = head_ltid(g), warp = tid >> 5, lane = tid & 31;  // logical (placement-independent)
+  // physical thread index: the chain warps never move (head_wperm keeps warps 0 .. NCW-1 in
+  // place; a logical index here costs ~1.5 % of the step in re-materialised address math)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int c = warp * 32 + lane;
   const bool act = c < C;
   const int nch = g.NCW * 32;
