@@ -628,6 +628,7 @@ def _fill_pinned(out: torch.Tensor, t: torch.Tensor) -> None:
 
 
 _GATE_SHIFT = 12  # 4096-row chunks of S
+_EARLY_CHUNKS = int(os.environ.get("SCRF_EARLY_CHUNKS", "4"))  # chunks queued before the kernels are launched (two per sweep direction)
 _PIN_KEEP = []    # pinned staging buffers of streamed uploads still in flight
 
 
@@ -658,10 +659,12 @@ def _prime_streaming(dev) -> None:
 
 
 def _stream_S(prob: DeviceProblem, S_host, gate: torch.Tensor, shift: int, gate_ready: torch.cuda.Event,
-              pin: torch.Tensor) -> None:
+              pin: torch.Tensor, part: slice = slice(None), last: bool = True) -> None:
     """Copy S to prob.S chunk by chunk on the copy stream -- chunks from both ends inward, the
     order the alpha and beta sweeps consume them -- marking each chunk's gate after its copy.
-    The current stream then waits for the last copy (later consumers of S)."""
+    `part` selects a slice of that order (the first chunks are queued before the kernels are
+    launched, the rest after); with `last` the current stream then waits for the last copy
+    (later consumers of S)."""
     lib = _lib.load()
     Sh = np.asarray(S_host)
     if Sh.dtype != np.float64 or not Sh.flags.c_contiguous:
@@ -681,12 +684,14 @@ def _stream_S(prob: DeviceProblem, S_host, gate: torch.Tensor, shift: int, gate_
     cs.wait_event(gate_ready)
     row_bytes = Sh.shape[2] * 8
     with torch.cuda.stream(cs):
-        for j in order:
+        for j in order[part]:
             r0, r1 = j * R, min((j + 1) * R, T1)
             pin[:, r0:r1].copy_(St[:, r0:r1])
             # one 2-D copy of the chunk's rows of every sequence, then its gate
             _lib.check(lib.scrf_upload_rows(_lib.ptr(prob.S), _lib.ptr(pin), B, T1, row_bytes, r0, r1,
                                             _lib.ptr(gate), j, _lib.stream_handle()), "scrf_upload_rows")
+    if not last:
+        return
     # keep the pinned staging alive until its copies have run (torch's host allocator only
     # tracks copies it issued itself)
     done = torch.cuda.Event()
@@ -834,6 +839,10 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         # pinned staging allocated before the launch: nothing that could wait for the device
         # may run on this thread between the launch and the last chunk mark
         pin = torch.empty(prob.S.shape, dtype=torch.float64, pin_memory=True)
+        # the first row chunks of both sweeps go out before the launch: the launch sequence of the
+        # overlapped passes takes ~1 ms of host time, during which the sweeps would otherwise
+        # wait on their first gates
+        _stream_S(prob, cum.S, gate, shift, gate_ready, pin, part=slice(0, _EARLY_CHUNKS), last=False)
     else:
         prob = shape_only
         Sh = torch.from_numpy(np.ascontiguousarray(cum.S, dtype=np.float64))
@@ -858,7 +867,7 @@ def posterior(cum, params, delta=None, upstream=None, *, ledger=None, stats=None
         if streamed:
             lib.scrf_input_gate(None, 0, 0)
     if streamed:
-        _stream_S(prob, cum.S, gate, shift, gate_ready, pin)
+        _stream_S(prob, cum.S, gate, shift, gate_ready, pin, part=slice(_EARLY_CHUNKS, None))
     side = _side_stream()
     dev_outs = (bw.grad_S, bw.grad_P_start, bw.grad_P_end, bw.position_marginals, bw.boundary_posterior)
     if plan:
