@@ -1475,7 +1475,10 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
 // ----------------------------------------------------------------------------
 // tail CTA: durations kc+1..K of a label slice (one warp per label), ahead of the chain
 
-template <typename R>
+// GATE: streamed input (MODE 3): the tails check the input gates before staging new rows. A
+// template parameter so that the other modes carry no gate code (their tail loops are measurably
+// faster without it: c4 MODE 0 sweep 33.8 -> 33.4 ms)
+template <typename R, bool GATE>
 __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                           const TailLayout& TL, int lo, int Cg) {
   using R2 = typename Vec2<R>::T;
@@ -1493,7 +1496,7 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   const int WPL_ = g.WPL, lstep_ = g.NWt / WPL_, cl0_ = warp / WPL_;
   int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
   auto stage = [&](int u, int cl) {
-    if (a.gate && u >= gnext) {
+    if (GATE && u >= gnext) {
       gate_span_wait(a, x, u, min(u + 512, x.L));
       gnext = u + 256;
     }
@@ -1573,7 +1576,7 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
 // four (one window load of 35 w values feeds 4 x 32 FMAs); the newest, incomplete block is
 // summed term by term. Each target's partial is in the frame n_{u-kc-1} of its newest
 // source. Needs kc + 32 <= K <= 1024 + kc.
-template <typename R>
+template <typename R, bool GATE>
 __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                                   const TailLayout& TL, int lo, int Cg) {
   using R2 = typename Vec2<R>::T;
@@ -1595,7 +1598,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
   const R bmax = bx[kBlk];
   int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
   auto stage = [&](int u) {
-    if (a.gate && u >= gnext) {
+    if (GATE && u >= gnext) {
       gate_span_wait(a, x, u, min(u + 512, x.L));
       gnext = u + 256;
     }
@@ -1841,7 +1844,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
 // (block j in sub-lane j % LB), and the newest, incomplete block's 32 sources are spread over
 // the group, 32 / LB per lane. Lets the exp-space tails serve 43-label slices (config 5: C = 128
 // over 3 tails, where one label per warp would need 43 warps).
-template <typename R, int LB>
+template <typename R, int LB, bool GATE>
 __device__ void tail_loop_blocked_ml(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem,
                                      const HeadLayout& HL, const TailLayout& TL, int lo, int Cg) {
   using R2 = typename Vec2<R>::T;
@@ -1864,7 +1867,7 @@ __device__ void tail_loop_blocked_ml(const SweepArgs<R>& a, const SweepCtx& x, u
   const R bmax = bx[kBlk];
   int gnext = 0;  // streamed input: rows below local position gnext are known to be on the device
   auto stage = [&](int u) {
-    if (a.gate && u >= gnext) {
+    if (GATE && u >= gnext) {
       gate_span_wait(a, x, u, min(u + 512, x.L));
       gnext = u + 256;
     }
@@ -2082,7 +2085,7 @@ __device__ void tail_loop_blocked_ml(const SweepArgs<R>& a, const SweepCtx& x, u
   cp_async_wait<0>();
 }
 
-template <typename R>
+template <typename R, int MODE>
 __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned char* smem, const HeadLayout& HL,
                           const TailLayout& TL) {
   const SweepGeo& g = a.geo;
@@ -2132,13 +2135,13 @@ __device__ void tail_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   cluster_sync_all();
   if ((tid >> 5) < g.NWt) {
     if (g.TBlk == 8)
-      tail_loop_blocked_ml<R, 8>(a, x, smem, HL, TL, lo, Cg);
+      tail_loop_blocked_ml<R, 8, MODE == 3>(a, x, smem, HL, TL, lo, Cg);
     else if (g.TBlk == 16)
-      tail_loop_blocked_ml<R, 16>(a, x, smem, HL, TL, lo, Cg);
+      tail_loop_blocked_ml<R, 16, MODE == 3>(a, x, smem, HL, TL, lo, Cg);
     else if (g.TBlk)
-      tail_loop_blocked<R>(a, x, smem, HL, TL, lo, Cg);
+      tail_loop_blocked<R, MODE == 3>(a, x, smem, HL, TL, lo, Cg);
     else
-      tail_loop<R>(a, x, smem, HL, TL, lo, Cg);
+      tail_loop<R, MODE == 3>(a, x, smem, HL, TL, lo, Cg);
   }
 }
 
@@ -2207,7 +2210,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(SweepArgs<R> a) {
   if (x.rank == 0)
     head_main<R, TAILS, CW1, MODE>(a, x, smem, HL, TL);
   else if (TAILS)
-    tail_main<R>(a, x, smem, HL, TL);
+    tail_main<R, MODE>(a, x, smem, HL, TL);
   if (TAILS) cluster_sync_all();
 }
 
