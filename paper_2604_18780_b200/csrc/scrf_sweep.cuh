@@ -241,8 +241,23 @@ __device__ __forceinline__ long long gtimer() {
 #endif
 
 // mbarrier wait with an optional watchdog (a.hang != null): after ~1e8 polls record where
-// and trap instead of hanging the device.
-template <typename A>
+// and trap instead of hanging the device. The watchdog is out of line: the hot loops that wait
+// carry only the plain wait (their instruction footprint matters, see the tail GATE note).
+__device__ __noinline__ void sweep_wait_watchdog(int* hang, uint32_t bar, uint32_t parity, int site, int idx) {
+  for (long long i = 0; i < 100000000LL; ++i)
+    if (mbar_try(bar, parity)) return;
+  if (atomicCAS(hang, 0, 1) == 0) {
+    hang[1] = blockIdx.x;
+    hang[2] = threadIdx.x;
+    hang[3] = site;
+    hang[4] = idx;
+    __threadfence_system();
+  }
+  __trap();
+}
+// OOL: the watchdog path as a call (MODE 3 instantiations: -1.2 ms of sweep at c4) or inline
+// (the other modes measure faster with it inline: instruction layout of their hot loops)
+template <bool OOL, typename A>
 __device__ __forceinline__ void sweep_wait(const A& a, uint32_t bar, uint32_t parity, int site, int idx) {
   if (!a.hang) {
 #ifdef SCRF_EXP_BACKOFF
@@ -252,6 +267,10 @@ __device__ __forceinline__ void sweep_wait(const A& a, uint32_t bar, uint32_t pa
     }
 #endif
     mbar_wait(bar, parity);
+    return;
+  }
+  if (OOL) {
+    sweep_wait_watchdog(a.hang, bar, parity, site, idx);
     return;
   }
   for (long long i = 0; i < 100000000LL; ++i)
@@ -1144,7 +1163,7 @@ __device__ void head_chain(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>&
 // waits A(p-4) and sums durations 5..kc of target p from the source ring (sources <= p-5,
 // written by the source warps) plus the tail partial (durations kc+1..K), in frame n_{p-4};
 // then arrives B(p).
-template <typename R, bool TAILS>
+template <typename R, bool TAILS, int MODE>
 __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& h, int NA, int NAE, int NB) {
   using R2 = typename Vec2<R>::T;
   const SweepGeo& g = a.geo;
@@ -1226,7 +1245,7 @@ __device__ void head_near(const SweepArgs<R>& a, const SweepCtx& x, HeadPtr<R>& 
       const int pi = p - kc - 1;
       const int sl = pi & (kSlots - 1);
       if (tr) tr[5] = clock64();
-      sweep_wait(a, smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1), 1, p);
+      sweep_wait<MODE == 3>(a, smem_u32(&h.tbar[sl]), (uint32_t)((pi / kSlots) & 1), 1, p);
       if (blockIdx.x == 0 && gtid == 0) SCRF_GT(3, p);
       if (tr) tr[6] = clock64();
       if (act && j == 0) {
@@ -1463,7 +1482,7 @@ __device__ void head_main(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
   if (warp < g.NCW)
     head_chain<R, CW1, MODE>(a, x, h, NA, NAE, NB);
   else if (warp < g.NCW + g.NNW)
-    head_near<R, TAILS>(a, x, h, NA, NAE, NB);
+    head_near<R, TAILS, MODE>(a, x, h, NA, NAE, NB);
   else if (warp < 2 * g.NCW + g.NNW)
     head_src<R, TAILS, MODE>(a, x, smem, h, TL, NA, NAE, g.NCW + g.NNW, g.NAS == 1);
   else if (g.NAS == 2 && warp < 3 * g.NCW + g.NNW)
@@ -1534,7 +1553,7 @@ __device__ void tail_loop(const SweepArgs<R>& a, const SweepCtx& x, unsigned cha
     cp_async_wait<kAhead - 1>();
     __syncwarp();
     if (tr) tr[1] = clock64();
-    sweep_wait(a, smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1), 2, u);
+    sweep_wait<GATE>(a, smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)((s_new / kSlots) & 1), 2, u);
     if (tr) tr[2] = clock64();
     if (threadIdx.x == 0 && s_new + kSlots <= L - kc - 1)
       mbar_expect(smem_u32(&tbar[s_new & (kSlots - 1)]), (uint32_t)(Cg * 2 * sizeof(R) + sizeof(double)));
@@ -1664,7 +1683,7 @@ __device__ void tail_loop_blocked(const SweepArgs<R>& a, const SweepCtx& x, unsi
     // them); warp 0 re-arms each slot for its next use
     const int s0 = snext;
     for (int s = s0; s < sb + nt; ++s) {
-      sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
+      sweep_wait<GATE>(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
       if (threadIdx.x == 0 && blockIdx.x == 1) SCRF_GT(1, s);
     }
     snext = sb + nt;
@@ -1901,7 +1920,7 @@ __device__ void tail_loop_blocked_ml(const SweepArgs<R>& a, const SweepCtx& x, u
     cp_async_wait<2>();
     __syncwarp();
     const int s0 = snext;
-    for (int s = s0; s < sb + nt; ++s) sweep_wait(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
+    for (int s = s0; s < sb + nt; ++s) sweep_wait<GATE>(a, smem_u32(&tbar[s & (kSlots - 1)]), (uint32_t)((s / kSlots) & 1), 2, s);
     snext = sb + nt;
     R eh[4], el[4];
     {
